@@ -1,0 +1,329 @@
+#!/usr/bin/env python
+"""Benchmark of the SENSEI finite-volume hot path on B200 (BASELINE.json).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--workload C2|C3|C4]
+
+One bench "step" = one full classical-RK4 time step (4 fused stage kernels:
+limiter + MUSCL + Roe/Harten + residual + update + ghosts, CFL dt and
+residual norms) over the whole grid.  Metric: Mcell-updates/s = cells x
+RK stages x steps / device time (reading A-R21: a cell-update is one cell
+through one RK stage, so Mcell-updates/s = np x ssspnt of Eq. 14).
+
+N = 1 runs BASELINE config C2 (1440 x 720 = 1,036,800 cells, 30-degree
+inlet).  N > 1 (torchrun, one process per GPU, NCCL) runs C2 per GPU as
+weak scaling: global grid (1440 N) x 720 in N slabs along i.
+--workload C3 / C4 select the strong (66.4 M cells) / weak (16.6 M per GPU)
+scaling configurations instead.
+
+--impl reference times the plain CPU oracle (oracle/, test infrastructure)
+as it stands on the host cores, on a bounded sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+from paper_2305_18057_b200 import inputs as I  # noqa: E402
+
+METRIC = "Mcell-updates/s (fp64, device-timed) at 1/2/4/8 B200; % of HBM roofline"
+UNIT = "Mcell-updates/s"
+ALG_BYTES_PER_CELL_STAGE = 120.0  # classical RK4, minimal data flow, node geometry
+L2_BYTES = 126e6
+
+
+def env_int(k, d):
+    try:
+        return int(os.environ.get(k, d))
+    except ValueError:
+        return d
+
+
+def workload(name, n_gpus):
+    """(ni, nj, theta, description, scaling, px) of the global grid."""
+    if name == "C2":
+        ni, nj = 1440 * n_gpus, 720
+        desc = (f"C2 2D supersonic inlet, 30-deg ramp, {1440}x{720} cells per GPU "
+                f"(global {ni}x{nj}), Table 1 freestream, RK4 CFL 0.8, VA limiter, Roe+Harten")
+        return ni, nj, 30.0, desc, "weak", n_gpus
+    if name == "C4":
+        ni, nj = 5760 * n_gpus, 2880
+        return ni, nj, 30.0, f"C4 weak scaling, 5760x2880 per GPU (global {ni}x{nj})", "weak", n_gpus
+    if name == "C3":
+        return 11520, 5760, 30.0, "C3 strong scaling, 11520x5760 = 66,355,200 cells", "strong", n_gpus
+    raise SystemExit(f"unknown workload {name}")
+
+
+class Clocks:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md)."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device):
+        self.device = device
+        self.p = None
+
+    def __enter__(self):
+        try:
+            self.p = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except (OSError, FileNotFoundError):
+            self.p = None
+        return self
+
+    def __exit__(self, *a):
+        self.out = ""
+        if self.p is not None:
+            time.sleep(0.05)
+            self.p.terminate()
+            try:
+                self.out, _ = self.p.communicate(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.p.kill()
+                self.out = ""
+
+    def summary(self):
+        rows = []
+        for line in (self.out or "").strip().splitlines():
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 8:
+                continue
+            try:
+                rows.append((float(f[0]), float(f[1]), f[4], f[5], f[6], f[7]))
+            except ValueError:
+                continue
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for r in rows for k in range(4) if r[2 + k].lower() == "active"})
+        return {"sm_mhz": statistics.median(r[0] for r in rows), "sm_max_mhz": max(r[1] for r in rows),
+                "reasons": reasons, "samples": len(rows)}
+
+
+def load_profile_traffic():
+    p = os.path.join(ROOT, "profiles", "ncu_stage_kernel.json")
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        return d.get("dram_bytes_per_cell_stage"), d
+    except (OSError, ValueError):
+        return None, None
+
+
+def measured_peak():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, copy burst)"
+    except (OSError, ValueError, KeyError):
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def cpu_baseline_oracle(budget_s=15.0, steps_cap=None):
+    """The oracle, as it stands, single-threaded on a bounded sample: the
+    bottom rows of the C2 grid (ramp included) for a few RK4 steps."""
+    import oracle
+    oracle.build()
+    ni = 1440
+    rows = 16
+    X, Y = I.ramp_nodes(ni, rows, 30.0)
+    cfg = I.default_config(ni, rows)
+    o = oracle.Oracle(cfg, X, Y)
+    o.set_state(I.uniform_state(ni, rows))
+    o.step(1)  # warm
+    t0 = time.perf_counter()
+    n = 0
+    while time.perf_counter() - t0 < budget_s and (steps_cap is None or n < steps_cap):
+        o.step(1)
+        n += 1
+    dt = time.perf_counter() - t0
+    v = ni * rows * 4 * n / dt / 1e6
+    return {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle",
+            "sample": f"C2 grid bottom {rows} rows ({ni}x{rows} cells incl. ramp), {n} RK4 steps, "
+                      f"{dt:.1f} s single-threaded -O2 -ffp-contract=off"}
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return
+    import oracle
+    oracle.build()
+    ni, nj, theta, desc, scaling, px = workload(args.workload, args.gpus)
+    ni1 = 1440 if args.workload == "C2" else (5760 if args.workload == "C4" else 11520)
+    # bounded sample: the bottom `rows` rows of one GPU's share, sized so the
+    # whole run stays around a minute of CPU time
+    rows = max(2, min(nj, int(round(60.0 * 2.0e6 / (4.0 * ni1 * (args.steps + args.warmup))))))
+    X, Y = I.ramp_nodes(ni1, rows, theta)
+    cfg = I.default_config(ni1, rows)
+    o = oracle.Oracle(cfg, X, Y)
+    o.set_state(I.uniform_state(ni1, rows))
+    o.step(args.warmup)
+    t0 = time.perf_counter()
+    o.step(args.steps)
+    dt = time.perf_counter() - t0
+    cells = ni1 * rows
+    v = cells * 4 * args.steps / dt / 1e6
+    sample = (f"{ni1}x{rows} bottom rows of the {args.workload} grid per step "
+              f"({cells} cells, ramp included), oracle single-threaded")
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt * 1e3 / max(args.steps, 1),
+            "higher_is_better": True, "scaling": scaling, "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded inputs)",
+            "config": {"workload": desc, "sample_cells": cells, "rk_stages": 4},
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample},
+            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3000)
+    ap.add_argument("--warmup", type=int, default=50)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="C2", choices=["C2", "C3", "C4"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+
+    world = env_int("WORLD_SIZE", 1)
+    rank = env_int("RANK", 0)
+    local_rank = env_int("LOCAL_RANK", 0)
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+
+    import torch
+    import torch.distributed as dist
+    from paper_2305_18057_b200 import sfv
+
+    assert torch.cuda.is_available(), "bench.py needs a GPU (no CPU fallback)"
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    n_gpus = world
+    if args.gpus != n_gpus and rank == 0:
+        print(f"# note: --gpus {args.gpus} but WORLD_SIZE {world}; using {world}", file=sys.stderr)
+
+    ni, nj, theta, desc, scaling, px = workload(args.workload, n_gpus)
+    X, Y = I.ramp_nodes(ni, nj, theta)
+    cfg = I.default_config(ni, nj, max_history=max(args.steps + args.warmup + 16, 64))
+    U0 = I.uniform_state(ni, nj)
+    nccl_id = None
+    if world > 1:
+        obj = [sfv.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        nccl_id = obj[0]
+    stream = torch.cuda.Stream(device=dev)
+    solver = sfv.Solver(cfg, X, Y, px=px, py=1, rank=rank, nranks=world, nccl_id=nccl_id,
+                        device=local_rank, stream=stream)
+    solver.set_state(U0)
+    solver.step(args.warmup)
+    solver.sync()
+
+    def barrier():
+        torch.cuda.synchronize(dev)
+        if world > 1:
+            dist.barrier()
+
+    # ---- device-timed region (inputs resident in HBM) ----
+    barrier()
+    with Clocks(local_rank) as clk:
+        solver.step(args.steps)
+        ms = solver.sync()
+    barrier()
+    t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_max = float(t.item())
+    cells_total = ni * nj
+    stages = 4
+    value = cells_total * stages * args.steps / (ms_max * 1e-3) / 1e6
+    cells_rank = cells_total // world
+    launches = stages * args.steps
+
+    # ---- roofline of the dominant kernel (the fused stage kernel) ----
+    avg_launch_s = ms_max * 1e-3 / launches
+    alg_bytes = ALG_BYTES_PER_CELL_STAGE * cells_rank
+    achieved = alg_bytes / avg_launch_s / 1e9
+    peak, peak_src = measured_peak()
+    traffic_pc, prof = load_profile_traffic()
+    roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+            "traffic": (traffic_pc * cells_rank) if traffic_pc else None,
+            "alg_bytes_per_cell_stage": ALG_BYTES_PER_CELL_STAGE, "peak_source": peak_src,
+            "kernel": "sfv::stage_kernel (4 launches per step, averaged)"}
+    if prof and prof.get("fp64_inst_per_cell_stage"):
+        fp64_rate = prof["fp64_inst_per_cell_stage"] * cells_rank / avg_launch_s
+        clk_mhz = clk.summary().get("sm_mhz") or 1965.0
+        fp64_peak = 148 * 64 * clk_mhz * 1e6  # warp-lane DFMA-class instr/s at the sampled clock
+        roof["fp64"] = {"achieved_inst_per_s": fp64_rate, "peak_inst_per_s": fp64_peak,
+                        "frac": fp64_rate / fp64_peak,
+                        "inst_per_cell_stage": prof["fp64_inst_per_cell_stage"]}
+
+    # ---- end to end through the public API with host buffers ----
+    e2e = None
+    if not args.no_e2e:
+        Uh = torch.from_numpy(np.ascontiguousarray(U0)).pin_memory() if world == 1 else None
+        Uout = torch.empty_like(Uh) if Uh is not None else None
+        if Uh is None:
+            Uh = torch.from_numpy(np.ascontiguousarray(U0)).pin_memory()
+            Uout = torch.empty_like(Uh)
+        K = args.steps
+        barrier()
+        t0 = time.perf_counter()
+        solver.set_state_ptr(Uh.data_ptr())
+        solver.step(K)
+        norms = solver.residual_norms(0, K)
+        solver.get_state_ptr(Uout.data_ptr())
+        barrier()
+        wall = time.perf_counter() - t0
+        tw = torch.tensor([wall], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(tw, op=dist.ReduceOp.MAX)
+        wall = float(tw.item())
+        sbytes = cells_total * 4 * 8
+        e2e = {"value": cells_total * stages * K / wall / 1e6, "unit": UNIT,
+               "h2d_bytes_per_step": sbytes / K, "d2h_bytes_per_step": sbytes / K + 64.0,
+               "note": "set_state(pinned host U) + K steps + residual norms (64 B/step) + get_state, wall clock"}
+        assert np.all(np.isfinite(norms))
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline_oracle()
+
+    li = solver.launch_info()
+    if rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": n_gpus, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
+                "scaling": scaling, "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded inputs)",
+                "config": {"workload": desc, "global_cells": cells_total, "cells_per_gpu": cells_rank,
+                           "rk_stages": stages, "parallelism": f"slab{px}x1",
+                           "l2": f"no flush: working set {solver.ws.numel() / 1e6:.0f} MB per GPU vs 126 MB L2",
+                           "launch": li,
+                           "mcell_steps_per_s": value / stages,
+                           "pct_hbm_roofline_8TBs": 100.0 * value * 1e6 * ALG_BYTES_PER_CELL_STAGE / n_gpus / 8e12},
+                "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
+                "clocks": clk.summary()}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,180 @@
+/* sfv.h -- C ABI of the B200-native structured-grid finite-volume hot path
+ * of SENSEI (Xue, Wang, Roy, arXiv 2305.18057).
+ *
+ * What one step computes (PAPER.md citations; DESIGN.md lists the readings
+ * A-R* of every point the paper leaves open):
+ *   - ghost refresh of the stage input: physical boundary conditions
+ *     ("ghost cell extrapolation") and halo exchange with
+ *     neighbouring partitions ("boundary data exchange"),
+ *     2 layers deep because Eq. 7 reads i-1..i+2;
+ *   - MUSCL extrapolation with limiters Psi, Eq. 7, each
+ *     Psi computed once per cell and direction;
+ *   - the inviscid normal face flux of Eq. 2 by Roe's
+ *     scheme with Harten's entropy fix (reading A-R1/A-R2);
+ *   - flux-difference accumulation R_h = sum_f F_n ds, Eq. 5;
+ *   - the explicit s-stage Runge-Kutta update of Eq. 6
+ *     applied to |Omega| dU/dt + R_h = 0, Eq. 4;
+ *   - per step: the CFL time step (reading A-R6) and the residual norms of
+ *     R(U^n) ("residual print"; reading A-R20).
+ * Everything is IEEE binary64 on the device.
+ *
+ * Conventions
+ *   Ownership: the caller owns every host array and the device workspace.
+ *     Host inputs are copied before the call returns; no caller pointer is
+ *     retained, except the workspace given to sfv_bind, which must outlive
+ *     the ctx.  The library never frees the workspace.
+ *   Layouts (host):
+ *     nodes  x, y : (ni+1)*(nj+1) doubles, index j*(ni+1)+i
+ *     state  U    : ni*nj*4 doubles, index (j*ni+i)*4+k,
+ *                   k = rho, rho*u, rho*v, rho*E (conserved)
+ *     norms       : per step 8 doubles: L2[4] (RMS) then Linf[4] of R(U^n)
+ *   Errors: every call returns an sfv_status; sfv_last_error() gives text.
+ *     Physical-validity failures (rho <= 0 or p <= 0 in a face state or a
+ *     new stage state) are detected on the device into a sticky word and
+ *     reported by the next synchronising call (sfv_sync, sfv_get_*) as
+ *     SFV_ERR_STATE with the first failing (step, stage) and, within it,
+ *     the smallest global cell index j*ni+i (sfv_error_info).  After
+ *     SFV_ERR_STATE the state is undefined until the next sfv_set_state.
+ *   Concurrency: one ctx per process and GPU; calls on a ctx from one host
+ *     thread.  Device work is enqueued on the stream given to sfv_bind and
+ *     is asynchronous unless stated.
+ */
+#ifndef SFV_H
+#define SFV_H
+#include <stddef.h>
+#include <stdint.h>
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct sfv_ctx sfv_ctx;
+
+typedef enum {
+    SFV_OK = 0,
+    SFV_ERR_ARG = 1,         /* invalid argument or configuration */
+    SFV_ERR_GEOMETRY = 2,    /* a cell volume <= 0 */
+    SFV_ERR_STATE = 3,       /* rho <= 0 or p <= 0 */
+    SFV_ERR_SEQUENCE = 4,    /* call out of order, or history not available */
+    SFV_ERR_CUDA = 5,        /* CUDA runtime failure (incl. no device) */
+    SFV_ERR_NCCL = 6,        /* NCCL failure or NCCL library not loadable */
+    SFV_ERR_OOM = 7,         /* workspace too small */
+    SFV_ERR_UNSUPPORTED = 8
+} sfv_status;
+
+typedef enum { SFV_BC_INFLOW = 0, SFV_BC_OUTFLOW = 1, SFV_BC_SLIP_WALL = 2 } sfv_bc;
+typedef enum { SFV_LIM_VAN_ALBADA = 0, SFV_LIM_VAN_ALBADA2 = 1, SFV_LIM_NONE = 2 } sfv_limiter;
+typedef enum { SFV_RK4_CLASSIC = 0, SFV_RK2_HEUN = 1, SFV_RK4_JAMESON = 2 } sfv_rk;
+
+typedef struct {
+    int32_t ni, nj;              /* interior cells (paper N_l, N_w; N_d = 1), each >= 2 */
+    double gamma;                /* ratio of specific heats, > 1 (1.4) */
+    double muscl_eps;            /* epsilon of Eq. 7, 0 or 1 */
+    double muscl_kappa;          /* kappa of Eq. 7, in [-1, 1] (-1) */
+    int32_t limiter;             /* sfv_limiter (VAN_ALBADA)                             reading A-R3 */
+    double lim_delta;            /* limiter guard delta (1e-12) */
+    double harten_eps;           /* Harten constant; delta_H = max(eps*a, 1e-12) (0.1)   reading A-R2 */
+    int32_t rk;                  /* sfv_rk                                               reading A-R5 */
+    double cfl;                  /* CFL number of the 4-face dt (0.8 RK4)                reading A-R6 */
+    double dt_fixed;             /* > 0: fixed time step, cfl ignored */
+    int32_t bc[4];               /* physical boundary per edge W, E, S, N (sfv_bc)      reading A-R11/12 */
+    double inflow_U[4][4];       /* conserved inflow state per edge, used if INFLOW      reading A-R27 */
+    int64_t max_history;         /* capacity (steps) of the dt / norm history, >= 1 */
+} sfv_config;
+
+/* Validate cfg and copy the node arrays.  Host only (no device work).
+ * ARG: ni<2 || nj<2, gamma<=1, |kappa|>1, eps not in {0,1}, cfl<=0 without
+ *      dt_fixed, unknown enum, max_history<1.
+ * GEOMETRY: some cell volume <= 0 (sfv_error_info gives its i, j). */
+sfv_status sfv_create(const sfv_config *cfg, const double *x_nodes, const double *y_nodes,
+                      sfv_ctx **out);
+
+/* Decompose the grid into px*py blocks (reading A-R16/24/25):
+ * integer largest-remainder widths per direction from the optional integer
+ * weights wx[px], wy[py] (NULL = equal); block (bx, by) has rank index
+ * bx + px*by and owns [i0,i1) x [j0,j1).
+ *   nranks == 1 : all blocks live on this process's device and exchange
+ *                 halos by device copies ("loopback"; any px, py).
+ *   nranks  > 1 : px*py must equal nranks; this process owns block `rank`
+ *                 and exchanges halos with NCCL send/recv; nccl_unique_id
+ *                 (128 bytes from sfv_nccl_unique_id on rank 0, broadcast by
+ *                 the caller) is required.
+ * cuda_device is the device this ctx runs on.  Host only when nranks == 1.
+ * ARG: px*py inconsistent with nranks, any block width < 2, weight <= 0.
+ * NCCL: communicator initialisation failed.  SEQUENCE: after sfv_bind. */
+sfv_status sfv_partition(sfv_ctx *ctx, int32_t px, int32_t py, const int32_t *wx, const int32_t *wy,
+                         int32_t rank, int32_t nranks, const void *nccl_unique_id, int32_t cuda_device);
+
+/* Rank 0 calls this; the caller broadcasts the 128 bytes (torch.distributed). */
+sfv_status sfv_nccl_unique_id(void *out128);
+
+/* Partition map of block `block` (global block index): out8 =
+ * i0, i1, j0, j1, neighbour block W, E, S, N (-1 = physical boundary).
+ * Host only.  Bit-exact with the oracle's maps. */
+sfv_status sfv_partition_map(const sfv_ctx *ctx, int32_t block, int32_t *out8);
+
+/* Host-only integer largest-remainder split: starts[parts+1]. */
+sfv_status sfv_split(int32_t n, int32_t parts, const int32_t *weights, int32_t *starts);
+
+/* Bytes of device workspace this process needs for its blocks. */
+sfv_status sfv_workspace_size(const sfv_ctx *ctx, size_t *bytes);
+
+/* Bind caller-owned device memory (e.g. torch.empty(bytes, uint8, cuda)),
+ * >= sfv_workspace_size bytes, 256-byte aligned, and a CUDA stream
+ * (cudaStream_t; 0 = legacy default stream).  Computes the metrics (face
+ * normals, areas, inverse volumes) on the device.
+ * OOM: workspace too small.  CUDA: no device / launch failure. */
+sfv_status sfv_bind(sfv_ctx *ctx, void *device_workspace, size_t bytes, void *cuda_stream);
+
+/* Load the initial state (host array, full grid; every rank passes the full
+ * array and keeps its blocks), fill the ghost frames (boundary conditions +
+ * halo exchange), compute dt_0, reset the step counter, history and error
+ * word.  Synchronous.  STATE: some rho <= 0 or p <= 0. */
+sfv_status sfv_set_state(sfv_ctx *ctx, const double *U_global);
+
+/* Enqueue nsteps full RK steps on the bound stream (a CUDA graph per step);
+ * returns immediately.  SEQUENCE: before sfv_set_state. */
+sfv_status sfv_step(sfv_ctx *ctx, int32_t nsteps);
+
+/* Wait for enqueued work; *device_ms (may be NULL) = CUDA-event time of the
+ * steps enqueued since the previous sfv_sync.  Surfaces device errors. */
+sfv_status sfv_sync(sfv_ctx *ctx, double *device_ms);
+
+/* Steps completed (synchronising). */
+sfv_status sfv_steps_done(sfv_ctx *ctx, int64_t *out);
+
+/* Residual norms of steps first..first+count-1 (count x 8 doubles), reduced
+ * over all blocks and ranks (collective when nranks > 1).  Synchronising.
+ * SEQUENCE: range not completed or older than max_history steps. */
+sfv_status sfv_get_residual_norms(sfv_ctx *ctx, int64_t first, int64_t count, double *out);
+
+/* Time steps dt_n used by steps first..first+count-1.  Synchronising. */
+sfv_status sfv_get_dt(sfv_ctx *ctx, int64_t first, int64_t count, double *out);
+
+/* Copy the current interior state to a host array (full grid, same layout
+ * as sfv_set_state).  Collective when nranks > 1 (all ranks receive the
+ * full state).  Synchronising. */
+sfv_status sfv_get_state(sfv_ctx *ctx, double *U_global_out);
+
+/* Details of the last SFV_ERR_STATE / GEOMETRY: out4 = step, stage, i, j
+ * (-1 where not applicable). */
+sfv_status sfv_error_info(const sfv_ctx *ctx, int64_t *out4);
+
+/* Diagnostic: launch geometry of the stage kernel of local block 0:
+ * out4 = strips, segments, threads per CTA, resident CTAs per SM. */
+sfv_status sfv_launch_info(const sfv_ctx *ctx, int32_t *out4);
+
+/* Diagnostic: evaluate the device math helpers used by the stage kernel on
+ * n device doubles (which: 0 = reciprocal, 1 = reciprocal square root,
+ * 2 = square root) into out (device), on the bound stream; synchronising. */
+sfv_status sfv_debug_math(sfv_ctx *ctx, int32_t which, const double *in_dev, double *out_dev, int64_t n);
+
+/* Text of the last error on ctx (ctx-owned, valid until the next call). */
+const char *sfv_last_error(const sfv_ctx *ctx);
+
+/* Free library-owned host, CUDA-graph and NCCL resources (not the workspace). */
+void sfv_destroy(sfv_ctx *ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,847 @@
+// sfv_host.cu -- host runtime behind include/sfv.h: validation, partition
+// and ghost maps, workspace carve-up, per-step CUDA graph, halo exchange
+// (device copies between local blocks, NCCL send/recv between ranks), and
+// history / error bookkeeping.  See DESIGN.md §3-§6.
+#include <dlfcn.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "sfv.h"
+#include "sfv_internal.h"
+
+using namespace sfv;
+
+namespace {
+
+constexpr int NSEG_MAX = 256;
+constexpr size_t PADD = 512;  // padding doubles after each array (bulk-copy over-read)
+
+// ------------------------------------------------------------- NCCL (dlopen)
+struct Nccl {
+    bool ok = false;
+    ncclResult_t (*GetUniqueId)(ncclUniqueId *) = nullptr;
+    ncclResult_t (*CommInitRank)(ncclComm_t *, int, ncclUniqueId, int) = nullptr;
+    ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+    ncclResult_t (*Send)(const void *, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*Recv)(void *, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*GroupStart)() = nullptr;
+    ncclResult_t (*GroupEnd)() = nullptr;
+    ncclResult_t (*AllReduce)(const void *, void *, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                              cudaStream_t) = nullptr;
+    const char *(*GetErrorString)(ncclResult_t) = nullptr;
+};
+
+Nccl &nccl() {
+    static Nccl n;
+    static bool tried = false;
+    if (tried) return n;
+    tried = true;
+    void *h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL | RTLD_NOLOAD);
+    if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) return n;
+#define SFV_SYM(f) n.f = reinterpret_cast<decltype(n.f)>(dlsym(h, "nccl" #f))
+    SFV_SYM(GetUniqueId);
+    SFV_SYM(CommInitRank);
+    SFV_SYM(CommDestroy);
+    SFV_SYM(Send);
+    SFV_SYM(Recv);
+    SFV_SYM(GroupStart);
+    SFV_SYM(GroupEnd);
+    SFV_SYM(AllReduce);
+    SFV_SYM(GetErrorString);
+#undef SFV_SYM
+    n.ok = n.GetUniqueId && n.CommInitRank && n.CommDestroy && n.Send && n.Recv && n.GroupStart && n.GroupEnd &&
+           n.AllReduce && n.GetErrorString;
+    return n;
+}
+
+struct Block {
+    int id = 0, bx = 0, by = 0;
+    int i0 = 0, i1 = 0, j0 = 0, j1 = 0, ni = 0, nj = 0, PJ = 0;
+    int nbr[4] = {-1, -1, -1, -1};
+    int edge[4] = {0, 0, 0, 0};  // Edge kind per W, E, S, N
+    int nstrips = 1, nseg = 1;
+    double *buf[4] = {nullptr, nullptr, nullptr, nullptr};
+    double *met = nullptr, *nodes = nullptr, *stage = nullptr, *partials = nullptr;
+    unsigned *ticket = nullptr;
+    double *xs[2] = {nullptr, nullptr}, *xr[2] = {nullptr, nullptr};  // j-cut pack buffers (S, N)
+    size_t buf_elems() const { return (size_t)(ni + 4) * 4 * PJ + PADD; }
+    size_t met_elems() const { return (size_t)(ni + 1) * NMET * PJ + PADD; }
+};
+
+int nbuf_of(int rk) { return rk == SFV_RK4_CLASSIC ? 4 : (rk == SFV_RK2_HEUN ? 2 : 3); }
+int nstages_of(int rk) { return rk == SFV_RK2_HEUN ? 2 : 4; }
+
+struct StageSpec {
+    int in, out, mode;
+    double coef;
+    int pw[3];
+};
+// Data flow of each tableau (reading A-R5).  Algebraically
+// equal to Eq. 6: RK4's last stage recovers sum b_j R_j from the stored
+// stage states, U^{n+1} = U^n + ((W2-U^n) + 2(W3-U^n) + (W4-U^n))/3 - dt R4/(6V).
+StageSpec stage_spec(int rk, int k) {
+    if (rk == SFV_RK4_CLASSIC) {
+        switch (k) {
+            case 1: return {0, 1, M_OWN, 0.5, {-1, -1, -1}};
+            case 2: return {1, 2, M_UN, 0.5, {0, -1, -1}};
+            case 3: return {2, 3, M_UN, 1.0, {0, -1, -1}};
+            default: return {3, 0, M_RK4F, 1.0 / 6.0, {0, 1, 2}};
+        }
+    }
+    if (rk == SFV_RK2_HEUN) {
+        if (k == 1) return {0, 1, M_OWN, 1.0, {-1, -1, -1}};
+        return {1, 0, M_HEUNF, 0.5, {0, -1, -1}};
+    }
+    switch (k) {  // Jameson 4-stage, alpha = 1/4, 1/3, 1/2, 1
+        case 1: return {0, 1, M_OWN, 0.25, {-1, -1, -1}};
+        case 2: return {1, 2, M_UN, 1.0 / 3.0, {0, -1, -1}};
+        case 3: return {2, 1, M_UN, 0.5, {0, -1, -1}};
+        default: return {1, 0, M_UN, 1.0, {0, -1, -1}};
+    }
+}
+
+}  // namespace
+
+struct sfv_ctx {
+    sfv_config cfg{};
+    std::vector<double> X, Y;
+    int px = 1, py = 1;
+    std::vector<int> xs, ys;
+    int rank = 0, nranks = 1, device = 0;
+    bool partitioned = false, bound = false, have_state = false;
+    std::vector<Block> blocks;  // local blocks
+    int nblocks_total = 1;
+    uint8_t *ws = nullptr;
+    size_t ws_bytes = 0;
+    cudaStream_t st = nullptr;
+    double *sig = nullptr;
+    long long *step_ctr = nullptr;
+    unsigned long long *err = nullptr, *geo_bad = nullptr;
+    double *dt_hist = nullptr, *norm_hist = nullptr, *gbuf = nullptr;
+    size_t gbuf_elems = 0;
+    int nsm = 148, occ = 1;
+    Params P{};
+    long long steps_enq = 0;
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    bool timing_open = false;
+    cudaGraphExec_t gexec = nullptr;
+    bool graph_failed = false;
+    ncclComm_t comm = nullptr;
+    std::string msg;
+    long long einfo[4] = {-1, -1, -1, -1};
+};
+
+namespace {
+
+sfv_status fail(sfv_ctx *c, sfv_status s, const char *fmt, ...) {
+    if (c) {
+        char b[512];
+        va_list ap;
+        va_start(ap, fmt);
+        vsnprintf(b, sizeof b, fmt, ap);
+        va_end(ap);
+        c->msg = b;
+    }
+    return s;
+}
+
+#define CK(call)                                                                                  \
+    do {                                                                                          \
+        cudaError_t e_ = (call);                                                                  \
+        if (e_ != cudaSuccess) return fail(c, SFV_ERR_CUDA, "%s: %s", #call, cudaGetErrorString(e_)); \
+    } while (0)
+#define NK(call)                                                                                   \
+    do {                                                                                           \
+        ncclResult_t r_ = (call);                                                                  \
+        if (r_ != ncclSuccess) return fail(c, SFV_ERR_NCCL, "%s: %s", #call, nccl().GetErrorString(r_)); \
+    } while (0)
+
+// Largest-remainder split (reading A-R24).
+sfv_status split_impl(int32_t n, int32_t parts, const int32_t *w, int32_t *starts) {
+    if (parts < 1 || n < 1) return SFV_ERR_ARG;
+    long long sw = 0;
+    for (int r = 0; r < parts; ++r) {
+        long long x = w ? w[r] : 1;
+        if (x <= 0) return SFV_ERR_ARG;
+        sw += x;
+    }
+    std::vector<long long> base(parts), rem(parts);
+    long long used = 0;
+    for (int r = 0; r < parts; ++r) {
+        long long x = w ? w[r] : 1;
+        base[r] = (long long)n * x / sw;
+        rem[r] = (long long)n * x % sw;
+        used += base[r];
+    }
+    std::vector<int> order(parts);
+    for (int r = 0; r < parts; ++r) order[r] = r;
+    std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return rem[a] > rem[b]; });
+    for (long long k = 0; k < n - used; ++k) base[order[k]] += 1;
+    sfv_status s = SFV_OK;
+    starts[0] = 0;
+    for (int r = 0; r < parts; ++r) {
+        if (base[r] < 2) s = SFV_ERR_ARG;
+        starts[r + 1] = starts[r] + (int32_t)base[r];
+    }
+    return s;
+}
+
+size_t al(size_t b) { return (b + 255) & ~(size_t)255; }
+
+int pitch_of(int nj) { return ((nj + JOFF + 2 + 15) / 16) * 16; }
+
+void build_params(sfv_ctx *c) {
+    const sfv_config &f = c->cfg;
+    Params &P = c->P;
+    P.gamma = f.gamma;
+    P.gm1 = f.gamma - 1.0;
+    P.c1 = f.muscl_eps * (1.0 - f.muscl_kappa) / 4.0;
+    P.c2 = f.muscl_eps * (1.0 + f.muscl_kappa) / 4.0;
+    P.delta = f.lim_delta;
+    P.heps = f.harten_eps;
+    P.hinv = f.harten_eps > 0.0 ? 0.5 / f.harten_eps : 0.0;
+    P.cfl = f.cfl;
+    P.dt_fixed = f.dt_fixed;
+    P.limiter = f.limiter;
+}
+
+// Launch geometry: strips of <= NT-4 columns (even starts), segments along i
+// so that strips*segments fills the device in whole waves.
+void choose_launch(sfv_ctx *c, Block &b) {
+    b.nstrips = (b.nj + (NT - 4) - 1) / (NT - 4);
+    const int slots = c->nsm * std::max(1, c->occ);
+    int best = 1;
+    double best_score = -1.0;
+    const int cap = std::min(NSEG_MAX, std::max(1, b.ni / 4));
+    for (int s = 1; s <= cap; ++s) {
+        const double waves = (double)b.nstrips * s / slots;
+        const double eff = waves / std::ceil(waves);
+        const double L = (double)b.ni / s;
+        const double score = eff * (L / (L + 1.5));
+        if (score > best_score + 1e-9) {
+            best_score = score;
+            best = s;
+        }
+    }
+    b.nseg = std::min(best, b.ni);
+}
+
+sfv_status build_blocks(sfv_ctx *c) {
+    c->blocks.clear();
+    const int nb = c->px * c->py;
+    c->nblocks_total = nb;
+    for (int id = 0; id < nb; ++id) {
+        if (c->nranks > 1 && id != c->rank) continue;
+        Block b;
+        b.id = id;
+        b.bx = id % c->px;
+        b.by = id / c->px;
+        b.i0 = c->xs[b.bx];
+        b.i1 = c->xs[b.bx + 1];
+        b.j0 = c->ys[b.by];
+        b.j1 = c->ys[b.by + 1];
+        b.ni = b.i1 - b.i0;
+        b.nj = b.j1 - b.j0;
+        b.PJ = pitch_of(b.nj);
+        b.nbr[0] = b.bx > 0 ? id - 1 : -1;
+        b.nbr[1] = b.bx < c->px - 1 ? id + 1 : -1;
+        b.nbr[2] = b.by > 0 ? id - c->px : -1;
+        b.nbr[3] = b.by < c->py - 1 ? id + c->px : -1;
+        for (int e = 0; e < 4; ++e) b.edge[e] = b.nbr[e] >= 0 ? E_CONNECTED : c->cfg.bc[e];
+        b.nstrips = (b.nj + (NT - 4) - 1) / (NT - 4);
+        b.nseg = 1;
+        c->blocks.push_back(b);
+    }
+    return SFV_OK;
+}
+
+size_t layout(sfv_ctx *c, bool assign) {
+    size_t off = 0;
+    auto take = [&](size_t bytes) {
+        size_t o = off;
+        off += al(bytes);
+        return o;
+    };
+    const int cap = (int)c->cfg.max_history;
+    const int nbuf = nbuf_of(c->cfg.rk);
+    size_t o_misc = take(256);
+    size_t o_dt = take(sizeof(double) * cap);
+    size_t o_norm = take(sizeof(double) * (size_t)cap * c->nblocks_total * 8);
+    size_t gb = 0;
+    if (c->nranks > 1) gb = std::max((size_t)c->cfg.ni * c->cfg.nj * 4, (size_t)c->nblocks_total * 8 * 4096);
+    size_t o_g = take(sizeof(double) * gb);
+    if (assign) {
+        c->sig = reinterpret_cast<double *>(c->ws + o_misc);
+        c->step_ctr = reinterpret_cast<long long *>(c->ws + o_misc + 16);
+        c->err = reinterpret_cast<unsigned long long *>(c->ws + o_misc + 24);
+        c->geo_bad = reinterpret_cast<unsigned long long *>(c->ws + o_misc + 32);
+        c->dt_hist = reinterpret_cast<double *>(c->ws + o_dt);
+        c->norm_hist = reinterpret_cast<double *>(c->ws + o_norm);
+        c->gbuf = gb ? reinterpret_cast<double *>(c->ws + o_g) : nullptr;
+        c->gbuf_elems = gb;
+    }
+    for (Block &b : c->blocks) {
+        size_t ob[4];
+        for (int k = 0; k < nbuf; ++k) ob[k] = take(sizeof(double) * b.buf_elems());
+        size_t om = take(sizeof(double) * b.met_elems());
+        size_t on = take(sizeof(double) * 2 * (size_t)(b.ni + 1) * (b.nj + 1));
+        size_t os = take(sizeof(double) * 4 * (size_t)b.ni * b.nj);
+        const int max_cta = ((b.nj + (NT - 4) - 1) / (NT - 4)) * NSEG_MAX;
+        size_t op = take(sizeof(double) * 8 * (size_t)max_cta);
+        size_t ot = take(256);
+        size_t ox[4];
+        for (int k = 0; k < 4; ++k) ox[k] = take(c->nranks > 1 ? sizeof(double) * 8 * (size_t)b.ni : 0);
+        if (assign) {
+            for (int k = 0; k < nbuf; ++k) b.buf[k] = reinterpret_cast<double *>(c->ws + ob[k]);
+            b.met = reinterpret_cast<double *>(c->ws + om);
+            b.nodes = reinterpret_cast<double *>(c->ws + on);
+            b.stage = reinterpret_cast<double *>(c->ws + os);
+            b.partials = reinterpret_cast<double *>(c->ws + op);
+            b.ticket = reinterpret_cast<unsigned *>(c->ws + ot);
+            b.xs[0] = reinterpret_cast<double *>(c->ws + ox[0]);
+            b.xs[1] = reinterpret_cast<double *>(c->ws + ox[1]);
+            b.xr[0] = reinterpret_cast<double *>(c->ws + ox[2]);
+            b.xr[1] = reinterpret_cast<double *>(c->ws + ox[3]);
+        }
+    }
+    return off;
+}
+
+Block *local_block(sfv_ctx *c, int id) {
+    for (Block &b : c->blocks)
+        if (b.id == id) return &b;
+    return nullptr;
+}
+
+// Halo exchange of state buffer k after a stage ("boundary
+// data exchange"; reading A-R16/A-R18: 2 layers, face neighbours only).
+// i-cuts: the 2 edge rows are one contiguous run in the [i][c][j] layout;
+// j-cuts: 2 columns, strided.
+sfv_status exchange(sfv_ctx *c, int k, cudaStream_t st) {
+    if (c->nblocks_total == 1) return SFV_OK;
+    if (c->nranks == 1) {
+        for (Block &b : c->blocks) {
+            if (b.nbr[1] >= 0) {  // E neighbour e: b rows ni-2,ni-1 -> e rows -2,-1; e rows 0,1 -> b rows ni,ni+1
+                Block &e = *local_block(c, b.nbr[1]);
+                const size_t run = (size_t)2 * 4 * b.PJ;
+                CK(cudaMemcpyAsync(e.buf[k], b.buf[k] + (size_t)(b.ni) * 4 * b.PJ, run * 8, cudaMemcpyDeviceToDevice, st));
+                CK(cudaMemcpyAsync(b.buf[k] + (size_t)(b.ni + 2) * 4 * b.PJ, e.buf[k] + (size_t)2 * 4 * e.PJ, run * 8,
+                                   cudaMemcpyDeviceToDevice, st));
+            }
+            if (b.nbr[3] >= 0) {  // N neighbour: b cols nj-2,nj-1 -> n cols -2,-1; n cols 0,1 -> b cols nj,nj+1
+                Block &n = *local_block(c, b.nbr[3]);
+                CK(cudaMemcpy2DAsync(n.buf[k] + (size_t)8 * n.PJ + (-2 + JOFF), (size_t)n.PJ * 8,
+                                     b.buf[k] + (size_t)8 * b.PJ + (b.nj - 2 + JOFF), (size_t)b.PJ * 8, 16,
+                                     (size_t)b.ni * 4, cudaMemcpyDeviceToDevice, st));
+                CK(cudaMemcpy2DAsync(b.buf[k] + (size_t)8 * b.PJ + (b.nj + JOFF), (size_t)b.PJ * 8,
+                                     n.buf[k] + (size_t)8 * n.PJ + (0 + JOFF), (size_t)n.PJ * 8, 16,
+                                     (size_t)n.ni * 4, cudaMemcpyDeviceToDevice, st));
+            }
+        }
+        return SFV_OK;
+    }
+    // NCCL: one block per rank; block id == rank.
+    Block &b = c->blocks[0];
+    Nccl &N = nccl();
+    for (int s = 0; s < 2; ++s) {  // pack j-cut columns first (S: cols 0,1; N: cols nj-2,nj-1)
+        const int nb = b.nbr[2 + s];
+        if (nb < 0) continue;
+        CK(launch_pack_cols(b.buf[k], b.xs[s], b.ni, b.PJ, s == 0 ? 0 : b.nj - 2, st));
+    }
+    NK(N.GroupStart());
+    const size_t run = (size_t)2 * 4 * b.PJ;
+    if (b.nbr[0] >= 0) {
+        NK(N.Send(b.buf[k] + (size_t)2 * 4 * b.PJ, run, ncclDouble, b.nbr[0], c->comm, st));
+        NK(N.Recv(b.buf[k], run, ncclDouble, b.nbr[0], c->comm, st));
+    }
+    if (b.nbr[1] >= 0) {
+        NK(N.Send(b.buf[k] + (size_t)(b.ni) * 4 * b.PJ, run, ncclDouble, b.nbr[1], c->comm, st));
+        NK(N.Recv(b.buf[k] + (size_t)(b.ni + 2) * 4 * b.PJ, run, ncclDouble, b.nbr[1], c->comm, st));
+    }
+    for (int s = 0; s < 2; ++s) {
+        const int nb = b.nbr[2 + s];
+        if (nb < 0) continue;
+        NK(N.Send(b.xs[s], (size_t)8 * b.ni, ncclDouble, nb, c->comm, st));
+        NK(N.Recv(b.xr[s], (size_t)8 * b.ni, ncclDouble, nb, c->comm, st));
+    }
+    NK(N.GroupEnd());
+    for (int s = 0; s < 2; ++s) {
+        const int nb = b.nbr[2 + s];
+        if (nb < 0) continue;
+        CK(launch_unpack_cols(b.xr[s], b.buf[k], b.ni, b.PJ, s == 0 ? -2 : b.nj, st));
+    }
+    return SFV_OK;
+}
+
+StageArgs make_args(sfv_ctx *c, Block &b, int k) {
+    const StageSpec sp = stage_spec(c->cfg.rk, k);
+    StageArgs a{};
+    a.in = b.buf[sp.in];
+    a.out = b.buf[sp.out];
+    a.pw0 = sp.pw[0] >= 0 ? b.buf[sp.pw[0]] : nullptr;
+    a.pw1 = sp.pw[1] >= 0 ? b.buf[sp.pw[1]] : nullptr;
+    a.pw2 = sp.pw[2] >= 0 ? b.buf[sp.pw[2]] : nullptr;
+    a.met = b.met;
+    a.ni = b.ni;
+    a.nj = b.nj;
+    a.PJ = b.PJ;
+    a.gi0 = b.i0;
+    a.gj0 = b.j0;
+    a.NI = c->cfg.ni;
+    a.NJ = c->cfg.nj;
+    a.nstrips = b.nstrips;
+    a.nseg = b.nseg;
+    for (int e = 0; e < 4; ++e) a.bc[e] = b.edge[e];
+    a.coef = sp.coef;
+    a.sig = c->sig;
+    a.step_ctr = c->step_ctr;
+    a.dt_hist = c->dt_hist;
+    a.norm_hist = c->norm_hist;
+    a.cap = (int)c->cfg.max_history;
+    a.block_id = b.id;
+    a.nblocks = c->nblocks_total;
+    a.partials = b.partials;
+    a.ticket = b.ticket;
+    a.err = c->err;
+    a.stage = k;
+    a.nstages = nstages_of(c->cfg.rk);
+    a.lead = (&b == &c->blocks.front()) ? 1 : 0;
+    a.bump = (k == a.nstages && &b == &c->blocks.back()) ? 1 : 0;
+    a.P = c->P;
+    return a;
+}
+
+sfv_status enqueue_step(sfv_ctx *c, cudaStream_t st) {
+    const int s = nstages_of(c->cfg.rk);
+    const bool cflmode = !(c->cfg.dt_fixed > 0.0);
+    for (int k = 1; k <= s; ++k) {
+        const StageSpec sp = stage_spec(c->cfg.rk, k);
+        for (Block &b : c->blocks) {
+            StageArgs a = make_args(c, b, k);
+            CK(launch_stage(a, sp.mode, k == 1, k == s && cflmode, st));
+        }
+        sfv_status r = exchange(c, sp.out, st);
+        if (r != SFV_OK) return r;
+    }
+    if (c->nranks > 1 && cflmode) NK(nccl().AllReduce(c->sig, c->sig, 2, ncclDouble, ncclMax, c->comm, st));
+    return SFV_OK;
+}
+
+sfv_status check_device_error(sfv_ctx *c) {
+    unsigned long long e = ~0ull;
+    CK(cudaMemcpy(&e, c->err, sizeof e, cudaMemcpyDeviceToHost));
+    if (e == ~0ull) return SFV_OK;
+    const long long hi = (long long)(e >> 32), cell = (long long)(e & 0xffffffffull);
+    const int s = nstages_of(c->cfg.rk);
+    const long long q = hi / 2, phase = hi % 2;
+    c->einfo[0] = q / s;
+    c->einfo[1] = q % s + 1;
+    c->einfo[2] = cell % c->cfg.ni;
+    c->einfo[3] = cell / c->cfg.ni;
+    c->have_state = false;
+    return fail(c, SFV_ERR_STATE, "invalid %s at step %lld stage %lld cell (%lld,%lld)",
+                phase ? "state (rho<=0 or p<=0)" : "face state", c->einfo[0], c->einfo[1], c->einfo[2],
+                c->einfo[3]);
+}
+
+}  // namespace
+
+// ======================================================================= ABI
+extern "C" {
+
+sfv_status sfv_split(int32_t n, int32_t parts, const int32_t *weights, int32_t *starts) {
+    return split_impl(n, parts, weights, starts);
+}
+
+sfv_status sfv_create(const sfv_config *cfg, const double *x, const double *y, sfv_ctx **out) {
+    if (!out || !cfg || !x || !y) return SFV_ERR_ARG;
+    *out = nullptr;
+    const sfv_config &f = *cfg;
+    if (f.ni < 2 || f.nj < 2 || !(f.gamma > 1.0) || !(std::fabs(f.muscl_kappa) <= 1.0) ||
+        !(f.muscl_eps == 0.0 || f.muscl_eps == 1.0) || (!(f.dt_fixed > 0.0) && !(f.cfl > 0.0)) ||
+        f.max_history < 1 || f.rk < 0 || f.rk > 2 || f.limiter < 0 || f.limiter > 2 || !(f.lim_delta >= 0.0) ||
+        !(f.harten_eps >= 0.0))
+        return SFV_ERR_ARG;
+    for (int e = 0; e < 4; ++e)
+        if (f.bc[e] < 0 || f.bc[e] > 2) return SFV_ERR_ARG;
+    if ((long long)f.ni * f.nj >= (1ll << 31)) return SFV_ERR_UNSUPPORTED;
+    sfv_ctx *c = new sfv_ctx();
+    c->cfg = f;
+    const size_t nn = (size_t)(f.ni + 1) * (f.nj + 1);
+    c->X.assign(x, x + nn);
+    c->Y.assign(y, y + nn);
+    build_params(c);
+    // volume check on the host (GEOMETRY error names the cell)
+    const int W = f.ni + 1;
+    for (int j = 0; j < f.nj; ++j)
+        for (int i = 0; i < f.ni; ++i) {
+            auto X = [&](int ii, int jj) { return c->X[(size_t)jj * W + ii]; };
+            auto Y = [&](int ii, int jj) { return c->Y[(size_t)jj * W + ii]; };
+            const double V = 0.5 * ((X(i + 1, j + 1) - X(i, j)) * (Y(i, j + 1) - Y(i + 1, j)) -
+                                    (Y(i + 1, j + 1) - Y(i, j)) * (X(i, j + 1) - X(i + 1, j)));
+            if (!(V > 0.0)) {
+                c->einfo[0] = -1; c->einfo[1] = -1; c->einfo[2] = i; c->einfo[3] = j;
+                *out = c;
+                fail(c, SFV_ERR_GEOMETRY, "non-positive cell volume at (%d,%d)", i, j);
+                return SFV_ERR_GEOMETRY;
+            }
+        }
+    c->xs = {0, f.ni};
+    c->ys = {0, f.nj};
+    build_blocks(c);
+    c->partitioned = true;
+    *out = c;
+    return SFV_OK;
+}
+
+sfv_status sfv_nccl_unique_id(void *out128) {
+    if (!out128) return SFV_ERR_ARG;
+    Nccl &N = nccl();
+    if (!N.ok) return SFV_ERR_NCCL;
+    ncclUniqueId id;
+    if (N.GetUniqueId(&id) != ncclSuccess) return SFV_ERR_NCCL;
+    static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId size");
+    memcpy(out128, &id, 128);
+    return SFV_OK;
+}
+
+sfv_status sfv_partition(sfv_ctx *c, int32_t px, int32_t py, const int32_t *wx, const int32_t *wy, int32_t rank,
+                         int32_t nranks, const void *uid, int32_t device) {
+    if (!c) return SFV_ERR_ARG;
+    if (c->bound) return fail(c, SFV_ERR_SEQUENCE, "sfv_partition after sfv_bind");
+    if (px < 1 || py < 1 || nranks < 1 || rank < 0 || rank >= nranks)
+        return fail(c, SFV_ERR_ARG, "bad px/py/rank/nranks");
+    if (nranks > 1 && px * py != nranks) return fail(c, SFV_ERR_ARG, "px*py (%d) != nranks (%d)", px * py, nranks);
+    std::vector<int> xs(px + 1), ys(py + 1);
+    if (split_impl(c->cfg.ni, px, wx, xs.data()) != SFV_OK || split_impl(c->cfg.nj, py, wy, ys.data()) != SFV_OK)
+        return fail(c, SFV_ERR_ARG, "partition: block width < 2 or weight <= 0");
+    c->px = px;
+    c->py = py;
+    c->xs = xs;
+    c->ys = ys;
+    c->rank = rank;
+    c->nranks = nranks;
+    c->device = device;
+    build_blocks(c);
+    if (nranks > 1) {
+        if (!uid) return fail(c, SFV_ERR_ARG, "nccl_unique_id required when nranks > 1");
+        Nccl &N = nccl();
+        if (!N.ok) return fail(c, SFV_ERR_NCCL, "libnccl.so.2 not loadable");
+        CK(cudaSetDevice(device));
+        ncclUniqueId id;
+        memcpy(&id, uid, 128);
+        NK(N.CommInitRank(&c->comm, nranks, id, rank));
+    }
+    c->partitioned = true;
+    return SFV_OK;
+}
+
+sfv_status sfv_partition_map(const sfv_ctx *c, int32_t block, int32_t *out8) {
+    if (!c || !out8 || block < 0 || block >= c->px * c->py) return SFV_ERR_ARG;
+    const int bx = block % c->px, by = block / c->px;
+    out8[0] = c->xs[bx];
+    out8[1] = c->xs[bx + 1];
+    out8[2] = c->ys[by];
+    out8[3] = c->ys[by + 1];
+    out8[4] = bx > 0 ? block - 1 : -1;
+    out8[5] = bx < c->px - 1 ? block + 1 : -1;
+    out8[6] = by > 0 ? block - c->px : -1;
+    out8[7] = by < c->py - 1 ? block + c->px : -1;
+    return SFV_OK;
+}
+
+sfv_status sfv_workspace_size(const sfv_ctx *c, size_t *bytes) {
+    if (!c || !bytes) return SFV_ERR_ARG;
+    *bytes = layout(const_cast<sfv_ctx *>(c), false) + 256;
+    return SFV_OK;
+}
+
+sfv_status sfv_bind(sfv_ctx *c, void *ws, size_t bytes, void *stream) {
+    if (!c || !ws) return SFV_ERR_ARG;
+    if (c->bound) return fail(c, SFV_ERR_SEQUENCE, "already bound");
+    size_t need = layout(c, false);
+    if (bytes < need) return fail(c, SFV_ERR_OOM, "workspace %zu < %zu bytes", bytes, need);
+    if (reinterpret_cast<uintptr_t>(ws) % 256) return fail(c, SFV_ERR_ARG, "workspace not 256-byte aligned");
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) return fail(c, SFV_ERR_CUDA, "no CUDA device");
+    CK(cudaSetDevice(c->device));
+    c->ws = static_cast<uint8_t *>(ws);
+    c->ws_bytes = bytes;
+    c->st = static_cast<cudaStream_t>(stream);
+    layout(c, true);
+    cudaDeviceProp prop;
+    CK(cudaGetDeviceProperties(&prop, c->device));
+    c->nsm = prop.multiProcessorCount;
+    int o = 1;
+    CK(prepare_stage_kernels());
+    CK(stage_occupancy(M_UN, false, false, &o));
+    c->occ = std::max(1, o);
+    CK(cudaEventCreate(&c->ev0));
+    CK(cudaEventCreate(&c->ev1));
+    cudaStream_t st = c->st;
+    CK(cudaMemsetAsync(c->ws, 0, need, st));
+    CK(cudaMemsetAsync(c->geo_bad, 0xff, 8, st));
+    const int W = c->cfg.ni + 1;
+    for (Block &b : c->blocks) {
+        choose_launch(c, b);
+        // block-local nodes, [j][i]
+        std::vector<double> h(2 * (size_t)(b.ni + 1) * (b.nj + 1));
+        const size_t nn = (size_t)(b.ni + 1) * (b.nj + 1);
+        for (int j = 0; j <= b.nj; ++j)
+            for (int i = 0; i <= b.ni; ++i) {
+                h[(size_t)j * (b.ni + 1) + i] = c->X[(size_t)(b.j0 + j) * W + b.i0 + i];
+                h[nn + (size_t)j * (b.ni + 1) + i] = c->Y[(size_t)(b.j0 + j) * W + b.i0 + i];
+            }
+        CK(cudaMemcpyAsync(b.nodes, h.data(), h.size() * 8, cudaMemcpyHostToDevice, st));
+        MetricsArgs m{b.nodes, b.nodes + nn, b.met, b.ni, b.nj, b.PJ, c->geo_bad};
+        CK(launch_metrics(m, st));
+        CK(cudaStreamSynchronize(st));  // h is freed at scope end
+    }
+    unsigned long long bad = ~0ull;
+    CK(cudaMemcpy(&bad, c->geo_bad, 8, cudaMemcpyDeviceToHost));
+    if (bad != ~0ull) return fail(c, SFV_ERR_GEOMETRY, "non-positive volume (device metrics)");
+    c->bound = true;
+    return SFV_OK;
+}
+
+sfv_status sfv_set_state(sfv_ctx *c, const double *U) {
+    if (!c || !U) return SFV_ERR_ARG;
+    if (!c->bound) return fail(c, SFV_ERR_SEQUENCE, "sfv_set_state before sfv_bind");
+    cudaStream_t st = c->st;
+    const int nbuf = nbuf_of(c->cfg.rk);
+    const int NI = c->cfg.ni;
+    int bcfill[4];
+    CK(cudaMemsetAsync(c->err, 0xff, 8, st));
+    for (Block &b : c->blocks) {
+        CK(cudaMemcpy2DAsync(b.stage, (size_t)b.ni * 32, U + ((size_t)b.j0 * NI + b.i0) * 4, (size_t)NI * 32,
+                             (size_t)b.ni * 32, b.nj, cudaMemcpyHostToDevice, st));
+        CK(launch_scatter(b.stage, b.buf[0], b.ni, b.nj, b.PJ, st));
+        for (int e = 0; e < 4; ++e) bcfill[e] = b.edge[e] == E_CONNECTED ? -1 : b.edge[e];
+        for (int k = 0; k < nbuf; ++k) {
+            CK(launch_poison_corners(b.buf[k], b.ni, b.nj, b.PJ, st));
+            CK(launch_bc_fill(b.buf[k], b.met, b.ni, b.nj, b.PJ, bcfill, c->cfg.inflow_U, st));
+        }
+        CK(launch_check_state(b.buf[0], b.ni, b.nj, b.PJ, b.i0, b.j0, NI, c->err, st));
+        CK(cudaMemsetAsync(b.ticket, 0, 256, st));
+    }
+    sfv_status r = exchange(c, 0, st);
+    if (r != SFV_OK) return r;
+    CK(cudaMemsetAsync(c->sig, 0, 24, st));  // sig[2], step counter
+    CK(cudaMemsetAsync(c->dt_hist, 0, sizeof(double) * c->cfg.max_history, st));
+    CK(cudaMemsetAsync(c->norm_hist, 0, sizeof(double) * c->cfg.max_history * c->nblocks_total * 8, st));
+    CK(cudaStreamSynchronize(st));
+    unsigned long long e = ~0ull;
+    CK(cudaMemcpy(&e, c->err, 8, cudaMemcpyDeviceToHost));
+    if (e != ~0ull) {
+        c->einfo[0] = -1; c->einfo[1] = 0; c->einfo[2] = (long long)(e % NI); c->einfo[3] = (long long)(e / NI);
+        c->have_state = false;
+        return fail(c, SFV_ERR_STATE, "invalid state (rho<=0 or p<=0) at cell (%lld,%lld)", c->einfo[2], c->einfo[3]);
+    }
+    if (!(c->cfg.dt_fixed > 0.0)) {
+        for (Block &b : c->blocks) CK(launch_sigma(b.buf[0], b.met, b.ni, b.nj, b.PJ, c->P, c->sig, st));
+        if (c->nranks > 1) NK(nccl().AllReduce(c->sig, c->sig, 2, ncclDouble, ncclMax, c->comm, st));
+    }
+    CK(cudaStreamSynchronize(st));
+    c->steps_enq = 0;
+    c->have_state = true;
+    c->timing_open = false;
+    return SFV_OK;
+}
+
+sfv_status sfv_step(sfv_ctx *c, int32_t nsteps) {
+    if (!c) return SFV_ERR_ARG;
+    if (!c->have_state) return fail(c, SFV_ERR_SEQUENCE, "sfv_step before sfv_set_state");
+    if (nsteps < 0) return fail(c, SFV_ERR_ARG, "nsteps < 0");
+    if (nsteps == 0) return SFV_OK;
+    if (!c->gexec && !c->graph_failed) {
+        cudaStream_t cap;
+        CK(cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking));
+        cudaGraph_t g = nullptr;
+        bool ok = cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal) == cudaSuccess;
+        sfv_status r = SFV_OK;
+        if (ok) {
+            r = enqueue_step(c, cap);
+            ok = (cudaStreamEndCapture(cap, &g) == cudaSuccess) && r == SFV_OK;
+        }
+        if (ok) ok = cudaGraphInstantiate(&c->gexec, g, 0) == cudaSuccess;
+        if (g) cudaGraphDestroy(g);
+        cudaStreamDestroy(cap);
+        if (!ok) {
+            c->gexec = nullptr;
+            c->graph_failed = true;
+            cudaGetLastError();
+        }
+    }
+    if (!c->timing_open) {
+        CK(cudaEventRecord(c->ev0, c->st));
+        c->timing_open = true;
+    }
+    for (int s = 0; s < nsteps; ++s) {
+        if (c->gexec) {
+            CK(cudaGraphLaunch(c->gexec, c->st));
+        } else {
+            sfv_status r = enqueue_step(c, c->st);
+            if (r != SFV_OK) return r;
+        }
+    }
+    CK(cudaEventRecord(c->ev1, c->st));
+    c->steps_enq += nsteps;
+    return SFV_OK;
+}
+
+sfv_status sfv_sync(sfv_ctx *c, double *ms) {
+    if (!c) return SFV_ERR_ARG;
+    if (!c->bound) return fail(c, SFV_ERR_SEQUENCE, "not bound");
+    CK(cudaStreamSynchronize(c->st));
+    if (ms) *ms = 0.0;
+    if (c->timing_open) {
+        float f = 0.f;
+        CK(cudaEventElapsedTime(&f, c->ev0, c->ev1));
+        if (ms) *ms = f;
+        c->timing_open = false;
+    }
+    return check_device_error(c);
+}
+
+sfv_status sfv_steps_done(sfv_ctx *c, int64_t *out) {
+    if (!c || !out) return SFV_ERR_ARG;
+    if (!c->bound) return fail(c, SFV_ERR_SEQUENCE, "not bound");
+    CK(cudaStreamSynchronize(c->st));
+    long long n = 0;
+    CK(cudaMemcpy(&n, c->step_ctr, 8, cudaMemcpyDeviceToHost));
+    *out = n;
+    return SFV_OK;
+}
+
+static sfv_status hist_range(sfv_ctx *c, int64_t first, int64_t count, long long *done) {
+    sfv_status s = sfv_steps_done(c, (int64_t *)done);
+    if (s != SFV_OK) return s;
+    if (first < 0 || count < 0 || first + count > *done || first < *done - c->cfg.max_history)
+        return fail(c, SFV_ERR_SEQUENCE, "history range [%lld,%lld) not available (done %lld, cap %lld)",
+                    (long long)first, (long long)(first + count), *done, (long long)c->cfg.max_history);
+    return SFV_OK;
+}
+
+sfv_status sfv_get_residual_norms(sfv_ctx *c, int64_t first, int64_t count, double *out) {
+    if (!c || (!out && count)) return SFV_ERR_ARG;
+    long long done = 0;
+    sfv_status s = hist_range(c, first, count, &done);
+    if (s != SFV_OK) return s;
+    s = check_device_error(c);
+    if (s != SFV_OK) return s;
+    const int nb = c->nblocks_total;
+    const long long cap = c->cfg.max_history;
+    std::vector<double> h((size_t)count * nb * 8);
+    // per step: nb x 8 partials (sum of squares, max |R|)
+    for (long long q = 0; q < count; ++q) {
+        const long long slot = (first + q) % cap;
+        CK(cudaMemcpy(h.data() + (size_t)q * nb * 8, c->norm_hist + (size_t)slot * nb * 8, sizeof(double) * nb * 8,
+                      cudaMemcpyDeviceToHost));
+    }
+    if (c->nranks > 1) {  // non-local blocks are zero: a sum all-reduce gathers them
+        for (long long q0 = 0; q0 < count; q0 += 4096) {
+            const long long m = std::min<long long>(4096, count - q0);
+            CK(cudaMemcpy(c->gbuf, h.data() + (size_t)q0 * nb * 8, sizeof(double) * m * nb * 8,
+                          cudaMemcpyHostToDevice));
+            NK(nccl().AllReduce(c->gbuf, c->gbuf, (size_t)m * nb * 8, ncclDouble, ncclSum, c->comm, c->st));
+            CK(cudaStreamSynchronize(c->st));
+            CK(cudaMemcpy(h.data() + (size_t)q0 * nb * 8, c->gbuf, sizeof(double) * m * nb * 8,
+                          cudaMemcpyDeviceToHost));
+        }
+    }
+    const double N = (double)c->cfg.ni * (double)c->cfg.nj;
+    for (long long q = 0; q < count; ++q) {
+        const double *p = h.data() + (size_t)q * nb * 8;
+        for (int k = 0; k < 4; ++k) {
+            double sum = 0.0, mx = 0.0;
+            for (int b = 0; b < nb; ++b) {
+                sum += p[b * 8 + k];
+                mx = std::max(mx, p[b * 8 + 4 + k]);
+            }
+            out[q * 8 + k] = std::sqrt(sum / N);
+            out[q * 8 + 4 + k] = mx;
+        }
+    }
+    return SFV_OK;
+}
+
+sfv_status sfv_get_dt(sfv_ctx *c, int64_t first, int64_t count, double *out) {
+    if (!c || (!out && count)) return SFV_ERR_ARG;
+    long long done = 0;
+    sfv_status s = hist_range(c, first, count, &done);
+    if (s != SFV_OK) return s;
+    const long long cap = c->cfg.max_history;
+    for (long long q = 0; q < count; ++q)
+        CK(cudaMemcpy(out + q, c->dt_hist + (first + q) % cap, 8, cudaMemcpyDeviceToHost));
+    return check_device_error(c);
+}
+
+sfv_status sfv_get_state(sfv_ctx *c, double *U) {
+    if (!c || !U) return SFV_ERR_ARG;
+    if (!c->have_state) return fail(c, SFV_ERR_SEQUENCE, "no state");
+    CK(cudaStreamSynchronize(c->st));
+    sfv_status s = check_device_error(c);
+    if (s != SFV_OK) return s;
+    const int NI = c->cfg.ni;
+    if (c->nranks == 1) {
+        for (Block &b : c->blocks) {
+            CK(launch_gather(b.buf[0], b.stage, b.ni, b.nj, b.PJ, c->st));
+            CK(cudaMemcpy2DAsync(U + ((size_t)b.j0 * NI + b.i0) * 4, (size_t)NI * 32, b.stage, (size_t)b.ni * 32,
+                                 (size_t)b.ni * 32, b.nj, cudaMemcpyDeviceToHost, c->st));
+        }
+        CK(cudaStreamSynchronize(c->st));
+        return SFV_OK;
+    }
+    Block &b = c->blocks[0];
+    CK(cudaMemsetAsync(c->gbuf, 0, sizeof(double) * (size_t)c->cfg.ni * c->cfg.nj * 4, c->st));
+    CK(launch_gather(b.buf[0], b.stage, b.ni, b.nj, b.PJ, c->st));
+    CK(cudaMemcpy2DAsync(c->gbuf + ((size_t)b.j0 * NI + b.i0) * 4, (size_t)NI * 32, b.stage, (size_t)b.ni * 32,
+                         (size_t)b.ni * 32, b.nj, cudaMemcpyDeviceToDevice, c->st));
+    NK(nccl().AllReduce(c->gbuf, c->gbuf, (size_t)c->cfg.ni * c->cfg.nj * 4, ncclDouble, ncclSum, c->comm, c->st));
+    CK(cudaMemcpyAsync(U, c->gbuf, sizeof(double) * (size_t)c->cfg.ni * c->cfg.nj * 4, cudaMemcpyDeviceToHost, c->st));
+    CK(cudaStreamSynchronize(c->st));
+    return SFV_OK;
+}
+
+sfv_status sfv_error_info(const sfv_ctx *c, int64_t *out4) {
+    if (!c || !out4) return SFV_ERR_ARG;
+    for (int k = 0; k < 4; ++k) out4[k] = c->einfo[k];
+    return SFV_OK;
+}
+
+sfv_status sfv_launch_info(const sfv_ctx *c, int32_t *out4) {
+    if (!c || !out4 || c->blocks.empty()) return SFV_ERR_ARG;
+    out4[0] = c->blocks[0].nstrips;
+    out4[1] = c->blocks[0].nseg;
+    out4[2] = NT;
+    out4[3] = c->occ;
+    return SFV_OK;
+}
+
+sfv_status sfv_debug_math(sfv_ctx *c, int32_t which, const double *in, double *out, int64_t n) {
+    if (!c || !c->bound) return SFV_ERR_SEQUENCE;
+    CK(launch_debug_math(which, in, out, n, c->st));
+    CK(cudaStreamSynchronize(c->st));
+    return SFV_OK;
+}
+
+const char *sfv_last_error(const sfv_ctx *c) { return c ? c->msg.c_str() : "null ctx"; }
+
+void sfv_destroy(sfv_ctx *c) {
+    if (!c) return;
+    if (c->gexec) cudaGraphExecDestroy(c->gexec);
+    if (c->ev0) cudaEventDestroy(c->ev0);
+    if (c->ev1) cudaEventDestroy(c->ev1);
+    if (c->comm && nccl().ok) nccl().CommDestroy(c->comm);
+    delete c;
+}
+
+}  // extern "C"

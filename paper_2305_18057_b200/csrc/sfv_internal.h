@@ -1,0 +1,86 @@
+// sfv_internal.h -- shared host/device declarations of libsfv (product path).
+// Not part of the C ABI (include/sfv.h is).  No code here is shared with the
+// oracle (oracle/), which is test infrastructure.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace sfv {
+
+// Device layout of one block's state buffer ("[i][c][j]", j fastest):
+//   element (i, j, c) at ((i + 2) * 4 + c) * PJ + (j + JOFF),
+//   i in [-2, ni+2), j in [-2, nj+2), c = rho, rho u, rho v, rho E.
+// The partitioned index i is the slow one, so the 2 edge rows of an i-cut
+// are one contiguous run (zero-copy halo send/recv).
+// Metrics: row r in [0, ni] holds 7 fields, each PJ doubles at column
+// j + JOFF: i-face (r, j) nx, ny, A; j-face (r, j) nx, ny, A; 1/V(r, j).
+constexpr int JOFF = 4;
+constexpr int NMET = 7;
+constexpr int SMEM_ROW = 132;     // doubles per staged row in shared memory
+constexpr int ROW_COLS = 130;     // columns staged per row: j0-2 .. j0+127
+constexpr int NT = 128;           // threads per CTA of the stage kernel
+
+
+enum Mode { M_OWN = 0, M_UN = 1, M_RK4F = 2, M_HEUNF = 3 };
+enum Edge { E_INFLOW = 0, E_OUTFLOW = 1, E_SLIP = 2, E_CONNECTED = 3 };
+
+struct Params {
+    double gamma, gm1;
+    double c1, c2;          // eps(1-kappa)/4, eps(1+kappa)/4 (Eq. 7)
+    double delta;           // limiter guard
+    double heps, hinv;      // Harten eps and 0.5/eps
+    double cfl, dt_fixed;
+    int limiter;
+};
+
+struct StageArgs {
+    const double *in;       // stage input (stencil)
+    double *out;            // stage output
+    const double *pw0, *pw1, *pw2;   // pointwise inputs (U^n, W2, W3)
+    const double *met;
+    int ni, nj, PJ;
+    int gi0, gj0, NI, NJ;
+    int nstrips, nseg;
+    int bc[4];              // Edge per W, E, S, N
+    double coef;            // this stage's dt multiplier
+    double *sig;            // [2] max over cells of sigma/V (bits, atomicMax)
+    long long *step_ctr;
+    double *dt_hist;        // [cap]
+    double *norm_hist;      // [cap][nblocks][8]
+    int cap, block_id, nblocks;
+    double *partials;       // [ncta][8]
+    unsigned int *ticket;
+    unsigned long long *err;
+    int stage, nstages;
+    int lead, bump;
+    Params P;
+};
+
+struct MetricsArgs {
+    const double *x, *y;    // block-local nodes (nj+1) x (ni+1), [j][i]
+    double *met;
+    int ni, nj, PJ;
+    unsigned long long *bad;  // smallest j*ni+i with V <= 0 (block-local)
+};
+
+// launchers (sfv_kernels.cu); all asynchronous on `st`
+cudaError_t launch_stage(const StageArgs &a, int mode, bool norms, bool dtmax, cudaStream_t st);
+cudaError_t stage_occupancy(int mode, bool norms, bool dtmax, int *ctas_per_sm);
+cudaError_t prepare_stage_kernels();
+size_t stage_smem_bytes(int mode);
+cudaError_t launch_metrics(const MetricsArgs &a, cudaStream_t st);
+cudaError_t launch_fill(double *buf, long long n, double v, cudaStream_t st);
+cudaError_t launch_poison_corners(double *buf, int ni, int nj, int PJ, cudaStream_t st);
+cudaError_t launch_bc_fill(double *buf, const double *met, int ni, int nj, int PJ, const int bc[4],
+                           const double inflow[4][4], cudaStream_t st);
+cudaError_t launch_scatter(const double *stage_jik, double *buf, int ni, int nj, int PJ, cudaStream_t st);
+cudaError_t launch_gather(const double *buf, double *stage_jik, int ni, int nj, int PJ, cudaStream_t st);
+cudaError_t launch_check_state(const double *buf, int ni, int nj, int PJ, int gi0, int gj0, int NI,
+                               unsigned long long *err, cudaStream_t st);
+cudaError_t launch_sigma(const double *buf, const double *met, int ni, int nj, int PJ, Params P,
+                         double *sig, cudaStream_t st);
+cudaError_t launch_pack_cols(const double *buf, double *dst, int ni, int PJ, int j_first, cudaStream_t st);
+cudaError_t launch_unpack_cols(const double *src, double *buf, int ni, int PJ, int j_first, cudaStream_t st);
+cudaError_t launch_debug_math(int which, const double *in, double *out, long long n, cudaStream_t st);
+
+}  // namespace sfv

@@ -1,0 +1,833 @@
+// sfv_kernels.cu -- sm_100a kernels of the SENSEI finite-volume hot path.
+//
+// The stage kernel fuses, for one explicit RK stage (Eq. 6)
+// over one block: limiter + MUSCL extrapolation (Eq. 7),
+// the Roe/Harten face flux (Eq. 2 normal flux; readings
+// A-R1, A-R2), the flux-difference residual (Eq. 5), the
+// stage update, the physical-boundary ghost writes of the new state
+// (PAPER.md:138-139), the residual-norm partials ("residual print",
+// PAPER.md:120) and the CFL reduction for the next step (reading A-R6).
+//
+// Design: a CTA of NT threads owns a strip of up to NT-2
+// contiguous j columns (+1 halo column each side) and marches along i over
+// a segment of rows.  Each row (state, metrics, pointwise RK inputs) is
+// staged into a 4-slot shared-memory ring by cp.async.bulk (TMA bulk copies,
+// mbarrier completion) issued by one thread, 3 rows ahead of use.  Along i
+// every thread keeps its column's stencil window in registers, so each
+// i-face flux is evaluated once and carried to the next row; along j the
+// face states and fluxes are exchanged through shared memory, so each j-face
+// is evaluated once too.  Each limiter value Psi is computed once per cell,
+// direction and component (the paper's §5 de-duplication),
+// on chip.
+#include "sfv_internal.h"
+
+#include <cstdio>
+
+namespace sfv {
+
+// --------------------------------------------------------------- PTX helpers
+__device__ __forceinline__ unsigned smem_u32(const void *p) {
+    return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t *bar, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, unsigned parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "SFV_WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra SFV_WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, unsigned bytes, uint64_t *bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+
+// Fast reciprocal / reciprocal square root: MUFU seed + one cubic-convergent
+// correction (relative error ~ seed^3 << 2^-53, i.e. within ~1 ulp).
+__device__ __forceinline__ double frcp(double d) {
+    double y;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(d));
+    double e = fma(-d, y, 1.0);
+    return fma(y, fma(e, e, e), y);
+}
+__device__ __forceinline__ double frsqrt(double x) {
+    double y;
+    asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+    double e = fma(-(x * y), y, 1.0);          // 1 - x y^2
+    return fma(y * e, fma(0.375, e, 0.5), y);  // y (1 + e/2 + 3e^2/8)
+}
+
+__device__ __forceinline__ unsigned long long err_key(long long n, int nstages, int stage, int phase,
+                                                      long long cell) {
+    return ((unsigned long long)((n * nstages + (stage - 1)) * 2 + phase) << 32) | (unsigned long long)cell;
+}
+
+// ------------------------------------------------------- MUSCL (Eq. 7)
+// For one cell and one direction, component by component: centre value w,
+// backward difference b = w - w_prev, forward difference f = w_next - w.
+// Returns qU (state at the cell's upper face, +1/2) and qD (lower face, -1/2):
+//   qU = w + c1 psi(f,b) b + c2 psi(b,f) f
+//   qD = w - c2 psi(f,b) b - c1 psi(b,f) f
+// with psi(a,b) the limiter value for difference b given neighbour a
+// (reading A-R4).  For VA1 both psi(f,b) b and psi(b,f) f share one
+// denominator b^2 + f^2 + delta: one reciprocal per cell, direction and
+// component.
+__device__ __forceinline__ void muscl_cell(double w, double b, double f, const Params &P, double &qU,
+                                           double &qD) {
+    double pb, pf;  // psi(f,b)*b, psi(b,f)*f
+    if (P.limiter == 0) {
+        double bf = b * f;
+        double r = frcp(fma(b, b, fma(f, f, P.delta)));
+        double bfd = bf + P.delta;
+        pb = fma(f, f, bfd) * b * r;
+        pf = fma(b, b, bfd) * f * r;
+        if (bf < 0.0) { pb = 0.0; pf = 0.0; }
+    } else if (P.limiter == 1) {
+        double bf = b * f;
+        double s = fma(2.0, bf, P.delta) * frcp(fma(b, b, fma(f, f, P.delta)));
+        s = s > 0.0 ? s : 0.0;
+        pb = s * b;
+        pf = s * f;
+    } else {
+        pb = b;
+        pf = f;
+    }
+    qU = fma(P.c1, pb, fma(P.c2, pf, w));
+    qD = fma(-P.c2, pb, fma(-P.c1, pf, w));
+}
+
+// ------------------------------------------------- Roe + Harten face flux
+// Flux through a face of area A with unit normal (nx, ny), times A
+// (eigenvector form re-associated into the compact
+// dissipation form; Roe averages with sqrt(rho) weights from one rsqrt per
+// side).  Returns false if rho <= 0, p <= 0 or a~^2 <= 0 on either side.
+__device__ __forceinline__ bool roe_flux(const double qL[4], const double qR[4], double nx, double ny,
+                                         double A, const Params &P, double G[4]) {
+    const double gm1 = P.gm1;
+    const double rsL = frsqrt(qL[0]), rsR = frsqrt(qR[0]);
+    const double irL = rsL * rsL, irR = rsR * rsR;
+    const double uL = qL[1] * irL, vL = qL[2] * irL;
+    const double uR = qR[1] * irR, vR = qR[2] * irR;
+    const double pL = gm1 * fma(-0.5, fma(qL[1], uL, qL[2] * vL), qL[3]);
+    const double pR = gm1 * fma(-0.5, fma(qR[1], uR, qR[2] * vR), qR[3]);
+    const double VnL = fma(uL, nx, vL * ny), VnR = fma(uR, nx, vR * ny);
+    const double EpL = qL[3] + pL, EpR = qR[3] + pR;
+
+    const double sL = qL[0] * rsL, sR = qR[0] * rsR;
+    const double w = frcp(sL + sR);
+    const double ut = fma(qL[1], rsL, qR[1] * rsR) * w;
+    const double vt = fma(qL[2], rsL, qR[2] * rsR) * w;
+    const double Ht = fma(EpL, rsL, EpR * rsR) * w;
+    const double rhot = sL * sR;
+    const double q2h = 0.5 * fma(ut, ut, vt * vt);
+    const double a2 = gm1 * (Ht - q2h);
+    const bool ok = (qL[0] > 0.0) & (qR[0] > 0.0) & (pL > 0.0) & (pR > 0.0) & (a2 > 0.0);
+    const double ra = frsqrt(a2);
+    const double at = a2 * ra;
+    const double ia2 = ra * ra;
+    const double Vnt = fma(ut, nx, vt * ny);
+
+    const double drho = qR[0] - qL[0], dp = pR - pL, du = uR - uL, dv = vR - vL, dVn = VnR - VnL;
+    const double tt = rhot * at * dVn;
+    const double hia2 = 0.5 * ia2;
+    const double a1 = (dp - tt) * hia2;
+    const double a4 = (dp + tt) * hia2;
+    const double a2w = fma(-dp, ia2, drho);
+
+    double l1 = fabs(Vnt - at);
+    const double l2 = fabs(Vnt);
+    double l4 = fabs(Vnt + at);
+    double dH = P.heps * at, inv2dH;
+    if (dH < 1e-12) {
+        dH = 1e-12;
+        inv2dH = 0.5e12;
+    } else {
+        inv2dH = P.hinv * ra;  // 1/(2 eps a) = (0.5/eps) (1/a)
+    }
+    const double dH2 = dH * dH;
+    if (l1 < dH) l1 = fma(l1, l1, dH2) * inv2dH;
+    if (l4 < dH) l4 = fma(l4, l4, dH2) * inv2dH;
+
+    const double a1l = l1 * a1, a4l = l4 * a4, a2l = l2 * a2w, r = l2 * rhot;
+    const double S = a1l + a4l, Dd = a4l - a1l;
+    const double D0 = S + a2l;
+    const double T = fma(Dd, at, -r * dVn);
+    const double D1 = fma(D0, ut, fma(T, nx, r * du));
+    const double D2 = fma(D0, vt, fma(T, ny, r * dv));
+    const double D3 = fma(S, Ht, fma(a2l, q2h, fma(T, Vnt, r * fma(ut, du, vt * dv))));
+
+    const double ps = pL + pR;
+    const double F0 = fma(qL[0], VnL, qR[0] * VnR);
+    const double F1 = fma(qL[1], VnL, fma(qR[1], VnR, ps * nx));
+    const double F2 = fma(qL[2], VnL, fma(qR[2], VnR, ps * ny));
+    const double F3 = fma(EpL, VnL, EpR * VnR);
+    const double hA = 0.5 * A;
+    G[0] = (F0 - D0) * hA;
+    G[1] = (F1 - D1) * hA;
+    G[2] = (F2 - D2) * hA;
+    G[3] = (F3 - D3) * hA;
+    return ok;
+}
+
+__device__ __forceinline__ void mirror(const double u[4], double nx, double ny, double g[4]) {
+    double mn2 = 2.0 * fma(u[1], nx, u[2] * ny);
+    g[0] = u[0];
+    g[1] = fma(-mn2, nx, u[1]);
+    g[2] = fma(-mn2, ny, u[2]);
+    g[3] = u[3];
+}
+
+__device__ __forceinline__ void store4(double *buf, int PJ, int i, int j, const double u[4]) {
+    double *p = buf + (size_t)((i + 2) * 4) * PJ + (j + JOFF);
+#pragma unroll
+    for (int c = 0; c < 4; ++c) p[(size_t)c * PJ] = u[c];
+}
+
+// ------------------------------------------------------------ stage kernel
+template <int MODE>
+struct StageTraits {
+    static constexpr int NPW = MODE == M_OWN ? 0 : (MODE == M_RK4F ? 3 : 1);
+    static constexpr int NROWS = 4 + NMET + 4 * NPW;
+    static constexpr int SLOT = NROWS * SMEM_ROW;  // doubles per ring slot
+    static constexpr int NS = MODE == M_RK4F ? 4 : 5;  // ring depth (rows in flight)
+};
+
+template <int MODE>
+__host__ __device__ constexpr size_t stage_smem() {
+    return sizeof(double) * ((size_t)StageTraits<MODE>::NS * StageTraits<MODE>::SLOT + 8 * NT + 8 * (NT / 32)) +
+           sizeof(uint64_t) * StageTraits<MODE>::NS;
+}
+
+template <int MODE, bool NORMS, bool DTMAX>
+__global__ void __launch_bounds__(NT) stage_kernel(const StageArgs a) {
+    using TR = StageTraits<MODE>;
+    extern __shared__ __align__(128) double smem[];
+    double *ring = smem;
+    double *xq = ring + TR::NS * TR::SLOT;  // [4][NT] north face states
+    double *xg = xq + 4 * NT;              // [4][NT] south face fluxes
+    double *red = xg + 4 * NT;             // [8][NT/32]
+    uint64_t *bars = reinterpret_cast<uint64_t *>(red + 8 * (NT / 32));
+
+    const Params &P = a.P;
+    const int t = threadIdx.x;
+    const int strip = blockIdx.x % a.nstrips;
+    const int seg = blockIdx.x / a.nstrips;
+    const int j0 = 2 * (int)(((long long)strip * a.nj) / (2 * a.nstrips));
+    const int j1 = (strip + 1 == a.nstrips) ? a.nj : 2 * (int)(((long long)(strip + 1) * a.nj) / (2 * a.nstrips));
+    const int jc = j0 - 1 + t;                         // this thread's column
+    const bool is_out = (t >= 1) && (jc < j1);         // owns output cell (v, jc)
+    const bool jflux = (t >= 1) && (jc <= j1);         // evaluates j-face (v, jc)
+    const bool jrec = (jc <= j1);                      // reconstructs cell (v, jc) along j
+    const int own = t + 1;                             // column index inside a staged row
+    const int i_start = (int)(((long long)a.ni * seg) / a.nseg);
+    const int i_end = (int)(((long long)a.ni * (seg + 1)) / a.nseg);
+    const int r0 = i_start - 2;                        // first staged row
+    const int r_last = i_end + 1;                      // last staged row
+
+    const long long n = *a.step_ctr;
+    const double dt = P.dt_fixed > 0.0 ? P.dt_fixed : P.cfl / a.sig[n & 1];
+    const double coef = a.coef * dt;
+    const int PJ = a.PJ;
+    const size_t col0 = (size_t)(j0 - 2 + JOFF);
+
+    auto slot_of = [&](int r) -> double * { return ring + ((r - r0) % TR::NS) * TR::SLOT; };
+    auto issue = [&](int r) {
+        const int s = (r - r0) % TR::NS;
+        double *dst = ring + s * TR::SLOT;
+        const bool has_met = (r >= 0) && (r <= a.ni);
+        const bool has_pw = TR::NPW > 0 && (r >= 0) && (r < a.ni);
+        unsigned bytes = 4u * ROW_COLS * 8u;
+        if (has_met) bytes += (unsigned)NMET * ROW_COLS * 8u;
+        if (has_pw) bytes += 4u * TR::NPW * ROW_COLS * 8u;
+        mbar_expect_tx(&bars[s], bytes);
+        const double *src = a.in + (size_t)((r + 2) * 4) * PJ + col0;
+#pragma unroll
+        for (int c = 0; c < 4; ++c) bulk_g2s(dst + c * SMEM_ROW, src + (size_t)c * PJ, ROW_COLS * 8u, &bars[s]);
+        if (has_met) {
+            const double *m = a.met + (size_t)(r * NMET) * PJ + col0;
+#pragma unroll
+            for (int f = 0; f < NMET; ++f)
+                bulk_g2s(dst + (4 + f) * SMEM_ROW, m + (size_t)f * PJ, ROW_COLS * 8u, &bars[s]);
+        }
+        if (has_pw) {
+            const double *pws[3] = {a.pw0, a.pw1, a.pw2};
+#pragma unroll
+            for (int p = 0; p < TR::NPW; ++p) {
+                const double *q = pws[p] + (size_t)((r + 2) * 4) * PJ + col0;
+#pragma unroll
+                for (int c = 0; c < 4; ++c)
+                    bulk_g2s(dst + (4 + NMET + 4 * p + c) * SMEM_ROW, q + (size_t)c * PJ, ROW_COLS * 8u, &bars[s]);
+            }
+        }
+    };
+    auto wait_row = [&](int r) { mbar_wait(&bars[(r - r0) % TR::NS], (unsigned)(((r - r0) / TR::NS) & 1)); };
+
+    if (t == 0) {
+        for (int s = 0; s < TR::NS; ++s) mbar_init(&bars[s], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    }
+    __syncthreads();
+    int next_issue = r0;
+    if (t == 0) {
+        for (; next_issue < r0 + TR::NS && next_issue <= r_last; ++next_issue) issue(next_issue);
+    }
+
+    double Wc[4], fp[4], QLp[4], GW[4] = {0, 0, 0, 0}, GE[4] = {0, 0, 0, 0};
+    double nWx = 0.0, nWy = 0.0;  // i-face(0) normal (W-edge slip ghosts)
+    double nrm[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    double smax = 0.0;
+
+    wait_row(r0);
+    wait_row(r0 + 1);
+    {
+        const double *s0 = slot_of(r0), *s1 = slot_of(r0 + 1);
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+            Wc[c] = s1[c * SMEM_ROW + own];
+            fp[c] = Wc[c] - s0[c * SMEM_ROW + own];
+            QLp[c] = 0.0;
+        }
+    }
+    // rows r0, r0+1 are consumed: refill their slots (rows r0+NS, r0+NS+1)
+    __syncthreads();
+    if (t == 0) {
+        for (; next_issue <= r0 + TR::NS + 1 && next_issue <= r_last; ++next_issue) issue(next_issue);
+    }
+
+    for (int v = r0; v < i_end; ++v) {
+        wait_row(v + 2);
+        // ---- i direction: reconstruct cell v+1, flux at face v+1/2 ----------
+        if (is_out) {
+            const double *sn = slot_of(v + 2);
+            double qU[4], qD[4];
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+                const double wn = sn[c * SMEM_ROW + own];
+                const double f = wn - Wc[c];
+                muscl_cell(Wc[c], fp[c], f, P, qU[c], qD[c]);
+                fp[c] = f;
+                Wc[c] = wn;
+            }
+            if (v >= i_start - 1) {
+                const double *m = slot_of(v + 1) + 4 * SMEM_ROW;
+                const double nx = m[0 * SMEM_ROW + own], ny = m[1 * SMEM_ROW + own], A = m[2 * SMEM_ROW + own];
+                if (v == -1) { nWx = nx; nWy = ny; }
+                if (!roe_flux(QLp, qD, nx, ny, A, P, GE)) {
+                    int I = a.gi0 + v + 1;
+                    if (I > a.NI - 1) I = a.NI - 1;
+                    atomicMin(a.err, err_key(n, a.nstages, a.stage, 0, (long long)(a.gj0 + jc) * a.NI + I));
+                }
+            }
+#pragma unroll
+            for (int c = 0; c < 4; ++c) QLp[c] = qU[c];
+        }
+        if (v >= i_start) {
+            // ---- j direction: reconstruct cell (v, jc), exchange, flux ------
+            const double *sv = slot_of(v);
+            const double *mv = sv + 4 * SMEM_ROW;
+            double Wv[4], qS[4];
+            if (jrec) {
+#pragma unroll
+                for (int c = 0; c < 4; ++c) {
+                    const double wm = sv[c * SMEM_ROW + own - 1];
+                    const double w = sv[c * SMEM_ROW + own];
+                    const double wp = sv[c * SMEM_ROW + own + 1];
+                    double qN;
+                    muscl_cell(w, w - wm, wp - w, P, qN, qS[c]);
+                    xq[c * NT + t] = qN;
+                    Wv[c] = w;
+                }
+            }
+            if (v == 0 && is_out) { nWx = mv[0 * SMEM_ROW + own]; nWy = mv[1 * SMEM_ROW + own]; }
+            __syncthreads();
+            if (t == 0) {
+                const int lim = min(v - 1 + TR::NS, r_last);
+                for (; next_issue <= lim; ++next_issue) issue(next_issue);
+            }
+            double GS[4];
+            if (jflux) {
+                double qN[4];
+#pragma unroll
+                for (int c = 0; c < 4; ++c) qN[c] = xq[c * NT + t - 1];
+                const double nx = mv[3 * SMEM_ROW + own], ny = mv[4 * SMEM_ROW + own], A = mv[5 * SMEM_ROW + own];
+                if (!roe_flux(qN, qS, nx, ny, A, P, GS)) {
+                    int J = a.gj0 + jc;
+                    if (J > a.NJ - 1) J = a.NJ - 1;
+                    atomicMin(a.err, err_key(n, a.nstages, a.stage, 0, (long long)J * a.NI + a.gi0 + v));
+                }
+#pragma unroll
+                for (int c = 0; c < 4; ++c) xg[c * NT + t] = GS[c];
+            }
+            __syncthreads();
+            if (is_out) {
+                // ---- residual (Eq. 5) and stage update (Eq. 6) ---------------
+                const double iV = mv[6 * SMEM_ROW + own];
+                double R[4], U[4];
+#pragma unroll
+                for (int c = 0; c < 4; ++c) {
+                    const double GN = xg[c * NT + t + 1];
+                    R[c] = ((GE[c] - GW[c]) + GN) - GS[c];
+                }
+                const double *pwr = sv + (4 + NMET) * SMEM_ROW;
+#pragma unroll
+                for (int c = 0; c < 4; ++c) {
+                    const double rv = R[c] * iV;
+                    if (MODE == M_OWN) {
+                        U[c] = fma(-coef, rv, Wv[c]);
+                    } else if (MODE == M_UN) {
+                        U[c] = fma(-coef, rv, pwr[c * SMEM_ROW + own]);
+                    } else if (MODE == M_RK4F) {
+                        const double un = pwr[c * SMEM_ROW + own];
+                        const double d2 = pwr[(4 + c) * SMEM_ROW + own] - un;
+                        const double d3 = pwr[(8 + c) * SMEM_ROW + own] - un;
+                        const double d4 = Wv[c] - un;
+                        const double comb = (fma(2.0, d3, d2) + d4) * (1.0 / 3.0);
+                        U[c] = un + fma(-coef, rv, comb);
+                    } else {  // M_HEUNF
+                        const double un = pwr[c * SMEM_ROW + own];
+                        U[c] = un + fma(-coef, rv, 0.5 * (Wv[c] - un));
+                    }
+                }
+                store4(a.out, PJ, v, jc, U);
+                // new-state validity: rho > 0 and 2 rho E > |m|^2 (<=> p > 0)
+                if (!((U[0] > 0.0) & (2.0 * U[0] * U[3] > fma(U[1], U[1], U[2] * U[2]))))
+                    atomicMin(a.err, err_key(n, a.nstages, a.stage, 1,
+                                             (long long)(a.gj0 + jc) * a.NI + a.gi0 + v));
+                // physical-boundary ghosts of the new state (reading A-R11)
+                if (a.bc[2] == E_SLIP && jc <= 1) {
+                    double g[4];
+                    const int k0 = own - jc;  // column 0
+                    mirror(U, mv[3 * SMEM_ROW + k0], mv[4 * SMEM_ROW + k0], g);
+                    store4(a.out, PJ, v, -1 - jc, g);
+                } else if (a.bc[2] == E_OUTFLOW && jc == 0) {
+                    store4(a.out, PJ, v, -1, U);
+                    store4(a.out, PJ, v, -2, U);
+                }
+                if (a.bc[3] == E_SLIP && jc >= a.nj - 2) {
+                    double g[4];
+                    const int kN = own + (a.nj - jc);  // column nj
+                    mirror(U, mv[3 * SMEM_ROW + kN], mv[4 * SMEM_ROW + kN], g);
+                    store4(a.out, PJ, v, a.nj + (a.nj - 1 - jc), g);
+                } else if (a.bc[3] == E_OUTFLOW && jc == a.nj - 1) {
+                    store4(a.out, PJ, v, a.nj, U);
+                    store4(a.out, PJ, v, a.nj + 1, U);
+                }
+                if (a.bc[0] == E_SLIP && v <= 1) {
+                    double g[4];
+                    mirror(U, nWx, nWy, g);
+                    store4(a.out, PJ, -1 - v, jc, g);
+                } else if (a.bc[0] == E_OUTFLOW && v == 0) {
+                    store4(a.out, PJ, -1, jc, U);
+                    store4(a.out, PJ, -2, jc, U);
+                }
+                if (a.bc[1] == E_SLIP && v >= a.ni - 2) {
+                    double g[4];
+                    const double *mE = slot_of(a.ni) + 4 * SMEM_ROW;  // resident: ni <= v+2
+                    mirror(U, mE[0 * SMEM_ROW + own], mE[1 * SMEM_ROW + own], g);
+                    store4(a.out, PJ, a.ni + (a.ni - 1 - v), jc, g);
+                } else if (a.bc[1] == E_OUTFLOW && v == a.ni - 1) {
+                    store4(a.out, PJ, a.ni, jc, U);
+                    store4(a.out, PJ, a.ni + 1, jc, U);
+                }
+                if (NORMS) {
+#pragma unroll
+                    for (int c = 0; c < 4; ++c) {
+                        nrm[c] = fma(R[c], R[c], nrm[c]);
+                        nrm[4 + c] = fmax(nrm[4 + c], fabs(R[c]));
+                    }
+                }
+                if (DTMAX) {
+                    // sigma/V of the new state for dt_{n+1} (reading A-R6)
+                    const double ir = frcp(U[0]);
+                    const double u = U[1] * ir, vv = U[2] * ir;
+                    const double p = P.gm1 * fma(-0.5, fma(U[1], u, U[2] * vv), U[3]);
+                    const double x = P.gamma * p * ir;
+                    const double snd = x * frsqrt(x);
+                    const double *m1 = slot_of(v + 1) + 4 * SMEM_ROW;
+                    const double tW = (fabs(fma(u, mv[0 * SMEM_ROW + own], vv * mv[1 * SMEM_ROW + own])) + snd) *
+                                      mv[2 * SMEM_ROW + own];
+                    const double tE = (fabs(fma(u, m1[0 * SMEM_ROW + own], vv * m1[1 * SMEM_ROW + own])) + snd) *
+                                      m1[2 * SMEM_ROW + own];
+                    const double tS = (fabs(fma(u, mv[3 * SMEM_ROW + own], vv * mv[4 * SMEM_ROW + own])) + snd) *
+                                      mv[5 * SMEM_ROW + own];
+                    const double tN =
+                        (fabs(fma(u, mv[3 * SMEM_ROW + own + 1], vv * mv[4 * SMEM_ROW + own + 1])) + snd) *
+                        mv[5 * SMEM_ROW + own + 1];
+                    smax = fmax(smax, (((tW + tE) + tS) + tN) * iV);
+                }
+            }
+        }
+#pragma unroll
+        for (int c = 0; c < 4; ++c) GW[c] = GE[c];
+    }
+
+    // ---- CTA reductions --------------------------------------------------
+    const int warp = t >> 5, lane = t & 31;
+    const unsigned ncta = gridDim.x;
+    if (DTMAX) {
+        for (int o = 16; o > 0; o >>= 1) smax = fmax(smax, __shfl_xor_sync(0xffffffffu, smax, o));
+        if (lane == 0) red[warp] = smax;
+        __syncthreads();
+        if (t == 0) {
+            double m = red[0];
+            for (int w = 1; w < NT / 32; ++w) m = fmax(m, red[w]);
+            atomicMax(reinterpret_cast<unsigned long long *>(&a.sig[(n + 1) & 1]),
+                      (unsigned long long)__double_as_longlong(m));
+        }
+        __syncthreads();
+    }
+    if (NORMS) {
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+            double x = nrm[q];
+            for (int o = 16; o > 0; o >>= 1) {
+                double y = __shfl_xor_sync(0xffffffffu, x, o);
+                x = q < 4 ? x + y : fmax(x, y);
+            }
+            if (lane == 0) red[q * (NT / 32) + warp] = x;
+        }
+        __syncthreads();
+        if (t < 8) {
+            double x = red[t * (NT / 32)];
+            for (int w = 1; w < NT / 32; ++w) x = t < 4 ? x + red[t * (NT / 32) + w] : fmax(x, red[t * (NT / 32) + w]);
+            a.partials[(size_t)blockIdx.x * 8 + t] = x;
+        }
+    }
+    // ---- last-CTA epilogue: norms finalize, dt record, step counter ---------
+    if (NORMS || a.bump) {
+        __shared__ unsigned s_last;
+        __threadfence();
+        __syncthreads();
+        if (t == 0) s_last = (atomicAdd(a.ticket, 1u) == ncta - 1);
+        __syncthreads();
+        if (s_last) {
+            __threadfence();
+            if (NORMS) {
+                // deterministic: fixed strided assignment, fixed-order tree
+                double acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+                for (unsigned b = t; b < ncta; b += NT) {
+#pragma unroll
+                    for (int q = 0; q < 8; ++q) {
+                        const double x = __ldcg(&a.partials[(size_t)b * 8 + q]);
+                        acc[q] = q < 4 ? acc[q] + x : fmax(acc[q], x);
+                    }
+                }
+                double *tree = xq;  // reuse: [8][NT]
+                __syncthreads();
+#pragma unroll
+                for (int q = 0; q < 8; ++q) tree[q * NT + t] = acc[q];
+                __syncthreads();
+                for (int s = NT / 2; s > 0; s >>= 1) {
+                    if (t < s) {
+#pragma unroll
+                        for (int q = 0; q < 8; ++q)
+                            tree[q * NT + t] = q < 4 ? tree[q * NT + t] + tree[q * NT + t + s]
+                                                     : fmax(tree[q * NT + t], tree[q * NT + t + s]);
+                    }
+                    __syncthreads();
+                }
+                if (t < 8) a.norm_hist[((size_t)(n % a.cap) * a.nblocks + a.block_id) * 8 + t] = tree[t * NT];
+                if (t == 0 && a.lead) {
+                    a.dt_hist[n % a.cap] = dt;
+                    if (!(P.dt_fixed > 0.0)) a.sig[(n + 1) & 1] = 0.0;
+                }
+            }
+            if (t == 0) {
+                if (a.bump) *a.step_ctr = n + 1;
+                *a.ticket = 0u;
+            }
+        }
+    }
+}
+
+template <int MODE, bool NORMS, bool DTMAX>
+static cudaError_t launch_t(const StageArgs &a, cudaStream_t st) {
+    auto k = stage_kernel<MODE, NORMS, DTMAX>;
+    const size_t sm = stage_smem<MODE>();  // attribute set by prepare_stage_kernels()
+    k<<<a.nstrips * a.nseg, NT, sm, st>>>(a);
+    return cudaGetLastError();
+}
+
+template <int MODE, bool NORMS, bool DTMAX>
+static cudaError_t occ_t(int *n) {
+    auto k = stage_kernel<MODE, NORMS, DTMAX>;
+    const size_t sm = stage_smem<MODE>();
+    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    if (e != cudaSuccess) return e;
+    return cudaOccupancyMaxActiveBlocksPerMultiprocessor(n, k, NT, sm);
+}
+
+#define SFV_DISPATCH(FN, ...)                                                         \
+    switch (mode * 4 + (norms ? 2 : 0) + (dtmax ? 1 : 0)) {                          \
+        case M_OWN * 4 + 2: return FN<M_OWN, true, false>(__VA_ARGS__);              \
+        case M_OWN * 4 + 0: return FN<M_OWN, false, false>(__VA_ARGS__);             \
+        case M_UN * 4 + 0: return FN<M_UN, false, false>(__VA_ARGS__);               \
+        case M_UN * 4 + 1: return FN<M_UN, false, true>(__VA_ARGS__);                \
+        case M_RK4F * 4 + 1: return FN<M_RK4F, false, true>(__VA_ARGS__);            \
+        case M_RK4F * 4 + 0: return FN<M_RK4F, false, false>(__VA_ARGS__);           \
+        case M_HEUNF * 4 + 1: return FN<M_HEUNF, false, true>(__VA_ARGS__);          \
+        case M_HEUNF * 4 + 0: return FN<M_HEUNF, false, false>(__VA_ARGS__);         \
+        default: return cudaErrorInvalidValue;                                       \
+    }
+
+cudaError_t launch_stage(const StageArgs &a, int mode, bool norms, bool dtmax, cudaStream_t st) {
+    SFV_DISPATCH(launch_t, a, st)
+}
+cudaError_t stage_occupancy(int mode, bool norms, bool dtmax, int *n) { SFV_DISPATCH(occ_t, n) }
+cudaError_t prepare_stage_kernels() {
+    const int variants[8][3] = {{M_OWN, 1, 0}, {M_OWN, 0, 0}, {M_UN, 0, 0}, {M_UN, 0, 1},
+                                {M_RK4F, 0, 1}, {M_RK4F, 0, 0}, {M_HEUNF, 0, 1}, {M_HEUNF, 0, 0}};
+    for (auto &v : variants) {
+        int n = 0;
+        cudaError_t e = stage_occupancy(v[0], v[1] != 0, v[2] != 0, &n);
+        if (e != cudaSuccess) return e;
+    }
+    return cudaSuccess;
+}
+size_t stage_smem_bytes(int mode) {
+    switch (mode) {
+        case M_OWN: return stage_smem<M_OWN>();
+        case M_UN: return stage_smem<M_UN>();
+        case M_RK4F: return stage_smem<M_RK4F>();
+        default: return stage_smem<M_HEUNF>();
+    }
+}
+
+// ------------------------------------------------------------------ metrics
+// IEEE round-to-nearest intrinsics, no contraction: the same arithmetic as
+// the paper's metric definitions.
+__global__ void metrics_kernel(const MetricsArgs a) {
+    const int j = blockIdx.x * blockDim.x + threadIdx.x;  // node column
+    const int i = blockIdx.y;                             // node row
+    if (j > a.nj) return;
+    const int W = a.ni + 1;
+    auto X = [&](int ii, int jj) { return a.x[(size_t)jj * W + ii]; };
+    auto Y = [&](int ii, int jj) { return a.y[(size_t)jj * W + ii]; };
+    double *row = a.met + (size_t)(i * NMET) * a.PJ + (j + JOFF);
+    if (j < a.nj) {  // i-face (i, j)
+        const double tx = __dsub_rn(X(i, j + 1), X(i, j)), ty = __dsub_rn(Y(i, j + 1), Y(i, j));
+        const double A = __dsqrt_rn(__dadd_rn(__dmul_rn(tx, tx), __dmul_rn(ty, ty)));
+        row[0 * (size_t)a.PJ] = __ddiv_rn(ty, A);
+        row[1 * (size_t)a.PJ] = __ddiv_rn(-tx, A);
+        row[2 * (size_t)a.PJ] = A;
+    }
+    if (i < a.ni) {  // j-face (i, j)
+        const double tx = __dsub_rn(X(i + 1, j), X(i, j)), ty = __dsub_rn(Y(i + 1, j), Y(i, j));
+        const double A = __dsqrt_rn(__dadd_rn(__dmul_rn(tx, tx), __dmul_rn(ty, ty)));
+        row[3 * (size_t)a.PJ] = __ddiv_rn(-ty, A);
+        row[4 * (size_t)a.PJ] = __ddiv_rn(tx, A);
+        row[5 * (size_t)a.PJ] = A;
+        if (j < a.nj) {
+            const double V = __dmul_rn(
+                0.5, __dsub_rn(__dmul_rn(__dsub_rn(X(i + 1, j + 1), X(i, j)), __dsub_rn(Y(i, j + 1), Y(i + 1, j))),
+                               __dmul_rn(__dsub_rn(Y(i + 1, j + 1), Y(i, j)), __dsub_rn(X(i, j + 1), X(i + 1, j)))));
+            row[6 * (size_t)a.PJ] = __ddiv_rn(1.0, V);
+            if (!(V > 0.0)) atomicMin(a.bad, (unsigned long long)((long long)j * a.ni + i));
+        }
+    }
+}
+
+cudaError_t launch_metrics(const MetricsArgs &a, cudaStream_t st) {
+    dim3 g((a.nj + 1 + 127) / 128, a.ni + 1);
+    metrics_kernel<<<g, 128, 0, st>>>(a);
+    return cudaGetLastError();
+}
+
+// --------------------------------------------------------- init / transpose
+__global__ void fill_kernel(double *p, long long n, double v) {
+    for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < n; k += (long long)gridDim.x * blockDim.x)
+        p[k] = v;
+}
+cudaError_t launch_fill(double *buf, long long n, double v, cudaStream_t st) {
+    fill_kernel<<<592, 256, 0, st>>>(buf, n, v);
+    return cudaGetLastError();
+}
+
+// Corner ghosts (both indices outside the interior) are never read by the
+// dimension-split stencil (reading A-R18); NaN makes any read visible.
+__global__ void corners_kernel(double *buf, int ni, int nj, int PJ) {
+    const int j = blockIdx.x * blockDim.x + threadIdx.x - 2;  // -2 .. nj+1
+    const int i = blockIdx.y - 2;
+    if (j > nj + 1) return;
+    const bool iout = i < 0 || i >= ni, jout = j < 0 || j >= nj;
+    if (!(iout && jout)) return;
+    const double nan = __longlong_as_double(0x7ff8000000000000LL);
+    for (int c = 0; c < 4; ++c) buf[(size_t)((i + 2) * 4 + c) * PJ + j + JOFF] = nan;
+}
+cudaError_t launch_poison_corners(double *buf, int ni, int nj, int PJ, cudaStream_t st) {
+    dim3 g((nj + 4 + 127) / 128, ni + 4);
+    corners_kernel<<<g, 128, 0, st>>>(buf, ni, nj, PJ);
+    return cudaGetLastError();
+}
+
+// Physical-edge ghost fill of a whole buffer (used at set_state; during
+// stepping the stage kernel writes these ghosts itself).  Same rules as
+// SURVEY §8(c).2 step 2.
+__global__ void bc_fill_kernel(double *buf, const double *met, int ni, int nj, int PJ, int4 bc, double4 in0,
+                               double4 in1, double4 in2, double4 in3) {
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    const int m = blockIdx.y;  // layer 0/1
+    auto ld = [&](int i, int j, double u[4]) {
+        for (int c = 0; c < 4; ++c) u[c] = buf[(size_t)((i + 2) * 4 + c) * PJ + j + JOFF];
+    };
+    auto st = [&](int i, int j, const double u[4]) {
+        for (int c = 0; c < 4; ++c) buf[(size_t)((i + 2) * 4 + c) * PJ + j + JOFF] = u[c];
+    };
+    auto metv = [&](int r, int f, int j) { return met[(size_t)(r * NMET + f) * PJ + j + JOFF]; };
+    double u[4], g[4];
+    if (k < nj) {  // W and E edges, column k
+        const int j = k;
+        if (bc.x == E_INFLOW) { double q[4] = {in0.x, in0.y, in0.z, in0.w}; st(-1 - m, j, q); }
+        else if (bc.x == E_OUTFLOW) { ld(0, j, u); st(-1 - m, j, u); }
+        else if (bc.x == E_SLIP) { ld(m, j, u); mirror(u, metv(0, 0, j), metv(0, 1, j), g); st(-1 - m, j, g); }
+        if (bc.y == E_INFLOW) { double q[4] = {in1.x, in1.y, in1.z, in1.w}; st(ni + m, j, q); }
+        else if (bc.y == E_OUTFLOW) { ld(ni - 1, j, u); st(ni + m, j, u); }
+        else if (bc.y == E_SLIP) { ld(ni - 1 - m, j, u); mirror(u, metv(ni, 0, j), metv(ni, 1, j), g); st(ni + m, j, g); }
+    }
+    if (k < ni) {  // S and N edges, row k
+        const int i = k;
+        if (bc.z == E_INFLOW) { double q[4] = {in2.x, in2.y, in2.z, in2.w}; st(i, -1 - m, q); }
+        else if (bc.z == E_OUTFLOW) { ld(i, 0, u); st(i, -1 - m, u); }
+        else if (bc.z == E_SLIP) { ld(i, m, u); mirror(u, metv(i, 3, 0), metv(i, 4, 0), g); st(i, -1 - m, g); }
+        if (bc.w == E_INFLOW) { double q[4] = {in3.x, in3.y, in3.z, in3.w}; st(i, nj + m, q); }
+        else if (bc.w == E_OUTFLOW) { ld(i, nj - 1, u); st(i, nj + m, u); }
+        else if (bc.w == E_SLIP) { ld(i, nj - 1 - m, u); mirror(u, metv(i, 3, nj), metv(i, 4, nj), g); st(i, nj + m, g); }
+    }
+}
+cudaError_t launch_bc_fill(double *buf, const double *met, int ni, int nj, int PJ, const int bc[4],
+                           const double in[4][4], cudaStream_t st) {
+    const int n = ni > nj ? ni : nj;
+    dim3 g((n + 127) / 128, 2);
+    bc_fill_kernel<<<g, 128, 0, st>>>(buf, met, ni, nj, PJ, make_int4(bc[0], bc[1], bc[2], bc[3]),
+                                      make_double4(in[0][0], in[0][1], in[0][2], in[0][3]),
+                                      make_double4(in[1][0], in[1][1], in[1][2], in[1][3]),
+                                      make_double4(in[2][0], in[2][1], in[2][2], in[2][3]),
+                                      make_double4(in[3][0], in[3][1], in[3][2], in[3][3]));
+    return cudaGetLastError();
+}
+
+// staging [j][i][4] <-> layout [i][c][j]
+__global__ void scatter_kernel(const double *s, double *buf, int ni, int nj, int PJ) {
+    const int j = blockIdx.x * blockDim.x + threadIdx.x, i = blockIdx.y;
+    if (j >= nj) return;
+    for (int c = 0; c < 4; ++c) buf[(size_t)((i + 2) * 4 + c) * PJ + j + JOFF] = s[((size_t)j * ni + i) * 4 + c];
+}
+__global__ void gather_kernel(const double *buf, double *s, int ni, int nj, int PJ) {
+    const int j = blockIdx.x * blockDim.x + threadIdx.x, i = blockIdx.y;
+    if (j >= nj) return;
+    for (int c = 0; c < 4; ++c) s[((size_t)j * ni + i) * 4 + c] = buf[(size_t)((i + 2) * 4 + c) * PJ + j + JOFF];
+}
+cudaError_t launch_scatter(const double *s, double *buf, int ni, int nj, int PJ, cudaStream_t st) {
+    dim3 g((nj + 127) / 128, ni);
+    scatter_kernel<<<g, 128, 0, st>>>(s, buf, ni, nj, PJ);
+    return cudaGetLastError();
+}
+cudaError_t launch_gather(const double *buf, double *s, int ni, int nj, int PJ, cudaStream_t st) {
+    dim3 g((nj + 127) / 128, ni);
+    gather_kernel<<<g, 128, 0, st>>>(buf, s, ni, nj, PJ);
+    return cudaGetLastError();
+}
+
+// rho > 0 and p > 0 for an initial state (exact test as the oracle: p from
+// u = m/rho); smallest global cell index into *err (key phase 0, stage 0).
+__global__ void check_state_kernel(const double *buf, int ni, int nj, int PJ, int gi0, int gj0, int NI,
+                                   unsigned long long *err) {
+    const int j = blockIdx.x * blockDim.x + threadIdx.x, i = blockIdx.y;
+    if (j >= nj) return;
+    double u[4];
+    for (int c = 0; c < 4; ++c) u[c] = buf[(size_t)((i + 2) * 4 + c) * PJ + j + JOFF];
+    bool ok = u[0] > 0.0;
+    if (ok) {
+        const double uu = u[1] / u[0], vv = u[2] / u[0];
+        ok = (u[3] - 0.5 * u[0] * (uu * uu + vv * vv)) > 0.0;
+    }
+    if (!ok) atomicMin(err, (unsigned long long)((long long)(gj0 + j) * NI + gi0 + i));
+}
+cudaError_t launch_check_state(const double *buf, int ni, int nj, int PJ, int gi0, int gj0, int NI,
+                               unsigned long long *err, cudaStream_t st) {
+    dim3 g((nj + 127) / 128, ni);
+    check_state_kernel<<<g, 128, 0, st>>>(buf, ni, nj, PJ, gi0, gj0, NI, err);
+    return cudaGetLastError();
+}
+
+// max over cells of sigma/V for dt_0 (set_state); atomicMax into *sig.
+__global__ void sigma_kernel(const double *buf, const double *met, int ni, int nj, int PJ, Params P, double *sig) {
+    const int j = blockIdx.x * blockDim.x + threadIdx.x, i = blockIdx.y;
+    double s = 0.0;
+    if (j < nj) {
+        double U[4];
+        for (int c = 0; c < 4; ++c) U[c] = buf[(size_t)((i + 2) * 4 + c) * PJ + j + JOFF];
+        auto m = [&](int r, int f, int jj) { return met[(size_t)(r * NMET + f) * PJ + jj + JOFF]; };
+        const double ir = frcp(U[0]);
+        const double u = U[1] * ir, vv = U[2] * ir;
+        const double p = P.gm1 * fma(-0.5, fma(U[1], u, U[2] * vv), U[3]);
+        const double x = P.gamma * p * ir;
+        const double snd = x * frsqrt(x);
+        const double tW = (fabs(fma(u, m(i, 0, j), vv * m(i, 1, j))) + snd) * m(i, 2, j);
+        const double tE = (fabs(fma(u, m(i + 1, 0, j), vv * m(i + 1, 1, j))) + snd) * m(i + 1, 2, j);
+        const double tS = (fabs(fma(u, m(i, 3, j), vv * m(i, 4, j))) + snd) * m(i, 5, j);
+        const double tN = (fabs(fma(u, m(i, 3, j + 1), vv * m(i, 4, j + 1))) + snd) * m(i, 5, j + 1);
+        s = (((tW + tE) + tS) + tN) * m(i, 6, j);
+    }
+    for (int o = 16; o > 0; o >>= 1) s = fmax(s, __shfl_xor_sync(0xffffffffu, s, o));
+    if ((threadIdx.x & 31) == 0 && s > 0.0)
+        atomicMax(reinterpret_cast<unsigned long long *>(sig), (unsigned long long)__double_as_longlong(s));
+}
+cudaError_t launch_sigma(const double *buf, const double *met, int ni, int nj, int PJ, Params P, double *sig,
+                         cudaStream_t st) {
+    dim3 g((nj + 127) / 128, ni);
+    sigma_kernel<<<g, 128, 0, st>>>(buf, met, ni, nj, PJ, P, sig);
+    return cudaGetLastError();
+}
+
+// j-cut halo pack / unpack (NCCL path): 2 columns starting at j_first,
+// rows i in [0, ni), 4 components -> contiguous [i][c][2].
+__global__ void pack_cols_kernel(const double *buf, double *dst, int ni, int PJ, int j_first) {
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;  // (i, c)
+    if (k >= ni * 4) return;
+    const int i = k >> 2, c = k & 3;
+    const double *p = buf + (size_t)((i + 2) * 4 + c) * PJ + j_first + JOFF;
+    dst[2 * k] = p[0];
+    dst[2 * k + 1] = p[1];
+}
+__global__ void unpack_cols_kernel(const double *src, double *buf, int ni, int PJ, int j_first) {
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= ni * 4) return;
+    const int i = k >> 2, c = k & 3;
+    double *p = buf + (size_t)((i + 2) * 4 + c) * PJ + j_first + JOFF;
+    p[0] = src[2 * k];
+    p[1] = src[2 * k + 1];
+}
+cudaError_t launch_pack_cols(const double *buf, double *dst, int ni, int PJ, int j_first, cudaStream_t st) {
+    pack_cols_kernel<<<(ni * 4 + 255) / 256, 256, 0, st>>>(buf, dst, ni, PJ, j_first);
+    return cudaGetLastError();
+}
+cudaError_t launch_unpack_cols(const double *src, double *buf, int ni, int PJ, int j_first, cudaStream_t st) {
+    unpack_cols_kernel<<<(ni * 4 + 255) / 256, 256, 0, st>>>(src, buf, ni, PJ, j_first);
+    return cudaGetLastError();
+}
+
+__global__ void debug_math_kernel(int which, const double *in, double *out, long long n) {
+    const long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (k >= n) return;
+    const double x = in[k];
+    out[k] = which == 0 ? frcp(x) : which == 1 ? frsqrt(x) : x * frsqrt(x);
+}
+cudaError_t launch_debug_math(int which, const double *in, double *out, long long n, cudaStream_t st) {
+    debug_math_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(which, in, out, n);
+    return cudaGetLastError();
+}
+
+}  // namespace sfv

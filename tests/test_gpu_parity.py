@@ -1,0 +1,249 @@
+"""GPU-vs-oracle parity through the C ABI.
+
+Gates (BASELINE.json north_star): per conserved variable e_k <= 1e-12 after
+1 step and <= 1e-9 after 1000 steps (reading A-R22 for the scale), residual
+norm histories within 1e-10, dt histories within 1e-13, partition maps
+bit-exact (tests/test_abi_host.py).  Every input is seeded and synthetic
+(paper_2305_18057_b200/inputs.py)."""
+import numpy as np
+import pytest
+
+from paper_2305_18057_b200 import inputs as I
+from parity_util import dt_error, norm_error, state_error
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def sfv_mod():
+    import torch
+    assert torch.cuda.is_available(), "GPU tests need a CUDA device"
+    from paper_2305_18057_b200 import sfv
+    sfv.lib()
+    return sfv
+
+
+def run_pair(sfv_mod, oracle_mod, cfg, X, Y, U0, steps, px=1, py=1, wx=None, wy=None):
+    g = sfv_mod.Solver(cfg, X, Y, px=px, py=py, wx=wx, wy=wy)
+    g.set_state(U0)
+    g.step(steps)
+    g.sync()
+    o = oracle_mod.Oracle(cfg, X, Y)
+    o.set_state(U0)
+    o.step(steps)
+    return g, o
+
+
+def check(g, o, tol_state, tol_norm=1e-10, tol_dt=1e-13):
+    Ug, Uo = g.get_state(), o.get_state()
+    assert np.all(np.isfinite(Ug))
+    e = state_error(Ug, Uo)
+    assert np.all(e <= tol_state), e
+    ng, no = g.residual_norms(), o.residual_norms()
+    assert norm_error(ng, no) <= tol_norm, norm_error(ng, no)
+    assert dt_error(g.dt(), o.dt()) <= tol_dt, dt_error(g.dt(), o.dt())
+    return e
+
+
+def test_debug_math_precision(sfv_mod):
+    import torch
+    X, Y = I.ramp_nodes(8, 4, 30.0)
+    s = sfv_mod.Solver(I.default_config(8, 4), X, Y)
+    rng = np.random.default_rng(0)
+    x = np.exp(rng.uniform(-30, 30, 1 << 16))
+    xd = torch.tensor(x, device="cuda"); od = torch.empty_like(xd)
+    for which, ref in [(0, 1.0 / x), (1, 1.0 / np.sqrt(x)), (2, np.sqrt(x))]:
+        s.debug_math(which, xd, od)
+        err = np.max(np.abs(od.cpu().numpy() - ref) / ref)
+        assert err < 4.5e-16, (which, err)
+
+
+@pytest.mark.parametrize("steps,tol", [(1, 1e-12), (100, 1e-10)])
+def test_c1_wedge(sfv_mod, oracle_mod, steps, tol):
+    ni, nj = 64, 32
+    X, Y = I.ramp_nodes(ni, nj, 15.0)
+    cfg = I.default_config(ni, nj)
+    g, o = run_pair(sfv_mod, oracle_mod, cfg, X, Y, I.uniform_state(ni, nj), steps)
+    check(g, o, tol)
+
+
+def test_c1_wedge_1000_steps(sfv_mod, oracle_mod):
+    ni, nj = 64, 32
+    X, Y = I.ramp_nodes(ni, nj, 15.0)
+    cfg = I.default_config(ni, nj)
+    g, o = run_pair(sfv_mod, oracle_mod, cfg, X, Y, I.uniform_state(ni, nj), 1000)
+    check(g, o, 1e-9)
+
+
+@pytest.mark.parametrize("seed", [0, 1, 2])
+def test_inlet_256x128_perturbed(sfv_mod, oracle_mod, seed):
+    ni, nj = 256, 128
+    X, Y = I.ramp_nodes(ni, nj, 30.0)
+    cfg = I.default_config(ni, nj)
+    U0 = I.perturbed_state(ni, nj, seed)
+    g, o = run_pair(sfv_mod, oracle_mod, cfg, X, Y, U0, 1)
+    check(g, o, 1e-12)
+    g.step(49); g.sync(); o.step(49)
+    check(g, o, 1e-10)
+
+
+def test_inlet_256x128_1000_steps(sfv_mod, oracle_mod):
+    ni, nj = 256, 128
+    X, Y = I.ramp_nodes(ni, nj, 30.0)
+    cfg = I.default_config(ni, nj)
+    g, o = run_pair(sfv_mod, oracle_mod, cfg, X, Y, I.uniform_state(ni, nj), 1000)
+    check(g, o, 1e-9)
+
+
+@pytest.mark.parametrize("rk", [I.RK2_HEUN, I.RK4_JAMESON])
+def test_other_tableaus(sfv_mod, oracle_mod, rk):
+    ni, nj = 96, 48
+    X, Y = I.ramp_nodes(ni, nj, 30.0)
+    cfg = I.default_config(ni, nj, rk=rk)
+    U0 = I.perturbed_state(ni, nj, 5)
+    g, o = run_pair(sfv_mod, oracle_mod, cfg, X, Y, U0, 1)
+    check(g, o, 1e-12)
+    g.step(99); g.sync(); o.step(99)
+    check(g, o, 1e-10)
+
+
+@pytest.mark.parametrize("kw", [dict(limiter=I.LIM_VAN_ALBADA2), dict(limiter=I.LIM_NONE, cfl=0.3),
+                                dict(kappa=1.0 / 3.0), dict(kappa=0.0), dict(eps=0.0),
+                                dict(harten_eps=0.0), dict(harten_eps=0.3)])
+def test_scheme_options(sfv_mod, oracle_mod, kw):
+    ni, nj = 80, 40
+    X, Y = I.ramp_nodes(ni, nj, 30.0)
+    cfg = I.default_config(ni, nj, **kw)
+    U0 = I.perturbed_state(ni, nj, 9)
+    g, o = run_pair(sfv_mod, oracle_mod, cfg, X, Y, U0, 1)
+    check(g, o, 1e-12)
+    g.step(19); g.sync(); o.step(19)
+    check(g, o, 1e-10)
+
+
+@pytest.mark.parametrize("bc", [(0, 1, 2, 2), (0, 1, 2, 1), (2, 2, 2, 2), (1, 1, 1, 1), (0, 0, 0, 0),
+                                (2, 1, 0, 2), (1, 2, 2, 0)])
+def test_boundary_combinations(sfv_mod, oracle_mod, bc):
+    ni, nj = 40, 36
+    X, Y = I.ramp_nodes(ni, nj, 10.0)
+    U0 = I.perturbed_state(ni, nj, 3)
+    cfg = I.default_config(ni, nj, bc=bc, cfl=0.5)
+    g, o = run_pair(sfv_mod, oracle_mod, cfg, X, Y, U0, 1)
+    check(g, o, 1e-12)
+    g.step(29); g.sync(); o.step(29)
+    check(g, o, 1e-10)
+
+
+@pytest.mark.parametrize("ni,nj", [(2, 2), (3, 2), (2, 5), (5, 3), (7, 130), (130, 7), (9, 250), (300, 251)])
+def test_small_and_ragged_grids(sfv_mod, oracle_mod, ni, nj):
+    X, Y = I.ramp_nodes(ni, nj, 20.0)
+    U0 = I.perturbed_state(ni, nj, 1)
+    cfg = I.default_config(ni, nj, cfl=0.5)
+    g, o = run_pair(sfv_mod, oracle_mod, cfg, X, Y, U0, 1)
+    check(g, o, 1e-12)
+    g.step(9); g.sync(); o.step(9)
+    check(g, o, 1e-11)
+
+
+def test_fixed_dt(sfv_mod, oracle_mod):
+    ni, nj = 64, 32
+    X, Y = I.ramp_nodes(ni, nj, 30.0)
+    cfg = I.default_config(ni, nj, dt_fixed=2e-6)
+    g, o = run_pair(sfv_mod, oracle_mod, cfg, X, Y, I.perturbed_state(ni, nj, 4), 20)
+    check(g, o, 1e-11, tol_dt=0.0)
+
+
+@pytest.mark.parametrize("px,py,wx,wy", [(2, 1, None, None), (4, 1, [3, 1, 1, 2], None), (1, 3, None, None),
+                                         (3, 2, None, [1, 2]), (8, 1, None, None)])
+def test_loopback_decomposition_invariance(sfv_mod, oracle_mod, px, py, wx, wy):
+    """GPU(P blocks) is bitwise equal to GPU(1 block) in the state (same
+    per-face arithmetic), and matches the oracle."""
+    ni, nj = 120, 40
+    X, Y = I.ramp_nodes(ni, nj, 30.0)
+    cfg = I.default_config(ni, nj)
+    U0 = I.perturbed_state(ni, nj, 4)
+    g1, o = run_pair(sfv_mod, oracle_mod, cfg, X, Y, U0, 50)
+    gp = sfv_mod.Solver(cfg, X, Y, px=px, py=py, wx=wx, wy=wy)
+    gp.set_state(U0); gp.step(50); gp.sync()
+    np.testing.assert_array_equal(gp.get_state(), g1.get_state())
+    np.testing.assert_array_equal(gp.dt(), g1.dt())
+    assert norm_error(gp.residual_norms(), g1.residual_norms()) < 1e-14
+    check(gp, o, 1e-10)
+
+
+def test_run_twice_bitwise(sfv_mod):
+    ni, nj = 200, 100
+    X, Y = I.ramp_nodes(ni, nj, 30.0)
+    cfg = I.default_config(ni, nj)
+    U0 = I.perturbed_state(ni, nj, 8)
+    res = []
+    for _ in range(2):
+        g = sfv_mod.Solver(cfg, X, Y)
+        g.set_state(U0); g.step(30); g.sync()
+        res.append((g.get_state(), g.residual_norms(), g.dt()))
+    for a, b in zip(*res):
+        np.testing.assert_array_equal(a, b)
+
+
+def test_j_invariance_gpu(sfv_mod):
+    ni, nj = 64, 16
+    X, Y = I.cartesian_nodes(ni, nj)
+    cfg = I.default_config(ni, nj, bc=(0, 1, 2, 2))
+    row = I.perturbed_state(ni, 1, 2)
+    prim_u = row[0, :, 1] / row[0, :, 0]
+    row = I.conserved_from_primitive(np.stack([row[0, :, 0], prim_u, np.zeros(ni), np.full(ni, I.TABLE1_P)], -1))[None]
+    U0 = np.repeat(row, nj, axis=0)
+    g = sfv_mod.Solver(cfg, X, Y)
+    g.set_state(U0); g.step(40); g.sync()
+    S = g.get_state()
+    assert np.all(np.isfinite(S))
+    np.testing.assert_array_equal(S, np.repeat(S[:1], nj, axis=0))
+
+
+def test_state_error_reported(sfv_mod, oracle_mod):
+    """An impulsive huge-velocity blob drives p < 0: both sides report
+    SFV_ERR_STATE at the same (step, stage)."""
+    ni, nj = 32, 16
+    X, Y = I.cartesian_nodes(ni, nj)
+    cfg = I.default_config(ni, nj, bc=(1, 1, 2, 2), dt_fixed=0.02, cfl=0.8)
+    prim = np.broadcast_to(np.array([1.0, 0.0, 0.0, 1.0]), (nj, ni, 4)).copy()
+    prim[6:10, 14:18] = [1e-3, 0.0, 0.0, 1e-6]
+    prim[6:10, 18:22] = [1.0, -40.0, 0.0, 1.0]
+    U0 = I.conserved_from_primitive(prim)
+    g = sfv_mod.Solver(cfg, X, Y)
+    o = oracle_mod.Oracle(cfg, X, Y)
+    g.set_state(U0); o.set_state(U0)
+    with pytest.raises(oracle_mod.OracleError) as eo:
+        o.step(20)
+    g.step(20)
+    with pytest.raises(sfv_mod.SfvError) as eg:
+        g.sync()
+    assert eg.value.code == sfv_mod.ERR_STATE
+    assert eg.value.info[:2] == eo.value.info[:2], (eg.value.info, eo.value.info)
+
+
+def test_set_state_rejects_invalid(sfv_mod):
+    ni, nj = 16, 8
+    X, Y = I.ramp_nodes(ni, nj, 30.0)
+    g = sfv_mod.Solver(I.default_config(ni, nj), X, Y)
+    U0 = I.uniform_state(ni, nj)
+    U0[3, 5, 0] = -1.0
+    with pytest.raises(sfv_mod.SfvError) as e:
+        g.set_state(U0)
+    assert e.value.code == sfv_mod.ERR_STATE and e.value.info[2:] == (5, 3)
+    with pytest.raises(sfv_mod.SfvError) as e2:
+        g.step(1)
+    assert e2.value.code == sfv_mod.ERR_SEQUENCE
+
+
+def test_c2_full_size_one_step(sfv_mod, oracle_mod):
+    """BASELINE config C2 (1440x720 inlet) in the launch configuration
+    bench.py times: full oracle comparison after 1 step, every cell."""
+    X, Y = I.config_nodes("C2")
+    c = I.CONFIGS["C2"]
+    cfg = I.default_config(c["ni"], c["nj"])
+    U0 = I.perturbed_state(c["ni"], c["nj"], 0, amplitude=0.02)
+    g, o = run_pair(sfv_mod, oracle_mod, cfg, X, Y, U0, 1)
+    check(g, o, 1e-12)
+    g.step(2); g.sync(); o.step(2)
+    check(g, o, 1e-12)
