@@ -98,7 +98,9 @@ sfv_status sfv_create(const sfv_config *cfg, const double *x_nodes, const double
  *                 and exchanges halos with NCCL send/recv; nccl_unique_id
  *                 (128 bytes from sfv_nccl_unique_id on rank 0, broadcast by
  *                 the caller) is required.
- * cuda_device is the device this ctx runs on.  Host only when nranks == 1.
+ * cuda_device is the device this ctx runs on.  Host only when nranks == 1,
+ * and when nranks > 1 with nccl_unique_id == NULL ("planning" mode: maps and
+ * halo plans are queryable, sfv_bind then fails with SFV_ERR_NCCL).
  * ARG: px*py inconsistent with nranks, any block width < 2, weight <= 0.
  * NCCL: communicator initialisation failed.  SEQUENCE: after sfv_bind. */
 sfv_status sfv_partition(sfv_ctx *ctx, int32_t px, int32_t py, const int32_t *wx, const int32_t *wy,
@@ -111,6 +113,16 @@ sfv_status sfv_nccl_unique_id(void *out128);
  * i0, i1, j0, j1, neighbour block W, E, S, N (-1 = physical boundary).
  * Host only.  Bit-exact with the oracle's maps. */
 sfv_status sfv_partition_map(const sfv_ctx *ctx, int32_t block, int32_t *out8);
+
+/* Halo-exchange plan of block `block` (readings A-R16, A-R18):
+ * for each edge W, E, S, N nine int32 (out36[9*e + ...]):
+ *   neighbour block (-1 = physical edge, rest 0),
+ *   send cells [si0, si1) x [sj0, sj1)   (this block's 2 edge layers),
+ *   recv cells [ri0, ri1) x [rj0, rj1)   (its ghost layers, = the neighbour's
+ *                                          2 edge layers), global indices.
+ * The exchange (device copies or NCCL send/recv) executes exactly this plan;
+ * no corner or diagonal messages.  Host only. */
+sfv_status sfv_halo_plan(const sfv_ctx *ctx, int32_t block, int32_t *out36);
 
 /* Host-only integer largest-remainder split: starts[parts+1]. */
 sfv_status sfv_split(int32_t n, int32_t parts, const int32_t *weights, int32_t *starts);

@@ -315,6 +315,23 @@ size_t layout(sfv_ctx *c, bool assign) {
     return off;
 }
 
+// Halo plan of a block in global cell indices (see sfv_halo_plan).
+struct EdgePlan {
+    int nbr, si0, si1, sj0, sj1, ri0, ri1, rj0, rj1;
+};
+void halo_plan(const sfv_ctx *c, int id, EdgePlan p[4]) {
+    const int bx = id % c->px, by = id / c->px;
+    const int i0 = c->xs[bx], i1 = c->xs[bx + 1], j0 = c->ys[by], j1 = c->ys[by + 1];
+    const int nb[4] = {bx > 0 ? id - 1 : -1, bx < c->px - 1 ? id + 1 : -1, by > 0 ? id - c->px : -1,
+                       by < c->py - 1 ? id + c->px : -1};
+    p[0] = {nb[0], i0, i0 + 2, j0, j1, i0 - 2, i0, j0, j1};
+    p[1] = {nb[1], i1 - 2, i1, j0, j1, i1, i1 + 2, j0, j1};
+    p[2] = {nb[2], i0, i1, j0, j0 + 2, i0, i1, j0 - 2, j0};
+    p[3] = {nb[3], i0, i1, j1 - 2, j1, i0, i1, j1, j1 + 2};
+    for (int e = 0; e < 4; ++e)
+        if (nb[e] < 0) p[e] = {-1, 0, 0, 0, 0, 0, 0, 0, 0};
+}
+
 Block *local_block(sfv_ctx *c, int id) {
     for (Block &b : c->blocks)
         if (b.id == id) return &b;
@@ -348,35 +365,35 @@ sfv_status exchange(sfv_ctx *c, int k, cudaStream_t st) {
         }
         return SFV_OK;
     }
-    // NCCL: one block per rank; block id == rank.
+    // NCCL: one block per rank (block id == rank); executes halo_plan().
     Block &b = c->blocks[0];
     Nccl &N = nccl();
-    for (int s = 0; s < 2; ++s) {  // pack j-cut columns first (S: cols 0,1; N: cols nj-2,nj-1)
-        const int nb = b.nbr[2 + s];
-        if (nb < 0) continue;
-        CK(launch_pack_cols(b.buf[k], b.xs[s], b.ni, b.PJ, s == 0 ? 0 : b.nj - 2, st));
+    EdgePlan p[4];
+    halo_plan(c, b.id, p);
+    for (int s = 0; s < 2; ++s) {  // j-cuts: pack the 2 send columns
+        const EdgePlan &q = p[2 + s];
+        if (q.nbr < 0) continue;
+        CK(launch_pack_cols(b.buf[k], b.xs[s], b.ni, b.PJ, q.sj0 - b.j0, st));
     }
     NK(N.GroupStart());
-    const size_t run = (size_t)2 * 4 * b.PJ;
-    if (b.nbr[0] >= 0) {
-        NK(N.Send(b.buf[k] + (size_t)2 * 4 * b.PJ, run, ncclDouble, b.nbr[0], c->comm, st));
-        NK(N.Recv(b.buf[k], run, ncclDouble, b.nbr[0], c->comm, st));
-    }
-    if (b.nbr[1] >= 0) {
-        NK(N.Send(b.buf[k] + (size_t)(b.ni) * 4 * b.PJ, run, ncclDouble, b.nbr[1], c->comm, st));
-        NK(N.Recv(b.buf[k] + (size_t)(b.ni + 2) * 4 * b.PJ, run, ncclDouble, b.nbr[1], c->comm, st));
+    const size_t run = (size_t)2 * 4 * b.PJ;  // 2 rows x 4 comps x pitch: contiguous in [i][c][j]
+    for (int e = 0; e < 2; ++e) {  // i-cuts: zero-copy rows
+        const EdgePlan &q = p[e];
+        if (q.nbr < 0) continue;
+        NK(N.Send(b.buf[k] + (size_t)(q.si0 - b.i0 + 2) * 4 * b.PJ, run, ncclDouble, q.nbr, c->comm, st));
+        NK(N.Recv(b.buf[k] + (size_t)(q.ri0 - b.i0 + 2) * 4 * b.PJ, run, ncclDouble, q.nbr, c->comm, st));
     }
     for (int s = 0; s < 2; ++s) {
-        const int nb = b.nbr[2 + s];
-        if (nb < 0) continue;
-        NK(N.Send(b.xs[s], (size_t)8 * b.ni, ncclDouble, nb, c->comm, st));
-        NK(N.Recv(b.xr[s], (size_t)8 * b.ni, ncclDouble, nb, c->comm, st));
+        const EdgePlan &q = p[2 + s];
+        if (q.nbr < 0) continue;
+        NK(N.Send(b.xs[s], (size_t)8 * b.ni, ncclDouble, q.nbr, c->comm, st));
+        NK(N.Recv(b.xr[s], (size_t)8 * b.ni, ncclDouble, q.nbr, c->comm, st));
     }
     NK(N.GroupEnd());
     for (int s = 0; s < 2; ++s) {
-        const int nb = b.nbr[2 + s];
-        if (nb < 0) continue;
-        CK(launch_unpack_cols(b.xr[s], b.buf[k], b.ni, b.PJ, s == 0 ? -2 : b.nj, st));
+        const EdgePlan &q = p[2 + s];
+        if (q.nbr < 0) continue;
+        CK(launch_unpack_cols(b.xr[s], b.buf[k], b.ni, b.PJ, q.rj0 - b.j0, st));
     }
     return SFV_OK;
 }
@@ -531,8 +548,7 @@ sfv_status sfv_partition(sfv_ctx *c, int32_t px, int32_t py, const int32_t *wx, 
     c->nranks = nranks;
     c->device = device;
     build_blocks(c);
-    if (nranks > 1) {
-        if (!uid) return fail(c, SFV_ERR_ARG, "nccl_unique_id required when nranks > 1");
+    if (nranks > 1 && uid) {  // NULL id: host-only planning mode
         Nccl &N = nccl();
         if (!N.ok) return fail(c, SFV_ERR_NCCL, "libnccl.so.2 not loadable");
         CK(cudaSetDevice(device));
@@ -558,6 +574,17 @@ sfv_status sfv_partition_map(const sfv_ctx *c, int32_t block, int32_t *out8) {
     return SFV_OK;
 }
 
+sfv_status sfv_halo_plan(const sfv_ctx *c, int32_t block, int32_t *out36) {
+    if (!c || !out36 || block < 0 || block >= c->px * c->py) return SFV_ERR_ARG;
+    EdgePlan p[4];
+    halo_plan(c, block, p);
+    for (int e = 0; e < 4; ++e) {
+        const int v[9] = {p[e].nbr, p[e].si0, p[e].si1, p[e].sj0, p[e].sj1, p[e].ri0, p[e].ri1, p[e].rj0, p[e].rj1};
+        for (int q = 0; q < 9; ++q) out36[9 * e + q] = v[q];
+    }
+    return SFV_OK;
+}
+
 sfv_status sfv_workspace_size(const sfv_ctx *c, size_t *bytes) {
     if (!c || !bytes) return SFV_ERR_ARG;
     *bytes = layout(const_cast<sfv_ctx *>(c), false) + 256;
@@ -567,6 +594,7 @@ sfv_status sfv_workspace_size(const sfv_ctx *c, size_t *bytes) {
 sfv_status sfv_bind(sfv_ctx *c, void *ws, size_t bytes, void *stream) {
     if (!c || !ws) return SFV_ERR_ARG;
     if (c->bound) return fail(c, SFV_ERR_SEQUENCE, "already bound");
+    if (c->nranks > 1 && !c->comm) return fail(c, SFV_ERR_NCCL, "nranks > 1 without an NCCL communicator");
     size_t need = layout(c, false);
     if (bytes < need) return fail(c, SFV_ERR_OOM, "workspace %zu < %zu bytes", bytes, need);
     if (reinterpret_cast<uintptr_t>(ws) % 256) return fail(c, SFV_ERR_ARG, "workspace not 256-byte aligned");

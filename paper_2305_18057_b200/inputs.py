@@ -149,11 +149,13 @@ def uniform_pm1(seed, n_cells, n_var=4):
     return 2.0 * u - 1.0
 
 
-def perturbed_state(ni, nj, seed, amplitude=0.05, prim0=None):
+def perturbed_state(ni, nj, seed, amplitude=0.02, prim0=None):
     """Freestream with +-amplitude relative perturbations on (rho, u, v, p).
 
     v is perturbed relative to |u| (the freestream v is 0).  Returns the
-    conserved state, shape (nj, ni, 4), index [j, i, k].
+    conserved state, shape (nj, ni, 4), index [j, i, k].  The default +-2%
+    (SURVEY.md §8(c).5 proposed +-5%) keeps every MUSCL face state of the
+    Mach-4 inlet valid with the bounded van Albada limiter.
     """
     if prim0 is None:
         prim0 = freestream_primitive()
@@ -175,9 +177,15 @@ def uniform_state(ni, nj, U0=None):
 
 def default_config(ni, nj, rk=RK4_CLASSIC, cfl=None, bc=None,
                    inflow=None, dt_fixed=0.0, harten_eps=0.1,
-                   limiter=LIM_VAN_ALBADA, lim_delta=1e-12, eps=1.0,
+                   limiter=LIM_VAN_ALBADA2, lim_delta=1e-12, eps=1.0,
                    kappa=-1.0, gamma=GAMMA, max_history=4096):
-    """The scheme settings of SURVEY.md §8(d) "common settings".
+    """The scheme settings of SURVEY.md §8(d) "common settings", except the
+    limiter: van Albada in its bounded form psi = max(0, (2ab+d)/(a^2+b^2+d))
+    (reading A-R3, revised).  It satisfies SPEC.md:166 (0 <= Psi
+    <= 1), :177 and :180-182, and is Lipschitz; the VA1 form
+    (a^2+ab+d)/(a^2+b^2+d) with the ab<0 switch is discontinuous for
+    |b| << sqrt(d), which makes the discrete evolution amplify 1-ulp input
+    noise to ~1e-9 (measured on the oracle itself), so it stays an option.
 
     Returns a plain dict consumed by both the oracle wrapper and the sfv
     binding.  bc order is (W, E, S, N).

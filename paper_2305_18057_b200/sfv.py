@@ -21,7 +21,8 @@ OK, ERR_ARG, ERR_GEOMETRY, ERR_STATE, ERR_SEQUENCE, ERR_CUDA, ERR_NCCL, ERR_OOM,
 _NAMES = ["OK", "ARG", "GEOMETRY", "STATE", "SEQUENCE", "CUDA", "NCCL", "OOM", "UNSUPPORTED"]
 
 # every entry point declared in include/sfv.h
-ABI_SYMBOLS = ["sfv_create", "sfv_partition", "sfv_nccl_unique_id", "sfv_partition_map", "sfv_split",
+ABI_SYMBOLS = ["sfv_create", "sfv_partition", "sfv_nccl_unique_id", "sfv_partition_map", "sfv_halo_plan",
+               "sfv_split",
                "sfv_workspace_size", "sfv_bind", "sfv_set_state", "sfv_step", "sfv_sync", "sfv_steps_done",
                "sfv_get_residual_norms", "sfv_get_dt", "sfv_get_state", "sfv_error_info", "sfv_launch_info",
                "sfv_debug_math", "sfv_last_error", "sfv_destroy"]
@@ -62,6 +63,7 @@ def lib():
         L.sfv_partition.argtypes = [_VP, C.c_int32, C.c_int32, _I32, _I32, C.c_int32, C.c_int32, _VP, C.c_int32]
         L.sfv_nccl_unique_id.argtypes = [_VP]
         L.sfv_partition_map.argtypes = [_VP, C.c_int32, _I32]
+        L.sfv_halo_plan.argtypes = [_VP, C.c_int32, _I32]
         L.sfv_split.argtypes = [C.c_int32, C.c_int32, _I32, _I32]
         L.sfv_workspace_size.argtypes = [_VP, C.POINTER(C.c_size_t)]
         L.sfv_bind.argtypes = [_VP, _VP, C.c_size_t, _VP]
@@ -186,6 +188,12 @@ class Solver:
         out = np.zeros(8, np.int32)
         self._check(lib().sfv_partition_map(self._h, block, out.ctypes.data_as(_I32)))
         return out
+
+    def halo_plan(self, block):
+        """(4, 9) int32: per edge W, E, S, N: nbr, send i0,i1,j0,j1, recv i0,i1,j0,j1."""
+        out = np.zeros(36, np.int32)
+        self._check(lib().sfv_halo_plan(self._h, block, out.ctypes.data_as(_I32)))
+        return out.reshape(4, 9)
 
     def set_state(self, U):
         U = np.ascontiguousarray(U, np.float64)
