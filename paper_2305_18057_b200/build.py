@@ -36,23 +36,29 @@ def up_to_date():
     return all(os.path.getmtime(d) <= t for d in DEPS)
 
 
-def build(force=False, verbose=False):
-    if not force and up_to_date():
+def build(force=False, verbose=False, out=None, defines=()):
+    if out is None and not force and up_to_date():
         return LIB
-    cmd = ["nvcc", *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xptxas", "-v",
+    target = out or LIB
+    cmd = ["nvcc", *ARCH, *[f"-D{d}" for d in defines], "-O3", "-lineinfo", "-std=c++17", "-Xptxas", "-v",
            "-Xcompiler", "-fPIC", "-shared", "-I", os.path.join(ROOT, "include"),
-           "-I", CSRC, "-I", nccl_include(), *SOURCES, "-o", LIB + ".tmp", "-ldl"]
+           "-I", CSRC, "-I", nccl_include(), *SOURCES, "-o", target + ".tmp", "-ldl"]
     r = subprocess.run(cmd, capture_output=True, text=True)
-    with open(os.path.join(HERE, "build.log"), "w") as f:
+    with open(os.path.join(HERE, "build.log" if out is None else os.path.basename(target) + ".log"), "w") as f:
         f.write(" ".join(cmd) + "\n" + r.stdout + r.stderr)
     if r.returncode != 0:
         sys.stderr.write(r.stderr)
         raise RuntimeError("nvcc failed building libsfv.so")
-    os.replace(LIB + ".tmp", LIB)
+    os.replace(target + ".tmp", target)
     if verbose:
         print(r.stderr)
-    return LIB
+    return target
 
 
 if __name__ == "__main__":
-    build(force="--force" in sys.argv, verbose=True)
+    if "--variant" in sys.argv:  # A/B experiment builds: --variant NAME DEF=V ...
+        k = sys.argv.index("--variant")
+        name, defs = sys.argv[k + 1], sys.argv[k + 2:]
+        print(build(out=os.path.join(HERE, f"libsfv_{name}.so"), defines=defs))
+    else:
+        build(force="--force" in sys.argv, verbose=True)

@@ -12,8 +12,10 @@ namespace sfv {
 //   i in [-2, ni+2), j in [-2, nj+2), c = rho, rho u, rho v, rho E.
 // The partitioned index i is the slow one, so the 2 edge rows of an i-cut
 // are one contiguous run (zero-copy halo send/recv).
-// Metrics: row r in [0, ni] holds 7 fields, each PJ doubles at column
-// j + JOFF: i-face (r, j) nx, ny, A; j-face (r, j) nx, ny, A; 1/V(r, j).
+// Metrics: memory row m in [0, ni] holds 7 fields, each PJ doubles at column
+// j + JOFF: i-face (m, j) nx, ny, A; j-face (m-1, j) nx, ny, A; 1/V(m-1, j),
+// so the stage kernel's iteration over cell row v stages one metrics row
+// (m = v+1) holding its east face, its south face and its volume.
 constexpr int JOFF = 4;
 constexpr int NMET = 7;
 constexpr int SMEM_ROW = 132;     // doubles per staged row in shared memory

@@ -198,26 +198,43 @@ __device__ __forceinline__ void store4(double *buf, int PJ, int i, int j, const 
 template <int MODE>
 struct StageTraits {
     static constexpr int NPW = MODE == M_OWN ? 0 : (MODE == M_RK4F ? 3 : 1);
-    static constexpr int NROWS = 4 + NMET + 4 * NPW;
-    static constexpr int SLOT = NROWS * SMEM_ROW;  // doubles per ring slot
-    static constexpr int NS = MODE == M_RK4F ? 4 : 5;  // ring depth (rows in flight)
+    static constexpr int NS_W = 4;                    // stencil ring: rows v..v+2 + 1 in flight
+    static constexpr int NS_M = 2;                    // metrics ring: row v + 1 in flight
+    static constexpr int W_SLOT = 4 * SMEM_ROW;
+    static constexpr int M_SLOT = NMET * SMEM_ROW;
+    static constexpr int P_SLOT = 4 * NPW * SMEM_ROW; // pointwise: row v only
+    static constexpr int NBAR = NS_W + NS_M + 1;
 };
 
 template <int MODE>
 __host__ __device__ constexpr size_t stage_smem() {
-    return sizeof(double) * ((size_t)StageTraits<MODE>::NS * StageTraits<MODE>::SLOT + 8 * NT + 8 * (NT / 32)) +
-           sizeof(uint64_t) * StageTraits<MODE>::NS;
+    using T = StageTraits<MODE>;
+    return sizeof(double) * ((size_t)T::NS_W * T::W_SLOT + (size_t)T::NS_M * T::M_SLOT + T::P_SLOT + 8 * NT +
+                             8 * (NT / 32)) +
+           sizeof(uint64_t) * T::NBAR;
 }
 
+// Metrics "row" r (r in [-1, ni)) = memory row r+1 = { i-face(r+1) nx, ny, A;
+// j-face(r) nx, ny, A; 1/V(r) }: everything iteration v needs is in row v.
+#ifndef SFV_MINB
+#define SFV_MINB 4  // resident CTAs per SM the register allocation targets
+#endif
 template <int MODE, bool NORMS, bool DTMAX>
-__global__ void __launch_bounds__(NT) stage_kernel(const StageArgs a) {
+__global__ void __launch_bounds__(NT, SFV_MINB) stage_kernel(const StageArgs a);
+
+template <int MODE, bool NORMS, bool DTMAX>
+__global__ void __launch_bounds__(NT, SFV_MINB) stage_kernel(const StageArgs a) {
     using TR = StageTraits<MODE>;
     extern __shared__ __align__(128) double smem[];
-    double *ring = smem;
-    double *xq = ring + TR::NS * TR::SLOT;  // [4][NT] north face states
-    double *xg = xq + 4 * NT;              // [4][NT] south face fluxes
-    double *red = xg + 4 * NT;             // [8][NT/32]
-    uint64_t *bars = reinterpret_cast<uint64_t *>(red + 8 * (NT / 32));
+    double *wring = smem;                           // [NS_W][4][SMEM_ROW] stencil rows
+    double *mring = wring + TR::NS_W * TR::W_SLOT;  // [NS_M][7][SMEM_ROW] metric rows
+    double *pring = mring + TR::NS_M * TR::M_SLOT;  // [4*NPW][SMEM_ROW] pointwise row
+    double *xq = pring + TR::P_SLOT;                // [4][NT] north face states
+    double *xg = xq + 4 * NT;                       // [4][NT] south face fluxes
+    double *red = xg + 4 * NT;                      // [8][NT/32]
+    uint64_t *wbar = reinterpret_cast<uint64_t *>(red + 8 * (NT / 32));
+    uint64_t *mbar = wbar + TR::NS_W;
+    uint64_t *pbar = mbar + TR::NS_M;
 
     const Params &P = a.P;
     const int t = threadIdx.x;
@@ -225,249 +242,269 @@ __global__ void __launch_bounds__(NT) stage_kernel(const StageArgs a) {
     const int seg = blockIdx.x / a.nstrips;
     const int j0 = 2 * (int)(((long long)strip * a.nj) / (2 * a.nstrips));
     const int j1 = (strip + 1 == a.nstrips) ? a.nj : 2 * (int)(((long long)(strip + 1) * a.nj) / (2 * a.nstrips));
-    const int jc = j0 - 1 + t;                         // this thread's column
-    const bool is_out = (t >= 1) && (jc < j1);         // owns output cell (v, jc)
-    const bool jflux = (t >= 1) && (jc <= j1);         // evaluates j-face (v, jc)
-    const bool jrec = (jc <= j1);                      // reconstructs cell (v, jc) along j
-    const int own = t + 1;                             // column index inside a staged row
+    const int jc = j0 - 1 + t;                 // this thread's column
+    const bool is_out = (t >= 1) && (jc < j1); // owns output cell (v, jc)
+    const bool jflux = (t >= 1) && (jc <= j1); // its j-face (v, jc) is needed
+    const int own = t + 1;                     // column index inside a staged row
+    const int tm1 = t > 0 ? t - 1 : 0;
     const int i_start = (int)(((long long)a.ni * seg) / a.nseg);
     const int i_end = (int)(((long long)a.ni * (seg + 1)) / a.nseg);
-    const int r0 = i_start - 2;                        // first staged row
-    const int r_last = i_end + 1;                      // last staged row
+    const int r0 = i_start - 2, r_last = i_end + 1;  // stencil rows
+    const int m0 = i_start - 1, m_last = i_end - 1;  // metric rows
 
     const long long n = *a.step_ctr;
     const double dt = P.dt_fixed > 0.0 ? P.dt_fixed : P.cfl / a.sig[n & 1];
     const double coef = a.coef * dt;
     const int PJ = a.PJ;
     const size_t col0 = (size_t)(j0 - 2 + JOFF);
+    constexpr unsigned ROWB = ROW_COLS * 8u;
 
-    auto slot_of = [&](int r) -> double * { return ring + ((r - r0) % TR::NS) * TR::SLOT; };
-    auto issue = [&](int r) {
-        const int s = (r - r0) % TR::NS;
-        double *dst = ring + s * TR::SLOT;
-        const bool has_met = (r >= 0) && (r <= a.ni);
-        const bool has_pw = TR::NPW > 0 && (r >= 0) && (r < a.ni);
-        unsigned bytes = 4u * ROW_COLS * 8u;
-        if (has_met) bytes += (unsigned)NMET * ROW_COLS * 8u;
-        if (has_pw) bytes += 4u * TR::NPW * ROW_COLS * 8u;
-        mbar_expect_tx(&bars[s], bytes);
+    auto wslot = [&](int r) -> const double * { return wring + ((r - r0) & 3) * TR::W_SLOT; };
+    auto mslot = [&](int r) -> const double * { return mring + ((r - m0) & 1) * TR::M_SLOT; };
+    auto issue_w = [&](int r) {
+        const int s = (r - r0) & 3;
+        mbar_expect_tx(&wbar[s], 4u * ROWB);
         const double *src = a.in + (size_t)((r + 2) * 4) * PJ + col0;
 #pragma unroll
-        for (int c = 0; c < 4; ++c) bulk_g2s(dst + c * SMEM_ROW, src + (size_t)c * PJ, ROW_COLS * 8u, &bars[s]);
-        if (has_met) {
-            const double *m = a.met + (size_t)(r * NMET) * PJ + col0;
+        for (int c = 0; c < 4; ++c) bulk_g2s(wring + s * TR::W_SLOT + c * SMEM_ROW, src + (size_t)c * PJ, ROWB, &wbar[s]);
+    };
+    auto issue_m = [&](int r) {
+        const int s = (r - m0) & 1;
+        mbar_expect_tx(&mbar[s], (unsigned)NMET * ROWB);
+        const double *src = a.met + (size_t)((r + 1) * NMET) * PJ + col0;
 #pragma unroll
-            for (int f = 0; f < NMET; ++f)
-                bulk_g2s(dst + (4 + f) * SMEM_ROW, m + (size_t)f * PJ, ROW_COLS * 8u, &bars[s]);
-        }
-        if (has_pw) {
+        for (int f = 0; f < NMET; ++f)
+            bulk_g2s(mring + s * TR::M_SLOT + f * SMEM_ROW, src + (size_t)f * PJ, ROWB, &mbar[s]);
+    };
+    auto issue_p = [&](int r) {
+        if constexpr (TR::NPW > 0) {
+            mbar_expect_tx(pbar, 4u * TR::NPW * ROWB);
             const double *pws[3] = {a.pw0, a.pw1, a.pw2};
 #pragma unroll
             for (int p = 0; p < TR::NPW; ++p) {
                 const double *q = pws[p] + (size_t)((r + 2) * 4) * PJ + col0;
 #pragma unroll
-                for (int c = 0; c < 4; ++c)
-                    bulk_g2s(dst + (4 + NMET + 4 * p + c) * SMEM_ROW, q + (size_t)c * PJ, ROW_COLS * 8u, &bars[s]);
+                for (int c = 0; c < 4; ++c) bulk_g2s(pring + (4 * p + c) * SMEM_ROW, q + (size_t)c * PJ, ROWB, pbar);
             }
         }
     };
-    auto wait_row = [&](int r) { mbar_wait(&bars[(r - r0) % TR::NS], (unsigned)(((r - r0) / TR::NS) & 1)); };
+    auto wait_w = [&](int r) { mbar_wait(&wbar[(r - r0) & 3], (unsigned)(((r - r0) >> 2) & 1)); };
+    auto wait_m = [&](int r) { mbar_wait(&mbar[(r - m0) & 1], (unsigned)(((r - m0) >> 1) & 1)); };
 
     if (t == 0) {
-        for (int s = 0; s < TR::NS; ++s) mbar_init(&bars[s], 1);
+        for (int s = 0; s < TR::NBAR; ++s) mbar_init(&wbar[s], 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     }
     __syncthreads();
-    int next_issue = r0;
+    int next_w = r0, next_m = m0;
     if (t == 0) {
-        for (; next_issue < r0 + TR::NS && next_issue <= r_last; ++next_issue) issue(next_issue);
+        for (; next_w <= r0 + 3 && next_w <= r_last; ++next_w) issue_w(next_w);
+        for (; next_m <= m0 + 1 && next_m <= m_last; ++next_m) issue_m(next_m);
     }
 
-    double Wc[4], fp[4], QLp[4], GW[4] = {0, 0, 0, 0}, GE[4] = {0, 0, 0, 0};
-    double nWx = 0.0, nWy = 0.0;  // i-face(0) normal (W-edge slip ghosts)
+    double Wc[4], fp[4], QLp[4], GW[4];
+    double nWx = 0.0, nWy = 0.0;                     // i-face(0) normal (W-edge slip ghosts)
+    double wfx = 0.0, wfy = 0.0, wfA = 0.0;          // west face of the current row (dt)
     double nrm[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     double smax = 0.0;
 
-    wait_row(r0);
-    wait_row(r0 + 1);
+    // ---- peeled prologue: rows i_start-2, i_start-1 (i direction only) ------
+    wait_w(r0);
+    wait_w(r0 + 1);
+    wait_w(r0 + 2);
     {
-        const double *s0 = slot_of(r0), *s1 = slot_of(r0 + 1);
+        const double *s0 = wslot(r0), *s1 = wslot(r0 + 1), *s2 = wslot(r0 + 2);
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
-            Wc[c] = s1[c * SMEM_ROW + own];
-            fp[c] = Wc[c] - s0[c * SMEM_ROW + own];
-            QLp[c] = 0.0;
+            const double w0 = s0[c * SMEM_ROW + own], w1 = s1[c * SMEM_ROW + own], w2 = s2[c * SMEM_ROW + own];
+            double qU, qD;
+            muscl_cell(w1, w1 - w0, w2 - w1, P, qU, qD);  // cell i_start-1
+            QLp[c] = qU;
+            fp[c] = w2 - w1;
+            Wc[c] = w2;
         }
     }
-    // rows r0, r0+1 are consumed: refill their slots (rows r0+NS, r0+NS+1)
-    __syncthreads();
+    __syncthreads();  // rows r0, r0+1 consumed
     if (t == 0) {
-        for (; next_issue <= r0 + TR::NS + 1 && next_issue <= r_last; ++next_issue) issue(next_issue);
+        for (; next_w <= r0 + 5 && next_w <= r_last; ++next_w) issue_w(next_w);
+    }
+    wait_w(r0 + 3);
+    wait_m(m0);
+    {
+        const double *s3 = wslot(r0 + 3);
+        const double *m = mslot(m0);
+        double qU[4], qD[4];
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+            const double wn = s3[c * SMEM_ROW + own];
+            const double f = wn - Wc[c];
+            muscl_cell(Wc[c], fp[c], f, P, qU[c], qD[c]);  // cell i_start
+            fp[c] = f;
+            Wc[c] = wn;
+        }
+        const double nx = m[0 * SMEM_ROW + own], ny = m[1 * SMEM_ROW + own], A = m[2 * SMEM_ROW + own];
+        const bool ok = roe_flux(QLp, qD, nx, ny, A, P, GW);
+        if (!ok && is_out)
+            atomicMin(a.err, err_key(n, a.nstages, a.stage, 0, (long long)(a.gj0 + jc) * a.NI + a.gi0 + i_start));
+        nWx = nx; nWy = ny;
+        wfx = nx; wfy = ny; wfA = A;
+#pragma unroll
+        for (int c = 0; c < 4; ++c) QLp[c] = qU[c];
     }
 
-    for (int v = r0; v < i_end; ++v) {
-        wait_row(v + 2);
-        // ---- i direction: reconstruct cell v+1, flux at face v+1/2 ----------
-        if (is_out) {
-            const double *sn = slot_of(v + 2);
-            double qU[4], qD[4];
+    // ---- main loop: one output row per iteration ------------------------------
+    for (int v = i_start; v < i_end; ++v) {
+        wait_w(v + 2);
+        double qD[4], qU[4], qS[4], Wv[4];
+        {
+            const double *sn = wslot(v + 2);
+            const double *sv = wslot(v);
 #pragma unroll
-            for (int c = 0; c < 4; ++c) {
+            for (int c = 0; c < 4; ++c) {  // i: reconstruct cell v+1
                 const double wn = sn[c * SMEM_ROW + own];
                 const double f = wn - Wc[c];
                 muscl_cell(Wc[c], fp[c], f, P, qU[c], qD[c]);
                 fp[c] = f;
                 Wc[c] = wn;
             }
-            if (v >= i_start - 1) {
-                const double *m = slot_of(v + 1) + 4 * SMEM_ROW;
-                const double nx = m[0 * SMEM_ROW + own], ny = m[1 * SMEM_ROW + own], A = m[2 * SMEM_ROW + own];
-                if (v == -1) { nWx = nx; nWy = ny; }
-                if (!roe_flux(QLp, qD, nx, ny, A, P, GE)) {
-                    int I = a.gi0 + v + 1;
-                    if (I > a.NI - 1) I = a.NI - 1;
-                    atomicMin(a.err, err_key(n, a.nstages, a.stage, 0, (long long)(a.gj0 + jc) * a.NI + I));
-                }
-            }
 #pragma unroll
-            for (int c = 0; c < 4; ++c) QLp[c] = qU[c];
+            for (int c = 0; c < 4; ++c) {  // j: reconstruct cell (v, jc)
+                const double wm = sv[c * SMEM_ROW + own - 1];
+                const double w = sv[c * SMEM_ROW + own];
+                const double wp = sv[c * SMEM_ROW + own + 1];
+                double qN;
+                muscl_cell(w, w - wm, wp - w, P, qN, qS[c]);
+                xq[c * NT + t] = qN;
+                Wv[c] = w;
+            }
         }
-        if (v >= i_start) {
-            // ---- j direction: reconstruct cell (v, jc), exchange, flux ------
-            const double *sv = slot_of(v);
-            const double *mv = sv + 4 * SMEM_ROW;
-            double Wv[4], qS[4];
-            if (jrec) {
+        __syncthreads();  // B1: face states visible, stencil row v-1 / metric row v-1 free
+        if (t == 0) {
+            const int lw = min(v + 3, r_last), lm = min(v + 1, m_last);
+            for (; next_w <= lw; ++next_w) issue_w(next_w);
+            for (; next_m <= lm; ++next_m) issue_m(next_m);
+            issue_p(v);
+        }
+        wait_m(v);
+        const double *mv = mslot(v);
+        double GE[4], GS[4], qN[4];
+#pragma unroll
+        for (int c = 0; c < 4; ++c) qN[c] = xq[c * NT + tm1];
+        // both face fluxes of this row: two independent Roe evaluations
+        const bool okE = roe_flux(QLp, qD, mv[0 * SMEM_ROW + own], mv[1 * SMEM_ROW + own], mv[2 * SMEM_ROW + own], P, GE);
+        const bool okS = roe_flux(qN, qS, mv[3 * SMEM_ROW + own], mv[4 * SMEM_ROW + own], mv[5 * SMEM_ROW + own], P, GS);
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+            QLp[c] = qU[c];
+            xg[c * NT + t] = GS[c];
+        }
+        if (!okE && is_out) {
+            int I = a.gi0 + v + 1;
+            if (I > a.NI - 1) I = a.NI - 1;
+            atomicMin(a.err, err_key(n, a.nstages, a.stage, 0, (long long)(a.gj0 + jc) * a.NI + I));
+        }
+        if (!okS && jflux) {
+            int J = a.gj0 + jc;
+            if (J > a.NJ - 1) J = a.NJ - 1;
+            atomicMin(a.err, err_key(n, a.nstages, a.stage, 0, (long long)J * a.NI + a.gi0 + v));
+        }
+        __syncthreads();  // B2: south fluxes visible
+        if (is_out) {
+            // ---- residual (Eq. 5) and stage update (Eq. 6) --------------------
+            const double iV = mv[6 * SMEM_ROW + own];
+            double R[4], U[4];
+#pragma unroll
+            for (int c = 0; c < 4; ++c) R[c] = ((GE[c] - GW[c]) + xg[c * NT + t + 1]) - GS[c];
+            if constexpr (TR::NPW > 0) mbar_wait(pbar, (unsigned)((v - i_start) & 1));
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+                const double rv = R[c] * iV;
+                if constexpr (MODE == M_OWN) {
+                    U[c] = fma(-coef, rv, Wv[c]);
+                } else if constexpr (MODE == M_UN) {
+                    U[c] = fma(-coef, rv, pring[c * SMEM_ROW + own]);
+                } else if constexpr (MODE == M_RK4F) {
+                    const double un = pring[c * SMEM_ROW + own];
+                    const double d2 = pring[(4 + c) * SMEM_ROW + own] - un;
+                    const double d3 = pring[(8 + c) * SMEM_ROW + own] - un;
+                    const double d4 = Wv[c] - un;
+                    const double comb = (fma(2.0, d3, d2) + d4) * (1.0 / 3.0);
+                    U[c] = un + fma(-coef, rv, comb);
+                } else {  // M_HEUNF
+                    const double un = pring[c * SMEM_ROW + own];
+                    U[c] = un + fma(-coef, rv, 0.5 * (Wv[c] - un));
+                }
+            }
+            store4(a.out, PJ, v, jc, U);
+            // new-state validity: rho > 0 and 2 rho E > |m|^2 (<=> p > 0)
+            if (!((U[0] > 0.0) & (2.0 * U[0] * U[3] > fma(U[1], U[1], U[2] * U[2]))))
+                atomicMin(a.err, err_key(n, a.nstages, a.stage, 1, (long long)(a.gj0 + jc) * a.NI + a.gi0 + v));
+            // physical-boundary ghosts of the new state (reading A-R11)
+            if (a.bc[2] == E_SLIP && jc <= 1) {
+                double g[4];
+                const int k0 = own - jc;  // column 0
+                mirror(U, mv[3 * SMEM_ROW + k0], mv[4 * SMEM_ROW + k0], g);
+                store4(a.out, PJ, v, -1 - jc, g);
+            } else if (a.bc[2] == E_OUTFLOW && jc == 0) {
+                store4(a.out, PJ, v, -1, U);
+                store4(a.out, PJ, v, -2, U);
+            }
+            if (a.bc[3] == E_SLIP && jc >= a.nj - 2) {
+                double g[4];
+                const int kN = own + (a.nj - jc);  // column nj
+                mirror(U, mv[3 * SMEM_ROW + kN], mv[4 * SMEM_ROW + kN], g);
+                store4(a.out, PJ, v, a.nj + (a.nj - 1 - jc), g);
+            } else if (a.bc[3] == E_OUTFLOW && jc == a.nj - 1) {
+                store4(a.out, PJ, v, a.nj, U);
+                store4(a.out, PJ, v, a.nj + 1, U);
+            }
+            if (a.bc[0] == E_SLIP && v <= 1) {
+                double g[4];
+                mirror(U, nWx, nWy, g);
+                store4(a.out, PJ, -1 - v, jc, g);
+            } else if (a.bc[0] == E_OUTFLOW && v == 0) {
+                store4(a.out, PJ, -1, jc, U);
+                store4(a.out, PJ, -2, jc, U);
+            }
+            if (a.bc[1] == E_SLIP && v >= a.ni - 2) {
+                double g[4];
+                wait_m(a.ni - 1);  // i-face(ni) lives in metric row ni-1 (issued: <= v+1)
+                const double *mE = mslot(a.ni - 1);
+                mirror(U, mE[0 * SMEM_ROW + own], mE[1 * SMEM_ROW + own], g);
+                store4(a.out, PJ, a.ni + (a.ni - 1 - v), jc, g);
+            } else if (a.bc[1] == E_OUTFLOW && v == a.ni - 1) {
+                store4(a.out, PJ, a.ni, jc, U);
+                store4(a.out, PJ, a.ni + 1, jc, U);
+            }
+            if constexpr (NORMS) {
 #pragma unroll
                 for (int c = 0; c < 4; ++c) {
-                    const double wm = sv[c * SMEM_ROW + own - 1];
-                    const double w = sv[c * SMEM_ROW + own];
-                    const double wp = sv[c * SMEM_ROW + own + 1];
-                    double qN;
-                    muscl_cell(w, w - wm, wp - w, P, qN, qS[c]);
-                    xq[c * NT + t] = qN;
-                    Wv[c] = w;
+                    nrm[c] = fma(R[c], R[c], nrm[c]);
+                    nrm[4 + c] = fmax(nrm[4 + c], fabs(R[c]));
                 }
             }
-            if (v == 0 && is_out) { nWx = mv[0 * SMEM_ROW + own]; nWy = mv[1 * SMEM_ROW + own]; }
-            __syncthreads();
-            if (t == 0) {
-                const int lim = min(v - 1 + TR::NS, r_last);
-                for (; next_issue <= lim; ++next_issue) issue(next_issue);
+            if constexpr (DTMAX) {
+                // sigma/V of the new state for dt_{n+1} (reading A-R6)
+                const double ir = frcp(U[0]);
+                const double u = U[1] * ir, vv = U[2] * ir;
+                const double p = P.gm1 * fma(-0.5, fma(U[1], u, U[2] * vv), U[3]);
+                const double x = P.gamma * p * ir;
+                const double snd = x * frsqrt(x);
+                const double tW = (fabs(fma(u, wfx, vv * wfy)) + snd) * wfA;
+                const double tE = (fabs(fma(u, mv[0 * SMEM_ROW + own], vv * mv[1 * SMEM_ROW + own])) + snd) *
+                                  mv[2 * SMEM_ROW + own];
+                const double tS = (fabs(fma(u, mv[3 * SMEM_ROW + own], vv * mv[4 * SMEM_ROW + own])) + snd) *
+                                  mv[5 * SMEM_ROW + own];
+                const double tN = (fabs(fma(u, mv[3 * SMEM_ROW + own + 1], vv * mv[4 * SMEM_ROW + own + 1])) + snd) *
+                                  mv[5 * SMEM_ROW + own + 1];
+                smax = fmax(smax, (((tW + tE) + tS) + tN) * iV);
             }
-            double GS[4];
-            if (jflux) {
-                double qN[4];
-#pragma unroll
-                for (int c = 0; c < 4; ++c) qN[c] = xq[c * NT + t - 1];
-                const double nx = mv[3 * SMEM_ROW + own], ny = mv[4 * SMEM_ROW + own], A = mv[5 * SMEM_ROW + own];
-                if (!roe_flux(qN, qS, nx, ny, A, P, GS)) {
-                    int J = a.gj0 + jc;
-                    if (J > a.NJ - 1) J = a.NJ - 1;
-                    atomicMin(a.err, err_key(n, a.nstages, a.stage, 0, (long long)J * a.NI + a.gi0 + v));
-                }
-#pragma unroll
-                for (int c = 0; c < 4; ++c) xg[c * NT + t] = GS[c];
-            }
-            __syncthreads();
-            if (is_out) {
-                // ---- residual (Eq. 5) and stage update (Eq. 6) ---------------
-                const double iV = mv[6 * SMEM_ROW + own];
-                double R[4], U[4];
-#pragma unroll
-                for (int c = 0; c < 4; ++c) {
-                    const double GN = xg[c * NT + t + 1];
-                    R[c] = ((GE[c] - GW[c]) + GN) - GS[c];
-                }
-                const double *pwr = sv + (4 + NMET) * SMEM_ROW;
-#pragma unroll
-                for (int c = 0; c < 4; ++c) {
-                    const double rv = R[c] * iV;
-                    if (MODE == M_OWN) {
-                        U[c] = fma(-coef, rv, Wv[c]);
-                    } else if (MODE == M_UN) {
-                        U[c] = fma(-coef, rv, pwr[c * SMEM_ROW + own]);
-                    } else if (MODE == M_RK4F) {
-                        const double un = pwr[c * SMEM_ROW + own];
-                        const double d2 = pwr[(4 + c) * SMEM_ROW + own] - un;
-                        const double d3 = pwr[(8 + c) * SMEM_ROW + own] - un;
-                        const double d4 = Wv[c] - un;
-                        const double comb = (fma(2.0, d3, d2) + d4) * (1.0 / 3.0);
-                        U[c] = un + fma(-coef, rv, comb);
-                    } else {  // M_HEUNF
-                        const double un = pwr[c * SMEM_ROW + own];
-                        U[c] = un + fma(-coef, rv, 0.5 * (Wv[c] - un));
-                    }
-                }
-                store4(a.out, PJ, v, jc, U);
-                // new-state validity: rho > 0 and 2 rho E > |m|^2 (<=> p > 0)
-                if (!((U[0] > 0.0) & (2.0 * U[0] * U[3] > fma(U[1], U[1], U[2] * U[2]))))
-                    atomicMin(a.err, err_key(n, a.nstages, a.stage, 1,
-                                             (long long)(a.gj0 + jc) * a.NI + a.gi0 + v));
-                // physical-boundary ghosts of the new state (reading A-R11)
-                if (a.bc[2] == E_SLIP && jc <= 1) {
-                    double g[4];
-                    const int k0 = own - jc;  // column 0
-                    mirror(U, mv[3 * SMEM_ROW + k0], mv[4 * SMEM_ROW + k0], g);
-                    store4(a.out, PJ, v, -1 - jc, g);
-                } else if (a.bc[2] == E_OUTFLOW && jc == 0) {
-                    store4(a.out, PJ, v, -1, U);
-                    store4(a.out, PJ, v, -2, U);
-                }
-                if (a.bc[3] == E_SLIP && jc >= a.nj - 2) {
-                    double g[4];
-                    const int kN = own + (a.nj - jc);  // column nj
-                    mirror(U, mv[3 * SMEM_ROW + kN], mv[4 * SMEM_ROW + kN], g);
-                    store4(a.out, PJ, v, a.nj + (a.nj - 1 - jc), g);
-                } else if (a.bc[3] == E_OUTFLOW && jc == a.nj - 1) {
-                    store4(a.out, PJ, v, a.nj, U);
-                    store4(a.out, PJ, v, a.nj + 1, U);
-                }
-                if (a.bc[0] == E_SLIP && v <= 1) {
-                    double g[4];
-                    mirror(U, nWx, nWy, g);
-                    store4(a.out, PJ, -1 - v, jc, g);
-                } else if (a.bc[0] == E_OUTFLOW && v == 0) {
-                    store4(a.out, PJ, -1, jc, U);
-                    store4(a.out, PJ, -2, jc, U);
-                }
-                if (a.bc[1] == E_SLIP && v >= a.ni - 2) {
-                    double g[4];
-                    const double *mE = slot_of(a.ni) + 4 * SMEM_ROW;  // resident: ni <= v+2
-                    mirror(U, mE[0 * SMEM_ROW + own], mE[1 * SMEM_ROW + own], g);
-                    store4(a.out, PJ, a.ni + (a.ni - 1 - v), jc, g);
-                } else if (a.bc[1] == E_OUTFLOW && v == a.ni - 1) {
-                    store4(a.out, PJ, a.ni, jc, U);
-                    store4(a.out, PJ, a.ni + 1, jc, U);
-                }
-                if (NORMS) {
-#pragma unroll
-                    for (int c = 0; c < 4; ++c) {
-                        nrm[c] = fma(R[c], R[c], nrm[c]);
-                        nrm[4 + c] = fmax(nrm[4 + c], fabs(R[c]));
-                    }
-                }
-                if (DTMAX) {
-                    // sigma/V of the new state for dt_{n+1} (reading A-R6)
-                    const double ir = frcp(U[0]);
-                    const double u = U[1] * ir, vv = U[2] * ir;
-                    const double p = P.gm1 * fma(-0.5, fma(U[1], u, U[2] * vv), U[3]);
-                    const double x = P.gamma * p * ir;
-                    const double snd = x * frsqrt(x);
-                    const double *m1 = slot_of(v + 1) + 4 * SMEM_ROW;
-                    const double tW = (fabs(fma(u, mv[0 * SMEM_ROW + own], vv * mv[1 * SMEM_ROW + own])) + snd) *
-                                      mv[2 * SMEM_ROW + own];
-                    const double tE = (fabs(fma(u, m1[0 * SMEM_ROW + own], vv * m1[1 * SMEM_ROW + own])) + snd) *
-                                      m1[2 * SMEM_ROW + own];
-                    const double tS = (fabs(fma(u, mv[3 * SMEM_ROW + own], vv * mv[4 * SMEM_ROW + own])) + snd) *
-                                      mv[5 * SMEM_ROW + own];
-                    const double tN =
-                        (fabs(fma(u, mv[3 * SMEM_ROW + own + 1], vv * mv[4 * SMEM_ROW + own + 1])) + snd) *
-                        mv[5 * SMEM_ROW + own + 1];
-                    smax = fmax(smax, (((tW + tE) + tS) + tN) * iV);
-                }
-            }
+        }
+        if constexpr (DTMAX) {
+            wfx = mv[0 * SMEM_ROW + own];
+            wfy = mv[1 * SMEM_ROW + own];
+            wfA = mv[2 * SMEM_ROW + own];
         }
 #pragma unroll
         for (int c = 0; c < 4; ++c) GW[c] = GE[c];
@@ -615,25 +652,27 @@ __global__ void metrics_kernel(const MetricsArgs a) {
     const int W = a.ni + 1;
     auto X = [&](int ii, int jj) { return a.x[(size_t)jj * W + ii]; };
     auto Y = [&](int ii, int jj) { return a.y[(size_t)jj * W + ii]; };
-    double *row = a.met + (size_t)(i * NMET) * a.PJ + (j + JOFF);
+    // memory row m holds i-face(m) (fields 0-2) and j-face(m-1), 1/V(m-1) (fields 3-6)
+    double *rowI = a.met + (size_t)(i * NMET) * a.PJ + (j + JOFF);
+    double *rowJ = a.met + (size_t)((i + 1) * NMET) * a.PJ + (j + JOFF);
     if (j < a.nj) {  // i-face (i, j)
         const double tx = __dsub_rn(X(i, j + 1), X(i, j)), ty = __dsub_rn(Y(i, j + 1), Y(i, j));
         const double A = __dsqrt_rn(__dadd_rn(__dmul_rn(tx, tx), __dmul_rn(ty, ty)));
-        row[0 * (size_t)a.PJ] = __ddiv_rn(ty, A);
-        row[1 * (size_t)a.PJ] = __ddiv_rn(-tx, A);
-        row[2 * (size_t)a.PJ] = A;
+        rowI[0 * (size_t)a.PJ] = __ddiv_rn(ty, A);
+        rowI[1 * (size_t)a.PJ] = __ddiv_rn(-tx, A);
+        rowI[2 * (size_t)a.PJ] = A;
     }
     if (i < a.ni) {  // j-face (i, j)
         const double tx = __dsub_rn(X(i + 1, j), X(i, j)), ty = __dsub_rn(Y(i + 1, j), Y(i, j));
         const double A = __dsqrt_rn(__dadd_rn(__dmul_rn(tx, tx), __dmul_rn(ty, ty)));
-        row[3 * (size_t)a.PJ] = __ddiv_rn(-ty, A);
-        row[4 * (size_t)a.PJ] = __ddiv_rn(tx, A);
-        row[5 * (size_t)a.PJ] = A;
+        rowJ[3 * (size_t)a.PJ] = __ddiv_rn(-ty, A);
+        rowJ[4 * (size_t)a.PJ] = __ddiv_rn(tx, A);
+        rowJ[5 * (size_t)a.PJ] = A;
         if (j < a.nj) {
             const double V = __dmul_rn(
                 0.5, __dsub_rn(__dmul_rn(__dsub_rn(X(i + 1, j + 1), X(i, j)), __dsub_rn(Y(i, j + 1), Y(i + 1, j))),
                                __dmul_rn(__dsub_rn(Y(i + 1, j + 1), Y(i, j)), __dsub_rn(X(i, j + 1), X(i + 1, j)))));
-            row[6 * (size_t)a.PJ] = __ddiv_rn(1.0, V);
+            rowJ[6 * (size_t)a.PJ] = __ddiv_rn(1.0, V);
             if (!(V > 0.0)) atomicMin(a.bad, (unsigned long long)((long long)j * a.ni + i));
         }
     }
@@ -700,10 +739,10 @@ __global__ void bc_fill_kernel(double *buf, const double *met, int ni, int nj, i
         const int i = k;
         if (bc.z == E_INFLOW) { double q[4] = {in2.x, in2.y, in2.z, in2.w}; st(i, -1 - m, q); }
         else if (bc.z == E_OUTFLOW) { ld(i, 0, u); st(i, -1 - m, u); }
-        else if (bc.z == E_SLIP) { ld(i, m, u); mirror(u, metv(i, 3, 0), metv(i, 4, 0), g); st(i, -1 - m, g); }
+        else if (bc.z == E_SLIP) { ld(i, m, u); mirror(u, metv(i + 1, 3, 0), metv(i + 1, 4, 0), g); st(i, -1 - m, g); }
         if (bc.w == E_INFLOW) { double q[4] = {in3.x, in3.y, in3.z, in3.w}; st(i, nj + m, q); }
         else if (bc.w == E_OUTFLOW) { ld(i, nj - 1, u); st(i, nj + m, u); }
-        else if (bc.w == E_SLIP) { ld(i, nj - 1 - m, u); mirror(u, metv(i, 3, nj), metv(i, 4, nj), g); st(i, nj + m, g); }
+        else if (bc.w == E_SLIP) { ld(i, nj - 1 - m, u); mirror(u, metv(i + 1, 3, nj), metv(i + 1, 4, nj), g); st(i, nj + m, g); }
     }
 }
 cudaError_t launch_bc_fill(double *buf, const double *met, int ni, int nj, int PJ, const int bc[4],
@@ -777,9 +816,9 @@ __global__ void sigma_kernel(const double *buf, const double *met, int ni, int n
         const double snd = x * frsqrt(x);
         const double tW = (fabs(fma(u, m(i, 0, j), vv * m(i, 1, j))) + snd) * m(i, 2, j);
         const double tE = (fabs(fma(u, m(i + 1, 0, j), vv * m(i + 1, 1, j))) + snd) * m(i + 1, 2, j);
-        const double tS = (fabs(fma(u, m(i, 3, j), vv * m(i, 4, j))) + snd) * m(i, 5, j);
-        const double tN = (fabs(fma(u, m(i, 3, j + 1), vv * m(i, 4, j + 1))) + snd) * m(i, 5, j + 1);
-        s = (((tW + tE) + tS) + tN) * m(i, 6, j);
+        const double tS = (fabs(fma(u, m(i + 1, 3, j), vv * m(i + 1, 4, j))) + snd) * m(i + 1, 5, j);
+        const double tN = (fabs(fma(u, m(i + 1, 3, j + 1), vv * m(i + 1, 4, j + 1))) + snd) * m(i + 1, 5, j + 1);
+        s = (((tW + tE) + tS) + tN) * m(i + 1, 6, j);
     }
     for (int o = 16; o > 0; o >>= 1) s = fmax(s, __shfl_xor_sync(0xffffffffu, s, o));
     if ((threadIdx.x & 31) == 0 && s > 0.0)

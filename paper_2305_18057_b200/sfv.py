@@ -15,7 +15,7 @@ import numpy as np
 from . import inputs as _inputs
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libsfv.so")
+LIB_PATH = os.environ.get("SFV_LIB") or os.path.join(HERE, "libsfv.so")  # SFV_LIB: A/B builds only
 
 OK, ERR_ARG, ERR_GEOMETRY, ERR_STATE, ERR_SEQUENCE, ERR_CUDA, ERR_NCCL, ERR_OOM, ERR_UNSUPPORTED = range(9)
 _NAMES = ["OK", "ARG", "GEOMETRY", "STATE", "SEQUENCE", "CUDA", "NCCL", "OOM", "UNSUPPORTED"]

@@ -107,14 +107,23 @@ def test_other_tableaus(sfv_mod, oracle_mod, rk):
     check(g, o, 1e-10)
 
 
+LOW_MACH = np.array([0.2, 60.0, 0.0, 12270.0])   # (rho, u, v, p), M ~ 0.2
+
+
 @pytest.mark.parametrize("kw", [dict(limiter=I.LIM_NONE, cfl=0.3),
                                 dict(kappa=1.0 / 3.0), dict(kappa=0.0), dict(eps=0.0),
                                 dict(harten_eps=0.0), dict(harten_eps=0.3)])
 def test_scheme_options(sfv_mod, oracle_mod, kw):
     ni, nj = 80, 40
     X, Y = I.ramp_nodes(ni, nj, 30.0)
-    cfg = I.default_config(ni, nj, **kw)
-    U0 = I.perturbed_state(ni, nj, 9)
+    if kw.get("limiter") == I.LIM_NONE:
+        # unlimited MUSCL at Mach 4 creates invalid face states (both sides
+        # reject them); use a subsonic perturbed state for this option
+        U0 = I.perturbed_state(ni, nj, 9, prim0=LOW_MACH)
+        cfg = I.default_config(ni, nj, inflow=I.conserved_from_primitive(LOW_MACH), **kw)
+    else:
+        cfg = I.default_config(ni, nj, **kw)
+        U0 = I.perturbed_state(ni, nj, 9)
     g, o = run_pair(sfv_mod, oracle_mod, cfg, X, Y, U0, 1)
     check(g, o, 1e-12)
     g.step(19); g.sync(); o.step(19)
@@ -136,10 +145,12 @@ def test_va1_limiter_option(sfv_mod, oracle_mod):
 @pytest.mark.parametrize("bc", [(0, 1, 2, 2), (0, 1, 2, 1), (2, 2, 2, 2), (1, 1, 1, 1), (0, 0, 0, 0),
                                 (2, 1, 0, 2), (1, 2, 2, 0)])
 def test_boundary_combinations(sfv_mod, oracle_mod, bc):
+    """All edge-kind combinations (reading A-R11) on a subsonic perturbed
+    state, so that every combination (closed boxes included) is valid."""
     ni, nj = 40, 36
     X, Y = I.ramp_nodes(ni, nj, 10.0)
-    U0 = I.perturbed_state(ni, nj, 3)
-    cfg = I.default_config(ni, nj, bc=bc, cfl=0.5)
+    U0 = I.perturbed_state(ni, nj, 3, prim0=LOW_MACH)
+    cfg = I.default_config(ni, nj, bc=bc, cfl=0.5, inflow=I.conserved_from_primitive(LOW_MACH))
     g, o = run_pair(sfv_mod, oracle_mod, cfg, X, Y, U0, 1)
     check(g, o, 1e-12)
     g.step(29); g.sync(); o.step(29)
@@ -232,6 +243,26 @@ def test_state_error_reported(sfv_mod, oracle_mod):
         g.sync()
     assert eg.value.code == sfv_mod.ERR_STATE
     assert eg.value.info[:2] == eo.value.info[:2], (eg.value.info, eo.value.info)
+
+
+@pytest.mark.parametrize("case", ["box", "wall"])
+def test_state_error_parity_mach4_walls(sfv_mod, oracle_mod, case):
+    """Mach-4 flow driven into slip walls produces an invalid face state at
+    the first steps; both sides report the same (step, stage, i, j)."""
+    ni, nj = 40, 36
+    X, Y = I.ramp_nodes(ni, nj, 10.0)
+    U0 = I.perturbed_state(ni, nj, 3)
+    bc = (2, 2, 2, 2) if case == "box" else (2, 1, 0, 2)
+    cfg = I.default_config(ni, nj, bc=bc, cfl=0.5)
+    g = sfv_mod.Solver(cfg, X, Y); o = oracle_mod.Oracle(cfg, X, Y)
+    g.set_state(U0); o.set_state(U0)
+    with pytest.raises(oracle_mod.OracleError) as eo:
+        o.step(30)
+    g.step(30)
+    with pytest.raises(sfv_mod.SfvError) as eg:
+        g.sync()
+    assert eg.value.code == sfv_mod.ERR_STATE
+    assert eg.value.info == eo.value.info, (eg.value.info, eo.value.info)
 
 
 def test_set_state_rejects_invalid(sfv_mod):
