@@ -54,7 +54,7 @@ def workload(name, n_gpus):
     if name == "C2":
         ni, nj = 1440 * n_gpus, 720
         desc = (f"C2 2D supersonic inlet, 30-deg ramp, {1440}x{720} cells per GPU "
-                f"(global {ni}x{nj}), Table 1 freestream, RK4 CFL 0.8, VA limiter, Roe+Harten")
+                f"(global {ni}x{nj}), Table 1 freestream, RK4 CFL 0.8, bounded van Albada MUSCL, Roe+Harten")
         return ni, nj, 30.0, desc, "weak", n_gpus
     if name == "C4":
         ni, nj = 5760 * n_gpus, 2880

@@ -72,6 +72,7 @@ struct Block {
     double *met = nullptr, *nodes = nullptr, *stage = nullptr, *partials = nullptr;
     unsigned *ticket = nullptr;
     double *xs[2] = {nullptr, nullptr}, *xr[2] = {nullptr, nullptr};  // j-cut pack buffers (S, N)
+    CUtensorMap tm_buf[4], tm_met;  // 2D TMA descriptors (made at sfv_bind)
     size_t buf_elems() const { return (size_t)(ni + 4) * 4 * PJ + PADD; }
     size_t met_elems() const { return (size_t)(ni + 1) * NMET * PJ + PADD; }
 };
@@ -206,6 +207,8 @@ void build_params(sfv_ctx *c) {
     P.c1 = f.muscl_eps * (1.0 - f.muscl_kappa) / 4.0;
     P.c2 = f.muscl_eps * (1.0 + f.muscl_kappa) / 4.0;
     P.delta = f.lim_delta;
+    P.c1x2 = 2.0 * P.c1;
+    P.c1d = P.c1 * f.lim_delta;
     P.heps = f.harten_eps;
     P.hinv = f.harten_eps > 0.0 ? 0.5 / f.harten_eps : 0.0;
     P.cfl = f.cfl;
@@ -216,8 +219,8 @@ void build_params(sfv_ctx *c) {
 // Launch geometry: strips of <= NT-4 columns (even starts), segments along i
 // so that strips*segments fills the device in whole waves.
 void choose_launch(sfv_ctx *c, Block &b) {
-    b.nstrips = (b.nj + (NT - 4) - 1) / (NT - 4);
-    const int slots = c->nsm * std::max(1, c->occ);
+    b.nstrips = (b.nj + WOUT - 1) / WOUT;
+    const int slots = c->nsm * std::max(1, c->occ) * WPC;  // resident warps
     int best = 1;
     double best_score = -1.0;
     const int cap = std::min(NSEG_MAX, std::max(1, b.ni / 4));
@@ -256,7 +259,7 @@ sfv_status build_blocks(sfv_ctx *c) {
         b.nbr[2] = b.by > 0 ? id - c->px : -1;
         b.nbr[3] = b.by < c->py - 1 ? id + c->px : -1;
         for (int e = 0; e < 4; ++e) b.edge[e] = b.nbr[e] >= 0 ? E_CONNECTED : c->cfg.bc[e];
-        b.nstrips = (b.nj + (NT - 4) - 1) / (NT - 4);
+        b.nstrips = (b.nj + WOUT - 1) / WOUT;
         b.nseg = 1;
         c->blocks.push_back(b);
     }
@@ -294,7 +297,7 @@ size_t layout(sfv_ctx *c, bool assign) {
         size_t om = take(sizeof(double) * b.met_elems());
         size_t on = take(sizeof(double) * 2 * (size_t)(b.ni + 1) * (b.nj + 1));
         size_t os = take(sizeof(double) * 4 * (size_t)b.ni * b.nj);
-        const int max_cta = ((b.nj + (NT - 4) - 1) / (NT - 4)) * NSEG_MAX;
+        const int max_cta = (((b.nj + WOUT - 1) / WOUT) * NSEG_MAX + WPC - 1) / WPC;
         size_t op = take(sizeof(double) * 8 * (size_t)max_cta);
         size_t ot = take(256);
         size_t ox[4];
@@ -401,6 +404,9 @@ sfv_status exchange(sfv_ctx *c, int k, cudaStream_t st) {
 StageArgs make_args(sfv_ctx *c, Block &b, int k) {
     const StageSpec sp = stage_spec(c->cfg.rk, k);
     StageArgs a{};
+    a.tm_in = b.tm_buf[sp.in];
+    a.tm_met = b.tm_met;
+    for (int q = 0; q < 3; ++q) a.tm_pw[q] = b.tm_buf[sp.pw[q] >= 0 ? sp.pw[q] : sp.in];
     a.in = b.buf[sp.in];
     a.out = b.buf[sp.out];
     a.pw0 = sp.pw[0] >= 0 ? b.buf[sp.pw[0]] : nullptr;
@@ -610,7 +616,7 @@ sfv_status sfv_bind(sfv_ctx *c, void *ws, size_t bytes, void *stream) {
     c->nsm = prop.multiProcessorCount;
     int o = 1;
     CK(prepare_stage_kernels());
-    CK(stage_occupancy(M_UN, false, false, &o));
+    CK(stage_occupancy(M_UN, false, false, fast_path(c->P), &o));
     c->occ = std::max(1, o);
     CK(cudaEventCreate(&c->ev0));
     CK(cudaEventCreate(&c->ev1));
@@ -618,8 +624,12 @@ sfv_status sfv_bind(sfv_ctx *c, void *ws, size_t bytes, void *stream) {
     CK(cudaMemsetAsync(c->ws, 0, need, st));
     CK(cudaMemsetAsync(c->geo_bad, 0xff, 8, st));
     const int W = c->cfg.ni + 1;
+    const int nbuf = nbuf_of(c->cfg.rk);
     for (Block &b : c->blocks) {
         choose_launch(c, b);
+        for (int k = 0; k < nbuf; ++k)
+            CK(make_row_tensor_map(&b.tm_buf[k], b.buf[k], (unsigned long long)(b.ni + 4) * 4, b.PJ, 4));
+        CK(make_row_tensor_map(&b.tm_met, b.met, (unsigned long long)(b.ni + 1) * NMET, b.PJ, NMET));
         // block-local nodes, [j][i]
         std::vector<double> h(2 * (size_t)(b.ni + 1) * (b.nj + 1));
         const size_t nn = (size_t)(b.ni + 1) * (b.nj + 1);

@@ -3,6 +3,7 @@
 // oracle (oracle/), which is test infrastructure.
 #pragma once
 #include <cstdint>
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 namespace sfv {
@@ -21,6 +22,8 @@ constexpr int NMET = 7;
 constexpr int SMEM_ROW = 132;     // doubles per staged row in shared memory
 constexpr int ROW_COLS = 130;     // columns staged per row: j0-2 .. j0+127
 constexpr int NT = 128;           // threads per CTA of the stage kernel
+constexpr int WPC = NT / 32;      // independent warps per CTA
+constexpr int WOUT = 30;          // output columns per warp strip (+1 halo lane each side)
 
 
 enum Mode { M_OWN = 0, M_UN = 1, M_RK4F = 2, M_HEUNF = 3 };
@@ -29,6 +32,7 @@ enum Edge { E_INFLOW = 0, E_OUTFLOW = 1, E_SLIP = 2, E_CONNECTED = 3 };
 struct Params {
     double gamma, gm1;
     double c1, c2;          // eps(1-kappa)/4, eps(1+kappa)/4 (Eq. 7)
+    double c1x2, c1d;       // 2 c1, c1 delta (fast path: bounded van Albada, kappa = -1)
     double delta;           // limiter guard
     double heps, hinv;      // Harten eps and 0.5/eps
     double cfl, dt_fixed;
@@ -36,6 +40,9 @@ struct Params {
 };
 
 struct StageArgs {
+    // 2D TMA descriptors: state buffers as [(ni+4)*4 rows][PJ] doubles,
+    // metrics as [(ni+1)*7 rows][PJ]; boxes of 36 columns x 4 (7) rows
+    CUtensorMap tm_in, tm_met, tm_pw[3];
     const double *in;       // stage input (stencil)
     double *out;            // stage output
     const double *pw0, *pw1, *pw2;   // pointwise inputs (U^n, W2, W3)
@@ -67,7 +74,8 @@ struct MetricsArgs {
 
 // launchers (sfv_kernels.cu); all asynchronous on `st`
 cudaError_t launch_stage(const StageArgs &a, int mode, bool norms, bool dtmax, cudaStream_t st);
-cudaError_t stage_occupancy(int mode, bool norms, bool dtmax, int *ctas_per_sm);
+cudaError_t stage_occupancy(int mode, bool norms, bool dtmax, bool fast, int *ctas_per_sm);
+bool fast_path(const Params &P);
 cudaError_t prepare_stage_kernels();
 size_t stage_smem_bytes(int mode);
 cudaError_t launch_metrics(const MetricsArgs &a, cudaStream_t st);
@@ -83,6 +91,8 @@ cudaError_t launch_sigma(const double *buf, const double *met, int ni, int nj, i
                          double *sig, cudaStream_t st);
 cudaError_t launch_pack_cols(const double *buf, double *dst, int ni, int PJ, int j_first, cudaStream_t st);
 cudaError_t launch_unpack_cols(const double *src, double *buf, int ni, int PJ, int j_first, cudaStream_t st);
+// cuTensorMapEncodeTiled through the runtime's driver entry point
+cudaError_t make_row_tensor_map(CUtensorMap *m, const double *base, unsigned long long rows, int PJ, int box_rows);
 cudaError_t launch_debug_math(int which, const double *in, double *out, long long n, cudaStream_t st);
 
 }  // namespace sfv

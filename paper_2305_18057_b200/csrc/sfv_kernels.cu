@@ -53,6 +53,14 @@ __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, unsigned by
         : "memory");
 }
 
+__device__ __forceinline__ void tma_2d(void *dst, const CUtensorMap *map, int x, int y, uint64_t *bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+            smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(smem_u32(bar))
+        : "memory");
+}
+
 // Fast reciprocal / reciprocal square root: MUFU seed + one cubic-convergent
 // correction (relative error ~ seed^3 << 2^-53, i.e. within ~1 ulp).
 __device__ __forceinline__ double frcp(double d) {
@@ -83,8 +91,19 @@ __device__ __forceinline__ unsigned long long err_key(long long n, int nstages, 
 // (reading A-R4).  For VA1 both psi(f,b) b and psi(b,f) f share one
 // denominator b^2 + f^2 + delta: one reciprocal per cell, direction and
 // component.
+template <bool FAST>
 __device__ __forceinline__ void muscl_cell(double w, double b, double f, const Params &P, double &qU,
                                            double &qD) {
+    if constexpr (FAST) {
+        // bounded van Albada, kappa = -1 (c2 = 0): s1 = c1 max(0, (2bf+d)/(b^2+f^2+d))
+        //   qU = w + s1 b,  qD = w - s1 f
+        const double r = frcp(fma(b, b, fma(f, f, P.delta)));
+        double s1 = fma(P.c1x2, b * f, P.c1d) * r;
+        s1 = s1 > 0.0 ? s1 : 0.0;
+        qU = fma(s1, b, w);
+        qD = fma(-s1, f, w);
+        return;
+    }
     double pb, pf;  // psi(f,b)*b, psi(b,f)*f
     if (P.limiter == 0) {
         double bf = b * f;
@@ -148,16 +167,14 @@ __device__ __forceinline__ bool roe_flux(const double qL[4], const double qR[4],
     double l1 = fabs(Vnt - at);
     const double l2 = fabs(Vnt);
     double l4 = fabs(Vnt + at);
-    double dH = P.heps * at, inv2dH;
-    if (dH < 1e-12) {
-        dH = 1e-12;
-        inv2dH = 0.5e12;
-    } else {
-        inv2dH = P.hinv * ra;  // 1/(2 eps a) = (0.5/eps) (1/a)
-    }
+    double dH = P.heps * at;
+    const bool floor_h = dH < 1e-12;
+    const double inv2dH = floor_h ? 0.5e12 : P.hinv * ra;  // 1/(2 eps a) = (0.5/eps) (1/a)
+    dH = floor_h ? 1e-12 : dH;
     const double dH2 = dH * dH;
-    if (l1 < dH) l1 = fma(l1, l1, dH2) * inv2dH;
-    if (l4 < dH) l4 = fma(l4, l4, dH2) * inv2dH;
+    const double l1f = fma(l1, l1, dH2) * inv2dH, l4f = fma(l4, l4, dH2) * inv2dH;
+    l1 = l1 < dH ? l1f : l1;
+    l4 = l4 < dH ? l4f : l4;
 
     const double a1l = l1 * a1, a4l = l4 * a4, a2l = l2 * a2w, r = l2 * rhot;
     const double S = a1l + a4l, Dd = a4l - a1l;
@@ -195,323 +212,312 @@ __device__ __forceinline__ void store4(double *buf, int PJ, int i, int j, const 
 }
 
 // ------------------------------------------------------------ stage kernel
+// Warp-independent layout: every warp owns a strip of WOUT = 30 output
+// columns [j0, j0+30) plus one halo lane on each side (lane l <-> column
+// j0-1+l) and marches along i over a segment of rows with its own TMA rings
+// and mbarriers.  j-face states / fluxes move between lanes by __shfl, so the
+// main loop has no CTA-wide barrier; warps drift independently.
+constexpr int WROW = 36;  // staged doubles per row: columns j0-2 .. j0+33 (288 B)
+
 template <int MODE>
 struct StageTraits {
     static constexpr int NPW = MODE == M_OWN ? 0 : (MODE == M_RK4F ? 3 : 1);
-    static constexpr int NS_W = 4;                    // stencil ring: rows v..v+2 + 1 in flight
-    static constexpr int NS_M = 2;                    // metrics ring: row v + 1 in flight
-    static constexpr int W_SLOT = 4 * SMEM_ROW;
-    static constexpr int M_SLOT = NMET * SMEM_ROW;
-    static constexpr int P_SLOT = 4 * NPW * SMEM_ROW; // pointwise: row v only
-    static constexpr int NBAR = NS_W + NS_M + 1;
+    static constexpr int W_SLOT = 4 * WROW;           // stencil ring: 4 rows (v..v+2 + 1 in flight), 1152 B
+    static constexpr int M_SLOT = 256;                // metrics ring: 2 rows (v + 1 in flight), 7*288 B -> 2 KB
+    static constexpr int P_SLOT = 4 * NPW * WROW;     // pointwise: row v
+    static constexpr int WARP_DBL = 4 * W_SLOT + 2 * M_SLOT + P_SLOT + 16;  // + 7 mbarriers, 128 B aligned
 };
 
 template <int MODE>
 __host__ __device__ constexpr size_t stage_smem() {
-    using T = StageTraits<MODE>;
-    return sizeof(double) * ((size_t)T::NS_W * T::W_SLOT + (size_t)T::NS_M * T::M_SLOT + T::P_SLOT + 8 * NT +
-                             8 * (NT / 32)) +
-           sizeof(uint64_t) * T::NBAR;
+    return sizeof(double) * ((size_t)WPC * StageTraits<MODE>::WARP_DBL + 8 * (NT / 32));
 }
 
-// Metrics "row" r (r in [-1, ni)) = memory row r+1 = { i-face(r+1) nx, ny, A;
-// j-face(r) nx, ny, A; 1/V(r) }: everything iteration v needs is in row v.
 #ifndef SFV_MINB
 #define SFV_MINB 4  // resident CTAs per SM the register allocation targets
 #endif
-template <int MODE, bool NORMS, bool DTMAX>
-__global__ void __launch_bounds__(NT, SFV_MINB) stage_kernel(const StageArgs a);
 
-template <int MODE, bool NORMS, bool DTMAX>
-__global__ void __launch_bounds__(NT, SFV_MINB) stage_kernel(const StageArgs a) {
+template <int MODE, bool NORMS, bool DTMAX, bool FAST>
+__global__ void __launch_bounds__(NT, SFV_MINB) stage_kernel(const __grid_constant__ StageArgs a) {
     using TR = StageTraits<MODE>;
     extern __shared__ __align__(128) double smem[];
-    double *wring = smem;                           // [NS_W][4][SMEM_ROW] stencil rows
-    double *mring = wring + TR::NS_W * TR::W_SLOT;  // [NS_M][7][SMEM_ROW] metric rows
-    double *pring = mring + TR::NS_M * TR::M_SLOT;  // [4*NPW][SMEM_ROW] pointwise row
-    double *xq = pring + TR::P_SLOT;                // [4][NT] north face states
-    double *xg = xq + 4 * NT;                       // [4][NT] south face fluxes
-    double *red = xg + 4 * NT;                      // [8][NT/32]
-    uint64_t *wbar = reinterpret_cast<uint64_t *>(red + 8 * (NT / 32));
-    uint64_t *mbar = wbar + TR::NS_W;
-    uint64_t *pbar = mbar + TR::NS_M;
+    const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+    double *wbase = smem + warp * TR::WARP_DBL;
+    double *wring = wbase;                      // [4][4][WROW]
+    double *mring = wring + 4 * TR::W_SLOT;     // [2][7][WROW]
+    double *pring = mring + 2 * TR::M_SLOT;     // [4*NPW][WROW]
+    uint64_t *wbar = reinterpret_cast<uint64_t *>(pring + TR::P_SLOT);  // [4]
+    uint64_t *mbar = wbar + 4;                                           // [2]
+    uint64_t *pbar = mbar + 2;                                           // [1]
+    double *red = smem + WPC * TR::WARP_DBL;    // [8][WPC]
 
     const Params &P = a.P;
-    const int t = threadIdx.x;
-    const int strip = blockIdx.x % a.nstrips;
-    const int seg = blockIdx.x / a.nstrips;
-    const int j0 = 2 * (int)(((long long)strip * a.nj) / (2 * a.nstrips));
-    const int j1 = (strip + 1 == a.nstrips) ? a.nj : 2 * (int)(((long long)(strip + 1) * a.nj) / (2 * a.nstrips));
-    const int jc = j0 - 1 + t;                 // this thread's column
-    const bool is_out = (t >= 1) && (jc < j1); // owns output cell (v, jc)
-    const bool jflux = (t >= 1) && (jc <= j1); // its j-face (v, jc) is needed
-    const int own = t + 1;                     // column index inside a staged row
-    const int tm1 = t > 0 ? t - 1 : 0;
-    const int i_start = (int)(((long long)a.ni * seg) / a.nseg);
-    const int i_end = (int)(((long long)a.ni * (seg + 1)) / a.nseg);
-    const int r0 = i_start - 2, r_last = i_end + 1;  // stencil rows
-    const int m0 = i_start - 1, m_last = i_end - 1;  // metric rows
-
     const long long n = *a.step_ctr;
     const double dt = P.dt_fixed > 0.0 ? P.dt_fixed : P.cfl / a.sig[n & 1];
     const double coef = a.coef * dt;
     const int PJ = a.PJ;
-    const size_t col0 = (size_t)(j0 - 2 + JOFF);
-    constexpr unsigned ROWB = ROW_COLS * 8u;
-
-    auto wslot = [&](int r) -> const double * { return wring + ((r - r0) & 3) * TR::W_SLOT; };
-    auto mslot = [&](int r) -> const double * { return mring + ((r - m0) & 1) * TR::M_SLOT; };
-    auto issue_w = [&](int r) {
-        const int s = (r - r0) & 3;
-        mbar_expect_tx(&wbar[s], 4u * ROWB);
-        const double *src = a.in + (size_t)((r + 2) * 4) * PJ + col0;
-#pragma unroll
-        for (int c = 0; c < 4; ++c) bulk_g2s(wring + s * TR::W_SLOT + c * SMEM_ROW, src + (size_t)c * PJ, ROWB, &wbar[s]);
-    };
-    auto issue_m = [&](int r) {
-        const int s = (r - m0) & 1;
-        mbar_expect_tx(&mbar[s], (unsigned)NMET * ROWB);
-        const double *src = a.met + (size_t)((r + 1) * NMET) * PJ + col0;
-#pragma unroll
-        for (int f = 0; f < NMET; ++f)
-            bulk_g2s(mring + s * TR::M_SLOT + f * SMEM_ROW, src + (size_t)f * PJ, ROWB, &mbar[s]);
-    };
-    auto issue_p = [&](int r) {
-        if constexpr (TR::NPW > 0) {
-            mbar_expect_tx(pbar, 4u * TR::NPW * ROWB);
-            const double *pws[3] = {a.pw0, a.pw1, a.pw2};
-#pragma unroll
-            for (int p = 0; p < TR::NPW; ++p) {
-                const double *q = pws[p] + (size_t)((r + 2) * 4) * PJ + col0;
-#pragma unroll
-                for (int c = 0; c < 4; ++c) bulk_g2s(pring + (4 * p + c) * SMEM_ROW, q + (size_t)c * PJ, ROWB, pbar);
-            }
-        }
-    };
-    auto wait_w = [&](int r) { mbar_wait(&wbar[(r - r0) & 3], (unsigned)(((r - r0) >> 2) & 1)); };
-    auto wait_m = [&](int r) { mbar_wait(&mbar[(r - m0) & 1], (unsigned)(((r - m0) >> 1) & 1)); };
-
-    if (t == 0) {
-        for (int s = 0; s < TR::NBAR; ++s) mbar_init(&wbar[s], 1);
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    }
-    __syncthreads();
-    int next_w = r0, next_m = m0;
-    if (t == 0) {
-        for (; next_w <= r0 + 3 && next_w <= r_last; ++next_w) issue_w(next_w);
-        for (; next_m <= m0 + 1 && next_m <= m_last; ++next_m) issue_m(next_m);
-    }
-
-    double Wc[4], fp[4], QLp[4], GW[4];
-    double nWx = 0.0, nWy = 0.0;                     // i-face(0) normal (W-edge slip ghosts)
-    double wfx = 0.0, wfy = 0.0, wfA = 0.0;          // west face of the current row (dt)
     double nrm[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     double smax = 0.0;
 
-    // ---- peeled prologue: rows i_start-2, i_start-1 (i direction only) ------
-    wait_w(r0);
-    wait_w(r0 + 1);
-    wait_w(r0 + 2);
-    {
-        const double *s0 = wslot(r0), *s1 = wslot(r0 + 1), *s2 = wslot(r0 + 2);
-#pragma unroll
-        for (int c = 0; c < 4; ++c) {
-            const double w0 = s0[c * SMEM_ROW + own], w1 = s1[c * SMEM_ROW + own], w2 = s2[c * SMEM_ROW + own];
-            double qU, qD;
-            muscl_cell(w1, w1 - w0, w2 - w1, P, qU, qD);  // cell i_start-1
-            QLp[c] = qU;
-            fp[c] = w2 - w1;
-            Wc[c] = w2;
-        }
-    }
-    __syncthreads();  // rows r0, r0+1 consumed
-    if (t == 0) {
-        for (; next_w <= r0 + 5 && next_w <= r_last; ++next_w) issue_w(next_w);
-    }
-    wait_w(r0 + 3);
-    wait_m(m0);
-    {
-        const double *s3 = wslot(r0 + 3);
-        const double *m = mslot(m0);
-        double qU[4], qD[4];
-#pragma unroll
-        for (int c = 0; c < 4; ++c) {
-            const double wn = s3[c * SMEM_ROW + own];
-            const double f = wn - Wc[c];
-            muscl_cell(Wc[c], fp[c], f, P, qU[c], qD[c]);  // cell i_start
-            fp[c] = f;
-            Wc[c] = wn;
-        }
-        const double nx = m[0 * SMEM_ROW + own], ny = m[1 * SMEM_ROW + own], A = m[2 * SMEM_ROW + own];
-        const bool ok = roe_flux(QLp, qD, nx, ny, A, P, GW);
-        if (!ok && is_out)
-            atomicMin(a.err, err_key(n, a.nstages, a.stage, 0, (long long)(a.gj0 + jc) * a.NI + a.gi0 + i_start));
-        nWx = nx; nWy = ny;
-        wfx = nx; wfy = ny; wfA = A;
-#pragma unroll
-        for (int c = 0; c < 4; ++c) QLp[c] = qU[c];
-    }
+    const int task = blockIdx.x * WPC + warp;
+    if (task < a.nstrips * a.nseg) {
+        const int strip = task % a.nstrips;
+        const int seg = task / a.nstrips;
+        const int j0 = strip * WOUT;
+        const int j1 = min(j0 + WOUT, a.nj);
+        const int jc = j0 - 1 + lane;                // this lane's column
+        const bool is_out = (lane >= 1) && (jc < j1);
+        const bool jflux = (lane >= 1) && (jc <= j1);
+        const int own = lane + 1;                    // column index in a staged row
+        const int i_start = (int)(((long long)a.ni * seg) / a.nseg);
+        const int i_end = (int)(((long long)a.ni * (seg + 1)) / a.nseg);
+        const int r0 = i_start - 2, r_last = i_end + 1;  // stencil rows
+        const int m0 = i_start - 1, m_last = i_end - 1;  // metric rows
+        constexpr unsigned ROWB = WROW * 8u;
 
-    // ---- main loop: one output row per iteration ------------------------------
-    for (int v = i_start; v < i_end; ++v) {
-        wait_w(v + 2);
-        double qD[4], qU[4], qS[4], Wv[4];
-        {
-            const double *sn = wslot(v + 2);
-            const double *sv = wslot(v);
+        auto wslot = [&](int r) -> const double * { return wring + ((r - r0) & 3) * TR::W_SLOT; };
+        auto mslot = [&](int r) -> const double * { return mring + ((r - m0) & 1) * TR::M_SLOT; };
+        // one 2D TMA box per ring row, issued by lane 0 (36 columns x 4 / 7 rows)
+        const int tx = j0 - 2 + JOFF;
+        auto issue_w = [&](int r) {
+            if (lane == 0) {
+                const int s = (r - r0) & 3;
+                mbar_expect_tx(&wbar[s], 4u * ROWB);
+                tma_2d(wring + s * TR::W_SLOT, &a.tm_in, tx, (r + 2) * 4, &wbar[s]);
+            }
+        };
+        auto issue_m = [&](int r) {
+            if (lane == 0) {
+                const int s = (r - m0) & 1;
+                mbar_expect_tx(&mbar[s], (unsigned)NMET * ROWB);
+                tma_2d(mring + s * TR::M_SLOT, &a.tm_met, tx, (r + 1) * NMET, &mbar[s]);
+            }
+        };
+        auto issue_p = [&](int r) {
+            if constexpr (TR::NPW > 0) {
+                if (lane == 0) {
+                    mbar_expect_tx(pbar, 4u * TR::NPW * ROWB);
 #pragma unroll
-            for (int c = 0; c < 4; ++c) {  // i: reconstruct cell v+1
-                const double wn = sn[c * SMEM_ROW + own];
+                    for (int p = 0; p < TR::NPW; ++p) tma_2d(pring + p * 4 * WROW, &a.tm_pw[p], tx, (r + 2) * 4, pbar);
+                }
+            }
+        };
+        auto wait_w = [&](int r) { mbar_wait(&wbar[(r - r0) & 3], (unsigned)(((r - r0) >> 2) & 1)); };
+        auto wait_m = [&](int r) { mbar_wait(&mbar[(r - m0) & 1], (unsigned)(((r - m0) >> 1) & 1)); };
+
+        if (lane == 0) {
+            for (int s = 0; s < 7; ++s) mbar_init(&wbar[s], 1);
+            asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        }
+        __syncwarp();
+        int next_w = r0, next_m = m0;
+        for (; next_w <= r0 + 3 && next_w <= r_last; ++next_w) issue_w(next_w);
+        for (; next_m <= m0 + 1 && next_m <= m_last; ++next_m) issue_m(next_m);
+
+        double Wc[4], fp[4], QLp[4], GW[4];
+        double nWx = 0.0, nWy = 0.0;             // i-face(0) normal (W-edge slip ghosts)
+        double wfx = 0.0, wfy = 0.0, wfA = 0.0;  // west face of the current row (dt)
+
+        // ---- peeled prologue: rows i_start-2, i_start-1 (i direction only) ---
+        wait_w(r0);
+        wait_w(r0 + 1);
+        wait_w(r0 + 2);
+        {
+            const double *s0 = wslot(r0), *s1 = wslot(r0 + 1), *s2 = wslot(r0 + 2);
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+                const double w0 = s0[c * WROW + own], w1 = s1[c * WROW + own], w2 = s2[c * WROW + own];
+                double qU, qD;
+                muscl_cell<FAST>(w1, w1 - w0, w2 - w1, P, qU, qD);  // cell i_start-1
+                QLp[c] = qU;
+                fp[c] = w2 - w1;
+                Wc[c] = w2;
+            }
+        }
+        __syncwarp();  // rows r0, r0+1 consumed
+        for (; next_w <= r0 + 5 && next_w <= r_last; ++next_w) issue_w(next_w);
+        wait_w(r0 + 3);
+        wait_m(m0);
+        {
+            const double *s3 = wslot(r0 + 3);
+            const double *m = mslot(m0);
+            double qU[4], qD[4];
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+                const double wn = s3[c * WROW + own];
                 const double f = wn - Wc[c];
-                muscl_cell(Wc[c], fp[c], f, P, qU[c], qD[c]);
+                muscl_cell<FAST>(Wc[c], fp[c], f, P, qU[c], qD[c]);  // cell i_start
                 fp[c] = f;
                 Wc[c] = wn;
             }
+            const double nx = m[0 * WROW + own], ny = m[1 * WROW + own], A = m[2 * WROW + own];
+            const bool ok = roe_flux(QLp, qD, nx, ny, A, P, GW);
+            if (!ok && is_out)
+                atomicMin(a.err, err_key(n, a.nstages, a.stage, 0, (long long)(a.gj0 + jc) * a.NI + a.gi0 + i_start));
+            nWx = nx; nWy = ny;
+            wfx = nx; wfy = ny; wfA = A;
 #pragma unroll
-            for (int c = 0; c < 4; ++c) {  // j: reconstruct cell (v, jc)
-                const double wm = sv[c * SMEM_ROW + own - 1];
-                const double w = sv[c * SMEM_ROW + own];
-                const double wp = sv[c * SMEM_ROW + own + 1];
-                double qN;
-                muscl_cell(w, w - wm, wp - w, P, qN, qS[c]);
-                xq[c * NT + t] = qN;
-                Wv[c] = w;
-            }
+            for (int c = 0; c < 4; ++c) QLp[c] = qU[c];
         }
-        __syncthreads();  // B1: face states visible, stencil row v-1 / metric row v-1 free
-        if (t == 0) {
-            const int lw = min(v + 3, r_last), lm = min(v + 1, m_last);
-            for (; next_w <= lw; ++next_w) issue_w(next_w);
-            for (; next_m <= lm; ++next_m) issue_m(next_m);
-            issue_p(v);
-        }
-        wait_m(v);
-        const double *mv = mslot(v);
-        double GE[4], GS[4], qN[4];
+
+        // ---- main loop: one output row per iteration ---------------------------
+        for (int v = i_start; v < i_end; ++v) {
+            wait_w(v + 2);
+            double qD[4], qU[4], qS[4], qN[4], Wv[4];
+            {
+                const double *sn = wslot(v + 2);
+                const double *sv = wslot(v);
 #pragma unroll
-        for (int c = 0; c < 4; ++c) qN[c] = xq[c * NT + tm1];
-        // both face fluxes of this row: two independent Roe evaluations
-        const bool okE = roe_flux(QLp, qD, mv[0 * SMEM_ROW + own], mv[1 * SMEM_ROW + own], mv[2 * SMEM_ROW + own], P, GE);
-        const bool okS = roe_flux(qN, qS, mv[3 * SMEM_ROW + own], mv[4 * SMEM_ROW + own], mv[5 * SMEM_ROW + own], P, GS);
+                for (int c = 0; c < 4; ++c) {  // i: reconstruct cell v+1
+                    const double wn = sn[c * WROW + own];
+                    const double f = wn - Wc[c];
+                    muscl_cell<FAST>(Wc[c], fp[c], f, P, qU[c], qD[c]);
+                    fp[c] = f;
+                    Wc[c] = wn;
+                }
 #pragma unroll
-        for (int c = 0; c < 4; ++c) {
-            QLp[c] = qU[c];
-            xg[c * NT + t] = GS[c];
-        }
-        if (!okE && is_out) {
-            int I = a.gi0 + v + 1;
-            if (I > a.NI - 1) I = a.NI - 1;
-            atomicMin(a.err, err_key(n, a.nstages, a.stage, 0, (long long)(a.gj0 + jc) * a.NI + I));
-        }
-        if (!okS && jflux) {
-            int J = a.gj0 + jc;
-            if (J > a.NJ - 1) J = a.NJ - 1;
-            atomicMin(a.err, err_key(n, a.nstages, a.stage, 0, (long long)J * a.NI + a.gi0 + v));
-        }
-        __syncthreads();  // B2: south fluxes visible
-        if (is_out) {
-            // ---- residual (Eq. 5) and stage update (Eq. 6) --------------------
-            const double iV = mv[6 * SMEM_ROW + own];
-            double R[4], U[4];
-#pragma unroll
-            for (int c = 0; c < 4; ++c) R[c] = ((GE[c] - GW[c]) + xg[c * NT + t + 1]) - GS[c];
-            if constexpr (TR::NPW > 0) mbar_wait(pbar, (unsigned)((v - i_start) & 1));
-#pragma unroll
-            for (int c = 0; c < 4; ++c) {
-                const double rv = R[c] * iV;
-                if constexpr (MODE == M_OWN) {
-                    U[c] = fma(-coef, rv, Wv[c]);
-                } else if constexpr (MODE == M_UN) {
-                    U[c] = fma(-coef, rv, pring[c * SMEM_ROW + own]);
-                } else if constexpr (MODE == M_RK4F) {
-                    const double un = pring[c * SMEM_ROW + own];
-                    const double d2 = pring[(4 + c) * SMEM_ROW + own] - un;
-                    const double d3 = pring[(8 + c) * SMEM_ROW + own] - un;
-                    const double d4 = Wv[c] - un;
-                    const double comb = (fma(2.0, d3, d2) + d4) * (1.0 / 3.0);
-                    U[c] = un + fma(-coef, rv, comb);
-                } else {  // M_HEUNF
-                    const double un = pring[c * SMEM_ROW + own];
-                    U[c] = un + fma(-coef, rv, 0.5 * (Wv[c] - un));
+                for (int c = 0; c < 4; ++c) {  // j: reconstruct cell (v, jc)
+                    const double wm = sv[c * WROW + own - 1];
+                    const double w = sv[c * WROW + own];
+                    const double wp = sv[c * WROW + own + 1];
+                    double qn;
+                    muscl_cell<FAST>(w, w - wm, wp - w, P, qn, qS[c]);
+                    qN[c] = __shfl_up_sync(0xffffffffu, qn, 1);  // north state of the cell below
+                    Wv[c] = w;
                 }
             }
-            store4(a.out, PJ, v, jc, U);
-            // new-state validity: rho > 0 and 2 rho E > |m|^2 (<=> p > 0)
-            if (!((U[0] > 0.0) & (2.0 * U[0] * U[3] > fma(U[1], U[1], U[2] * U[2]))))
-                atomicMin(a.err, err_key(n, a.nstages, a.stage, 1, (long long)(a.gj0 + jc) * a.NI + a.gi0 + v));
-            // physical-boundary ghosts of the new state (reading A-R11)
-            if (a.bc[2] == E_SLIP && jc <= 1) {
-                double g[4];
-                const int k0 = own - jc;  // column 0
-                mirror(U, mv[3 * SMEM_ROW + k0], mv[4 * SMEM_ROW + k0], g);
-                store4(a.out, PJ, v, -1 - jc, g);
-            } else if (a.bc[2] == E_OUTFLOW && jc == 0) {
-                store4(a.out, PJ, v, -1, U);
-                store4(a.out, PJ, v, -2, U);
+            __syncwarp();  // stencil row v-1, metric row v-1, pointwise slot consumed
+            {
+                const int lw = min(v + 3, r_last), lm = min(v + 1, m_last);
+                for (; next_w <= lw; ++next_w) issue_w(next_w);
+                for (; next_m <= lm; ++next_m) issue_m(next_m);
+                issue_p(v);
             }
-            if (a.bc[3] == E_SLIP && jc >= a.nj - 2) {
-                double g[4];
-                const int kN = own + (a.nj - jc);  // column nj
-                mirror(U, mv[3 * SMEM_ROW + kN], mv[4 * SMEM_ROW + kN], g);
-                store4(a.out, PJ, v, a.nj + (a.nj - 1 - jc), g);
-            } else if (a.bc[3] == E_OUTFLOW && jc == a.nj - 1) {
-                store4(a.out, PJ, v, a.nj, U);
-                store4(a.out, PJ, v, a.nj + 1, U);
+            wait_m(v);
+            const double *mv = mslot(v);
+            double GE[4], GS[4];
+            // both face fluxes of this row: two independent Roe evaluations
+            const bool okE = roe_flux(QLp, qD, mv[0 * WROW + own], mv[1 * WROW + own], mv[2 * WROW + own], P, GE);
+            const bool okS = roe_flux(qN, qS, mv[3 * WROW + own], mv[4 * WROW + own], mv[5 * WROW + own], P, GS);
+            double GN[4];
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+                QLp[c] = qU[c];
+                GN[c] = __shfl_down_sync(0xffffffffu, GS[c], 1);
             }
-            if (a.bc[0] == E_SLIP && v <= 1) {
-                double g[4];
-                mirror(U, nWx, nWy, g);
-                store4(a.out, PJ, -1 - v, jc, g);
-            } else if (a.bc[0] == E_OUTFLOW && v == 0) {
-                store4(a.out, PJ, -1, jc, U);
-                store4(a.out, PJ, -2, jc, U);
+            if (!okE && is_out) {
+                int I = a.gi0 + v + 1;
+                if (I > a.NI - 1) I = a.NI - 1;
+                atomicMin(a.err, err_key(n, a.nstages, a.stage, 0, (long long)(a.gj0 + jc) * a.NI + I));
             }
-            if (a.bc[1] == E_SLIP && v >= a.ni - 2) {
-                double g[4];
-                wait_m(a.ni - 1);  // i-face(ni) lives in metric row ni-1 (issued: <= v+1)
-                const double *mE = mslot(a.ni - 1);
-                mirror(U, mE[0 * SMEM_ROW + own], mE[1 * SMEM_ROW + own], g);
-                store4(a.out, PJ, a.ni + (a.ni - 1 - v), jc, g);
-            } else if (a.bc[1] == E_OUTFLOW && v == a.ni - 1) {
-                store4(a.out, PJ, a.ni, jc, U);
-                store4(a.out, PJ, a.ni + 1, jc, U);
+            if (!okS && jflux) {
+                int J = a.gj0 + jc;
+                if (J > a.NJ - 1) J = a.NJ - 1;
+                atomicMin(a.err, err_key(n, a.nstages, a.stage, 0, (long long)J * a.NI + a.gi0 + v));
             }
-            if constexpr (NORMS) {
+            if constexpr (TR::NPW > 0) mbar_wait(pbar, (unsigned)((v - i_start) & 1));
+            if (is_out) {
+                // ---- residual (Eq. 5) and stage update (Eq. 6) ----------------
+                const double iV = mv[6 * WROW + own];
+                double R[4], U[4];
+#pragma unroll
+                for (int c = 0; c < 4; ++c) R[c] = ((GE[c] - GW[c]) + GN[c]) - GS[c];
 #pragma unroll
                 for (int c = 0; c < 4; ++c) {
-                    nrm[c] = fma(R[c], R[c], nrm[c]);
-                    nrm[4 + c] = fmax(nrm[4 + c], fabs(R[c]));
+                    const double rv = R[c] * iV;
+                    if constexpr (MODE == M_OWN) {
+                        U[c] = fma(-coef, rv, Wv[c]);
+                    } else if constexpr (MODE == M_UN) {
+                        U[c] = fma(-coef, rv, pring[c * WROW + own]);
+                    } else if constexpr (MODE == M_RK4F) {
+                        const double un = pring[c * WROW + own];
+                        const double d2 = pring[(4 + c) * WROW + own] - un;
+                        const double d3 = pring[(8 + c) * WROW + own] - un;
+                        const double d4 = Wv[c] - un;
+                        const double comb = (fma(2.0, d3, d2) + d4) * (1.0 / 3.0);
+                        U[c] = un + fma(-coef, rv, comb);
+                    } else {  // M_HEUNF
+                        const double un = pring[c * WROW + own];
+                        U[c] = un + fma(-coef, rv, 0.5 * (Wv[c] - un));
+                    }
+                }
+                store4(a.out, PJ, v, jc, U);
+                // new-state validity: rho > 0 and 2 rho E > |m|^2 (<=> p > 0)
+                if (!((U[0] > 0.0) & (2.0 * U[0] * U[3] > fma(U[1], U[1], U[2] * U[2]))))
+                    atomicMin(a.err, err_key(n, a.nstages, a.stage, 1, (long long)(a.gj0 + jc) * a.NI + a.gi0 + v));
+                // physical-boundary ghosts of the new state (reading A-R11)
+                if (a.bc[2] == E_SLIP && jc <= 1) {
+                    double g[4];
+                    const int k0 = own - jc;  // column 0
+                    mirror(U, mv[3 * WROW + k0], mv[4 * WROW + k0], g);
+                    store4(a.out, PJ, v, -1 - jc, g);
+                } else if (a.bc[2] == E_OUTFLOW && jc == 0) {
+                    store4(a.out, PJ, v, -1, U);
+                    store4(a.out, PJ, v, -2, U);
+                }
+                if (a.bc[3] == E_SLIP && jc >= a.nj - 2) {
+                    double g[4];
+                    const int kN = own + (a.nj - jc);  // column nj
+                    mirror(U, mv[3 * WROW + kN], mv[4 * WROW + kN], g);
+                    store4(a.out, PJ, v, a.nj + (a.nj - 1 - jc), g);
+                } else if (a.bc[3] == E_OUTFLOW && jc == a.nj - 1) {
+                    store4(a.out, PJ, v, a.nj, U);
+                    store4(a.out, PJ, v, a.nj + 1, U);
+                }
+                if (a.bc[0] == E_SLIP && v <= 1) {  // segments start at 0 or >= 4 (choose_launch)
+                    double g[4];
+                    mirror(U, nWx, nWy, g);
+                    store4(a.out, PJ, -1 - v, jc, g);
+                } else if (a.bc[0] == E_OUTFLOW && v == 0) {
+                    store4(a.out, PJ, -1, jc, U);
+                    store4(a.out, PJ, -2, jc, U);
+                }
+                if (a.bc[1] == E_SLIP && v >= a.ni - 2) {
+                    double g[4];
+                    wait_m(a.ni - 1);  // i-face(ni) lives in metric row ni-1 (issued: <= v+1)
+                    const double *mE = mslot(a.ni - 1);
+                    mirror(U, mE[0 * WROW + own], mE[1 * WROW + own], g);
+                    store4(a.out, PJ, a.ni + (a.ni - 1 - v), jc, g);
+                } else if (a.bc[1] == E_OUTFLOW && v == a.ni - 1) {
+                    store4(a.out, PJ, a.ni, jc, U);
+                    store4(a.out, PJ, a.ni + 1, jc, U);
+                }
+                if constexpr (NORMS) {
+#pragma unroll
+                    for (int c = 0; c < 4; ++c) {
+                        nrm[c] = fma(R[c], R[c], nrm[c]);
+                        nrm[4 + c] = fmax(nrm[4 + c], fabs(R[c]));
+                    }
+                }
+                if constexpr (DTMAX) {
+                    // sigma/V of the new state for dt_{n+1} (reading A-R6)
+                    const double ir = frcp(U[0]);
+                    const double u = U[1] * ir, vv = U[2] * ir;
+                    const double p = P.gm1 * fma(-0.5, fma(U[1], u, U[2] * vv), U[3]);
+                    const double x = P.gamma * p * ir;
+                    const double snd = x * frsqrt(x);
+                    const double tW = (fabs(fma(u, wfx, vv * wfy)) + snd) * wfA;
+                    const double tE =
+                        (fabs(fma(u, mv[0 * WROW + own], vv * mv[1 * WROW + own])) + snd) * mv[2 * WROW + own];
+                    const double tS =
+                        (fabs(fma(u, mv[3 * WROW + own], vv * mv[4 * WROW + own])) + snd) * mv[5 * WROW + own];
+                    const double tN = (fabs(fma(u, mv[3 * WROW + own + 1], vv * mv[4 * WROW + own + 1])) + snd) *
+                                      mv[5 * WROW + own + 1];
+                    smax = fmax(smax, (((tW + tE) + tS) + tN) * iV);
                 }
             }
             if constexpr (DTMAX) {
-                // sigma/V of the new state for dt_{n+1} (reading A-R6)
-                const double ir = frcp(U[0]);
-                const double u = U[1] * ir, vv = U[2] * ir;
-                const double p = P.gm1 * fma(-0.5, fma(U[1], u, U[2] * vv), U[3]);
-                const double x = P.gamma * p * ir;
-                const double snd = x * frsqrt(x);
-                const double tW = (fabs(fma(u, wfx, vv * wfy)) + snd) * wfA;
-                const double tE = (fabs(fma(u, mv[0 * SMEM_ROW + own], vv * mv[1 * SMEM_ROW + own])) + snd) *
-                                  mv[2 * SMEM_ROW + own];
-                const double tS = (fabs(fma(u, mv[3 * SMEM_ROW + own], vv * mv[4 * SMEM_ROW + own])) + snd) *
-                                  mv[5 * SMEM_ROW + own];
-                const double tN = (fabs(fma(u, mv[3 * SMEM_ROW + own + 1], vv * mv[4 * SMEM_ROW + own + 1])) + snd) *
-                                  mv[5 * SMEM_ROW + own + 1];
-                smax = fmax(smax, (((tW + tE) + tS) + tN) * iV);
+                wfx = mv[0 * WROW + own];
+                wfy = mv[1 * WROW + own];
+                wfA = mv[2 * WROW + own];
             }
-        }
-        if constexpr (DTMAX) {
-            wfx = mv[0 * SMEM_ROW + own];
-            wfy = mv[1 * SMEM_ROW + own];
-            wfA = mv[2 * SMEM_ROW + own];
-        }
 #pragma unroll
-        for (int c = 0; c < 4; ++c) GW[c] = GE[c];
+            for (int c = 0; c < 4; ++c) GW[c] = GE[c];
+        }
     }
 
     // ---- CTA reductions --------------------------------------------------
-    const int warp = t >> 5, lane = t & 31;
     const unsigned ncta = gridDim.x;
     if (DTMAX) {
         for (int o = 16; o > 0; o >>= 1) smax = fmax(smax, __shfl_xor_sync(0xffffffffu, smax, o));
@@ -519,7 +525,7 @@ __global__ void __launch_bounds__(NT, SFV_MINB) stage_kernel(const StageArgs a) 
         __syncthreads();
         if (t == 0) {
             double m = red[0];
-            for (int w = 1; w < NT / 32; ++w) m = fmax(m, red[w]);
+            for (int w = 1; w < WPC; ++w) m = fmax(m, red[w]);
             atomicMax(reinterpret_cast<unsigned long long *>(&a.sig[(n + 1) & 1]),
                       (unsigned long long)__double_as_longlong(m));
         }
@@ -533,12 +539,12 @@ __global__ void __launch_bounds__(NT, SFV_MINB) stage_kernel(const StageArgs a) 
                 double y = __shfl_xor_sync(0xffffffffu, x, o);
                 x = q < 4 ? x + y : fmax(x, y);
             }
-            if (lane == 0) red[q * (NT / 32) + warp] = x;
+            if (lane == 0) red[q * WPC + warp] = x;
         }
         __syncthreads();
         if (t < 8) {
-            double x = red[t * (NT / 32)];
-            for (int w = 1; w < NT / 32; ++w) x = t < 4 ? x + red[t * (NT / 32) + w] : fmax(x, red[t * (NT / 32) + w]);
+            double x = red[t * WPC];
+            for (int w = 1; w < WPC; ++w) x = t < 4 ? x + red[t * WPC + w] : fmax(x, red[t * WPC + w]);
             a.partials[(size_t)blockIdx.x * 8 + t] = x;
         }
     }
@@ -561,8 +567,7 @@ __global__ void __launch_bounds__(NT, SFV_MINB) stage_kernel(const StageArgs a) 
                         acc[q] = q < 4 ? acc[q] + x : fmax(acc[q], x);
                     }
                 }
-                double *tree = xq;  // reuse: [8][NT]
-                __syncthreads();
+                double *tree = smem;  // rings are dead: [8][NT]
 #pragma unroll
                 for (int q = 0; q < 8; ++q) tree[q * NT + t] = acc[q];
                 __syncthreads();
@@ -589,48 +594,58 @@ __global__ void __launch_bounds__(NT, SFV_MINB) stage_kernel(const StageArgs a) 
     }
 }
 
-template <int MODE, bool NORMS, bool DTMAX>
+template <int MODE, bool NORMS, bool DTMAX, bool FAST>
 static cudaError_t launch_t(const StageArgs &a, cudaStream_t st) {
-    auto k = stage_kernel<MODE, NORMS, DTMAX>;
+    auto k = stage_kernel<MODE, NORMS, DTMAX, FAST>;
     const size_t sm = stage_smem<MODE>();  // attribute set by prepare_stage_kernels()
-    k<<<a.nstrips * a.nseg, NT, sm, st>>>(a);
+    k<<<(a.nstrips * a.nseg + WPC - 1) / WPC, NT, sm, st>>>(a);
     return cudaGetLastError();
 }
 
-template <int MODE, bool NORMS, bool DTMAX>
+template <int MODE, bool NORMS, bool DTMAX, bool FAST>
 static cudaError_t occ_t(int *n) {
-    auto k = stage_kernel<MODE, NORMS, DTMAX>;
+    auto k = stage_kernel<MODE, NORMS, DTMAX, FAST>;
     const size_t sm = stage_smem<MODE>();
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     if (e != cudaSuccess) return e;
     return cudaOccupancyMaxActiveBlocksPerMultiprocessor(n, k, NT, sm);
 }
 
-#define SFV_DISPATCH(FN, ...)                                                         \
+#define SFV_DISPATCH_F(FN, F, ...)                                                    \
     switch (mode * 4 + (norms ? 2 : 0) + (dtmax ? 1 : 0)) {                          \
-        case M_OWN * 4 + 2: return FN<M_OWN, true, false>(__VA_ARGS__);              \
-        case M_OWN * 4 + 0: return FN<M_OWN, false, false>(__VA_ARGS__);             \
-        case M_UN * 4 + 0: return FN<M_UN, false, false>(__VA_ARGS__);               \
-        case M_UN * 4 + 1: return FN<M_UN, false, true>(__VA_ARGS__);                \
-        case M_RK4F * 4 + 1: return FN<M_RK4F, false, true>(__VA_ARGS__);            \
-        case M_RK4F * 4 + 0: return FN<M_RK4F, false, false>(__VA_ARGS__);           \
-        case M_HEUNF * 4 + 1: return FN<M_HEUNF, false, true>(__VA_ARGS__);          \
-        case M_HEUNF * 4 + 0: return FN<M_HEUNF, false, false>(__VA_ARGS__);         \
+        case M_OWN * 4 + 2: return FN<M_OWN, true, false, F>(__VA_ARGS__);           \
+        case M_OWN * 4 + 0: return FN<M_OWN, false, false, F>(__VA_ARGS__);          \
+        case M_UN * 4 + 0: return FN<M_UN, false, false, F>(__VA_ARGS__);            \
+        case M_UN * 4 + 1: return FN<M_UN, false, true, F>(__VA_ARGS__);             \
+        case M_RK4F * 4 + 1: return FN<M_RK4F, false, true, F>(__VA_ARGS__);         \
+        case M_RK4F * 4 + 0: return FN<M_RK4F, false, false, F>(__VA_ARGS__);        \
+        case M_HEUNF * 4 + 1: return FN<M_HEUNF, false, true, F>(__VA_ARGS__);       \
+        case M_HEUNF * 4 + 0: return FN<M_HEUNF, false, false, F>(__VA_ARGS__);      \
         default: return cudaErrorInvalidValue;                                       \
     }
+#define SFV_DISPATCH(FN, ...)                                                         \
+    if (fast) {                                                                       \
+        SFV_DISPATCH_F(FN, true, __VA_ARGS__)                                         \
+    } else {                                                                          \
+        SFV_DISPATCH_F(FN, false, __VA_ARGS__)                                        \
+    }
 
+// fast = bounded van Albada with kappa = -1 (the default scheme, reading A-R3/A-R7)
+bool fast_path(const Params &P) { return P.limiter == 1 && P.c2 == 0.0; }
 cudaError_t launch_stage(const StageArgs &a, int mode, bool norms, bool dtmax, cudaStream_t st) {
+    const bool fast = fast_path(a.P);
     SFV_DISPATCH(launch_t, a, st)
 }
-cudaError_t stage_occupancy(int mode, bool norms, bool dtmax, int *n) { SFV_DISPATCH(occ_t, n) }
+cudaError_t stage_occupancy(int mode, bool norms, bool dtmax, bool fast, int *n) { SFV_DISPATCH(occ_t, n) }
 cudaError_t prepare_stage_kernels() {
     const int variants[8][3] = {{M_OWN, 1, 0}, {M_OWN, 0, 0}, {M_UN, 0, 0}, {M_UN, 0, 1},
                                 {M_RK4F, 0, 1}, {M_RK4F, 0, 0}, {M_HEUNF, 0, 1}, {M_HEUNF, 0, 0}};
-    for (auto &v : variants) {
-        int n = 0;
-        cudaError_t e = stage_occupancy(v[0], v[1] != 0, v[2] != 0, &n);
-        if (e != cudaSuccess) return e;
-    }
+    for (auto &v : variants)
+        for (int f = 0; f < 2; ++f) {
+            int n = 0;
+            cudaError_t e = stage_occupancy(v[0], v[1] != 0, v[2] != 0, f != 0, &n);
+            if (e != cudaSuccess) return e;
+        }
     return cudaSuccess;
 }
 size_t stage_smem_bytes(int mode) {
@@ -856,6 +871,29 @@ cudaError_t launch_pack_cols(const double *buf, double *dst, int ni, int PJ, int
 cudaError_t launch_unpack_cols(const double *src, double *buf, int ni, int PJ, int j_first, cudaStream_t st) {
     unpack_cols_kernel<<<(ni * 4 + 255) / 256, 256, 0, st>>>(src, buf, ni, PJ, j_first);
     return cudaGetLastError();
+}
+
+typedef CUresult (*EncodeTiledFn)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *, const cuuint64_t *,
+                                  const cuuint64_t *, const cuuint32_t *, const cuuint32_t *, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+cudaError_t make_row_tensor_map(CUtensorMap *m, const double *base, unsigned long long rows, int PJ, int box_rows) {
+    static EncodeTiledFn fn = nullptr;
+    if (!fn) {
+        cudaDriverEntryPointQueryResult q;
+        void *p = nullptr;
+        cudaError_t e = cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q);
+        if (e != cudaSuccess || q != cudaDriverEntryPointSuccess || !p) return cudaErrorNotSupported;
+        fn = reinterpret_cast<EncodeTiledFn>(p);
+    }
+    const cuuint64_t dims[2] = {(cuuint64_t)PJ, (cuuint64_t)rows};
+    const cuuint64_t strides[1] = {(cuuint64_t)PJ * sizeof(double)};
+    const cuuint32_t box[2] = {(cuuint32_t)WROW, (cuuint32_t)box_rows};
+    const cuuint32_t estr[2] = {1, 1};
+    CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double *>(base), dims, strides, box, estr,
+                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
 }
 
 __global__ void debug_math_kernel(int which, const double *in, double *out, long long n) {
