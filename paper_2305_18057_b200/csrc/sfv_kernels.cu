@@ -234,8 +234,12 @@ __host__ __device__ constexpr size_t stage_smem() {
 }
 
 #ifndef SFV_MINB
-#define SFV_MINB 4  // resident CTAs per SM the register allocation targets
+#define SFV_MINB 3  // resident CTAs per SM the register allocation targets (168 regs: no spills)
 #endif
+#ifndef SFV_UNROLL
+#define SFV_UNROLL 1  // row-loop unroll: lets ptxas rename the carried window instead of moving it
+#endif
+constexpr int kRowUnroll = SFV_UNROLL;
 
 template <int MODE, bool NORMS, bool DTMAX, bool FAST>
 __global__ void __launch_bounds__(NT, SFV_MINB) stage_kernel(const __grid_constant__ StageArgs a) {
@@ -362,6 +366,7 @@ __global__ void __launch_bounds__(NT, SFV_MINB) stage_kernel(const __grid_consta
         }
 
         // ---- main loop: one output row per iteration ---------------------------
+#pragma unroll kRowUnroll
         for (int v = i_start; v < i_end; ++v) {
             wait_w(v + 2);
             double qD[4], qU[4], qS[4], qN[4], Wv[4];
