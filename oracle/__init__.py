@@ -71,6 +71,7 @@ def lib():
         L.orc_muscl.restype = None
         L.orc_roe_flux.argtypes = [_D, _D, C.c_double, C.c_double, C.c_double, C.c_double, _D]
         L.orc_split.argtypes = [C.c_int32, C.c_int32, _I32, _I32]
+        L.orc_stable_dt.argtypes = [C.c_int32, C.c_int32, _D, _D, _D, C.c_double, C.c_double, _D]
         L.orc_create.argtypes = [C.POINTER(orc_config), _D, _D, C.POINTER(C.c_void_p)]
         L.orc_partition.argtypes = [C.c_void_p, C.c_int32, C.c_int32, _I32, _I32]
         L.orc_partition_map.argtypes = [C.c_void_p, C.c_int32, _I32]
@@ -150,6 +151,17 @@ def split(n, parts, weights=None):
     if st:
         raise OracleError(st, "bad split")
     return starts
+
+
+def stable_dt(X, Y, U, gamma=1.4, cfl=0.8):
+    """CFL dt of a whole grid (same arithmetic as the solver's dt), banded."""
+    X = _f64(X); Y = _f64(Y); U = _f64(U)
+    nj, ni = X.shape[0] - 1, X.shape[1] - 1
+    out = C.c_double()
+    st = lib().orc_stable_dt(ni, nj, _dp(X), _dp(Y), _dp(U), gamma, cfl, C.byref(out))
+    if st:
+        raise OracleError(st, "stable_dt")
+    return out.value
 
 
 # ------------------------------------------------------------------- solver

@@ -557,7 +557,24 @@ static int check_states(orc_ctx *c, int use_W, int64_t *bad)
 
 /* CFL time step from U^n interior cells (reading A-R6):
  * dt = CFL * min_c V_c / sigma_c, sigma = ((t_W + t_E) + t_S) + t_N,
- * t_f = (|u nx + v ny| + a) A_f. */
+ * t_f = (|u nx + v ny| + a) A_f.  cell_v_over_sigma returns V/sigma of one
+ * cell (faces W, E, S, N as {nx, ny, A}). */
+static int cell_v_over_sigma(const double *U, const double *fW, const double *fE, const double *fS,
+                             const double *fN, double V, double gamma, double *r)
+{
+    double prim[4];
+    if (orc_primitive(U, gamma, prim) != ORC_OK) return ORC_ERR_STATE;
+    double u = prim[1], v = prim[2];
+    double a = sqrt(gamma * prim[3] / prim[0]);
+    double tW = (fabs(u * fW[0] + v * fW[1]) + a) * fW[2];
+    double tE = (fabs(u * fE[0] + v * fE[1]) + a) * fE[2];
+    double tS = (fabs(u * fS[0] + v * fS[1]) + a) * fS[2];
+    double tN = (fabs(u * fN[0] + v * fN[1]) + a) * fN[2];
+    double sigma = ((tW + tE) + tS) + tN;
+    *r = V / sigma;
+    return ORC_OK;
+}
+
 static int compute_dt(orc_ctx *c, double *dt)
 {
     if (c->cfg.dt_fixed > 0.0) { *dt = c->cfg.dt_fixed; return ORC_OK; }
@@ -566,25 +583,49 @@ static int compute_dt(orc_ctx *c, double *dt)
         orc_block *bk = &c->b[n];
         for (int32_t j = 0; j < bk->nj; ++j)
             for (int32_t i = 0; i < bk->ni; ++i) {
-                double prim[4];
-                if (orc_primitive(bk->Un + IN(bk, i, j), c->cfg.gamma, prim) != ORC_OK) return ORC_ERR_STATE;
-                double u = prim[1], v = prim[2];
-                double a = sqrt(c->cfg.gamma * prim[3] / prim[0]);
-                const double *fW = bk->iface + ((int64_t)j * (bk->ni + 1) + i) * 3;
-                const double *fE = bk->iface + ((int64_t)j * (bk->ni + 1) + i + 1) * 3;
-                const double *fS = bk->jface + ((int64_t)j * bk->ni + i) * 3;
-                const double *fN = bk->jface + ((int64_t)(j + 1) * bk->ni + i) * 3;
-                double tW = (fabs(u * fW[0] + v * fW[1]) + a) * fW[2];
-                double tE = (fabs(u * fE[0] + v * fE[1]) + a) * fE[2];
-                double tS = (fabs(u * fS[0] + v * fS[1]) + a) * fS[2];
-                double tN = (fabs(u * fN[0] + v * fN[1]) + a) * fN[2];
-                double sigma = ((tW + tE) + tS) + tN;
-                double r = bk->vol[(int64_t)j * bk->ni + i] / sigma;
+                double r;
+                if (cell_v_over_sigma(bk->Un + IN(bk, i, j),
+                                      bk->iface + ((int64_t)j * (bk->ni + 1) + i) * 3,
+                                      bk->iface + ((int64_t)j * (bk->ni + 1) + i + 1) * 3,
+                                      bk->jface + ((int64_t)j * bk->ni + i) * 3,
+                                      bk->jface + ((int64_t)(j + 1) * bk->ni + i) * 3,
+                                      bk->vol[(int64_t)j * bk->ni + i], c->cfg.gamma, &r) != ORC_OK)
+                    return ORC_ERR_STATE;
                 if (r < mn) mn = r;
             }
     }
     *dt = c->cfg.cfl * mn;
     return ORC_OK;
+}
+
+/* The same dt for a whole grid without a solver context, processed in bands
+ * of rows so that very large grids (config C3) fit in memory. */
+int orc_stable_dt(int32_t ni, int32_t nj, const double *X, const double *Y, const double *U, double gamma,
+                  double cfl, double *dt)
+{
+    const int32_t band = 64;
+    double mn = INFINITY;
+    double *fi = (double *)malloc(sizeof(double) * 3 * (size_t)(ni + 1) * band);
+    double *fj = (double *)malloc(sizeof(double) * 3 * (size_t)ni * (band + 1));
+    double *vol = (double *)malloc(sizeof(double) * (size_t)ni * band);
+    int st = ORC_OK;
+    for (int32_t j0 = 0; j0 < nj && st == ORC_OK; j0 += band) {
+        int32_t nb = nj - j0 < band ? nj - j0 : band;
+        const double *Xb = X + (int64_t)j0 * (ni + 1), *Yb = Y + (int64_t)j0 * (ni + 1);
+        st = orc_metrics(ni, nb, Xb, Yb, fi, fj, vol, NULL);
+        for (int32_t j = 0; j < nb && st == ORC_OK; ++j)
+            for (int32_t i = 0; i < ni; ++i) {
+                double r;
+                st = cell_v_over_sigma(U + ((int64_t)(j0 + j) * ni + i) * 4, fi + ((int64_t)j * (ni + 1) + i) * 3,
+                                       fi + ((int64_t)j * (ni + 1) + i + 1) * 3, fj + ((int64_t)j * ni + i) * 3,
+                                       fj + ((int64_t)(j + 1) * ni + i) * 3, vol[(int64_t)j * ni + i], gamma, &r);
+                if (st != ORC_OK) break;
+                if (r < mn) mn = r;
+            }
+    }
+    free(fi); free(fj); free(vol);
+    *dt = cfl * mn;
+    return st;
 }
 
 int orc_set_state(orc_ctx *c, const double *U)

@@ -62,6 +62,8 @@ void orc_muscl(const double w[4], double eps, double kappa, int32_t kind,
 int orc_roe_flux(const double QL[4], const double QR[4], double nx, double ny,
                  double gamma, double harten_eps, double F[4]);
 int orc_split(int32_t n, int32_t parts, const int32_t *weights, int32_t *starts);
+int orc_stable_dt(int32_t ni, int32_t nj, const double *X, const double *Y, const double *U, double gamma,
+                  double cfl, double *dt);
 
 /* ---- whole-solver mirror of the sfv C ABI ---- */
 int orc_create(const orc_config *cfg, const double *X, const double *Y, orc_ctx **out);

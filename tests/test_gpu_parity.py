@@ -290,3 +290,41 @@ def test_c2_full_size_one_step(sfv_mod, oracle_mod):
     check(g, o, 1e-12)
     g.step(2); g.sync(); o.step(2)
     check(g, o, 1e-12)
+
+
+def test_c3_full_size_windows(sfv_mod, oracle_mod):
+    """BASELINE config C3 (11520x5760 = 66.4 M cells) on one GPU in the
+    launch configuration bench.py times: one RK4 step of a perturbed state.
+    The oracle cannot step the whole grid in a test, so it steps windows of
+    the same grid: one RK4 step has a domain of dependence of 4 stages x 2
+    cells, so cells >= 10 cells from an artificial window edge depend only on
+    data inside the window.  The window runs use the global dt_0 the oracle
+    computes itself over the full grid (orc_stable_dt), and the GPU's dt_0
+    must match it."""
+    ni, nj = I.CONFIGS["C3"]["ni"], I.CONFIGS["C3"]["nj"]
+    X, Y = I.config_nodes("C3")
+    cfg = I.default_config(ni, nj)
+    U0 = I.perturbed_state(ni, nj, 6)
+    g = sfv_mod.Solver(cfg, X, Y)
+    g.set_state(U0)
+    g.step(1)
+    g.sync()
+    Ug = g.get_state()
+    dt0 = oracle_mod.stable_dt(X, Y, U0, gamma=cfg["gamma"], cfl=cfg["cfl"])
+    assert dt_error(g.dt(), [dt0]) <= 1e-13
+    assert np.all(np.isfinite(g.residual_norms()))
+    M = 10
+    ni_in = int(round(ni / 3.0))
+    windows = [(0, 40, 0, 40), (ni_in - 24, ni_in + 24, 0, 40), (ni - 40, ni, nj - 40, nj),
+               (5000, 5040, 2000, 2040), (ni - 40, ni, 0, 40)]
+    for (i0, i1, j0, j1) in windows:
+        ilo, ihi, jlo, jhi = max(0, i0 - M), min(ni, i1 + M), max(0, j0 - M), min(nj, j1 + M)
+        bc = (cfg["bc"][0] if ilo == 0 else I.BC_OUTFLOW, cfg["bc"][1] if ihi == ni else I.BC_OUTFLOW,
+              cfg["bc"][2] if jlo == 0 else I.BC_OUTFLOW, cfg["bc"][3] if jhi == nj else I.BC_OUTFLOW)
+        sub = I.default_config(ihi - ilo, jhi - jlo, bc=bc, dt_fixed=dt0)
+        o = oracle_mod.Oracle(sub, X[jlo:jhi + 1, ilo:ihi + 1], Y[jlo:jhi + 1, ilo:ihi + 1])
+        o.set_state(U0[jlo:jhi, ilo:ihi])
+        o.step(1)
+        Uo = o.get_state()[j0 - jlo:j1 - jlo, i0 - ilo:i1 - ilo]
+        e = state_error(Ug[j0:j1, i0:i1], Uo)
+        assert np.all(e <= 1e-12), ((i0, i1, j0, j1), e)

@@ -460,3 +460,14 @@ def test_oblique_shock_wedge_C1(oracle_mod, golden):
     p21 = p.mean() / I.TABLE1_P
     want = golden["oblique_shock_M4"]["15"]["p21"]
     assert abs(p21 / want - 1) < 0.03, p21
+
+
+def test_stable_dt_matches_solver_dt(oracle_mod):
+    """orc_stable_dt (banded, no solver context; used by the C3 window
+    parity test) reproduces the solver's dt_0 bit for bit."""
+    for (ni, nj, th) in [(300, 200, 30.0), (64, 130, 15.0)]:
+        X, Y = I.ramp_nodes(ni, nj, th)
+        U = I.perturbed_state(ni, nj, 1)
+        o = oracle_mod.Oracle(I.default_config(ni, nj), X, Y)
+        o.set_state(U); o.step(1)
+        assert o.dt()[0] == oracle_mod.stable_dt(X, Y, U)
