@@ -9,6 +9,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -235,6 +236,11 @@ void choose_launch(sfv_ctx *c, Block &b) {
         }
     }
     b.nseg = std::min(best, b.ni);
+    // experiment override: SFV_WAVES = w forces about w waves of warp tasks
+    if (const char *ev = getenv("SFV_WAVES")) {
+        const double w = atof(ev);
+        if (w > 0) b.nseg = std::max(1, std::min(cap, (int)std::lround(w * slots / b.nstrips)));
+    }
 }
 
 sfv_status build_blocks(sfv_ctx *c) {

@@ -273,6 +273,9 @@ __global__ void __launch_bounds__(NT, SFV_MINB) stage_kernel(const __grid_consta
         const bool is_out = (lane >= 1) && (jc < j1);
         const bool jflux = (lane >= 1) && (jc <= j1);
         const int own = lane + 1;                    // column index in a staged row
+        auto writes_ghost = [&](int e) { return a.bc[e] == E_SLIP || a.bc[e] == E_OUTFLOW; };
+        const bool ghost_sn = (writes_ghost(2) && j0 == 0) || (writes_ghost(3) && j1 >= a.nj - 1);
+        const bool ghost_w = writes_ghost(0), ghost_e = writes_ghost(1);
         const int i_start = (int)(((long long)a.ni * seg) / a.nseg);
         const int i_end = (int)(((long long)a.ni * (seg + 1)) / a.nseg);
         const int r0 = i_start - 2, r_last = i_end + 1;  // stencil rows
@@ -411,47 +414,53 @@ __global__ void __launch_bounds__(NT, SFV_MINB) stage_kernel(const __grid_consta
                 QLp[c] = qU[c];
                 GN[c] = __shfl_down_sync(0xffffffffu, GS[c], 1);
             }
-            if (!okE && is_out) {
-                int I = a.gi0 + v + 1;
-                if (I > a.NI - 1) I = a.NI - 1;
-                atomicMin(a.err, err_key(n, a.nstages, a.stage, 0, (long long)(a.gj0 + jc) * a.NI + I));
-            }
-            if (!okS && jflux) {
-                int J = a.gj0 + jc;
-                if (J > a.NJ - 1) J = a.NJ - 1;
-                atomicMin(a.err, err_key(n, a.nstages, a.stage, 0, (long long)J * a.NI + a.gi0 + v));
-            }
             if constexpr (TR::NPW > 0) mbar_wait(pbar, (unsigned)((v - i_start) & 1));
-            if (is_out) {
-                // ---- residual (Eq. 5) and stage update (Eq. 6) ----------------
-                const double iV = mv[6 * WROW + own];
-                double R[4], U[4];
+            // ---- residual (Eq. 5) and stage update (Eq. 6): every lane computes,
+            // output lanes store (no divergence in the common path)
+            const double iV = mv[6 * WROW + own];
+            double R[4], U[4];
 #pragma unroll
-                for (int c = 0; c < 4; ++c) R[c] = ((GE[c] - GW[c]) + GN[c]) - GS[c];
+            for (int c = 0; c < 4; ++c) R[c] = ((GE[c] - GW[c]) + GN[c]) - GS[c];
 #pragma unroll
-                for (int c = 0; c < 4; ++c) {
-                    const double rv = R[c] * iV;
-                    if constexpr (MODE == M_OWN) {
-                        U[c] = fma(-coef, rv, Wv[c]);
-                    } else if constexpr (MODE == M_UN) {
-                        U[c] = fma(-coef, rv, pring[c * WROW + own]);
-                    } else if constexpr (MODE == M_RK4F) {
-                        const double un = pring[c * WROW + own];
-                        const double d2 = pring[(4 + c) * WROW + own] - un;
-                        const double d3 = pring[(8 + c) * WROW + own] - un;
-                        const double d4 = Wv[c] - un;
-                        const double comb = (fma(2.0, d3, d2) + d4) * (1.0 / 3.0);
-                        U[c] = un + fma(-coef, rv, comb);
-                    } else {  // M_HEUNF
-                        const double un = pring[c * WROW + own];
-                        U[c] = un + fma(-coef, rv, 0.5 * (Wv[c] - un));
-                    }
+            for (int c = 0; c < 4; ++c) {
+                const double rv = R[c] * iV;
+                if constexpr (MODE == M_OWN) {
+                    U[c] = fma(-coef, rv, Wv[c]);
+                } else if constexpr (MODE == M_UN) {
+                    U[c] = fma(-coef, rv, pring[c * WROW + own]);
+                } else if constexpr (MODE == M_RK4F) {
+                    const double un = pring[c * WROW + own];
+                    const double d2 = pring[(4 + c) * WROW + own] - un;
+                    const double d3 = pring[(8 + c) * WROW + own] - un;
+                    const double d4 = Wv[c] - un;
+                    const double comb = (fma(2.0, d3, d2) + d4) * (1.0 / 3.0);
+                    U[c] = un + fma(-coef, rv, comb);
+                } else {  // M_HEUNF
+                    const double un = pring[c * WROW + own];
+                    U[c] = un + fma(-coef, rv, 0.5 * (Wv[c] - un));
                 }
-                store4(a.out, PJ, v, jc, U);
-                // new-state validity: rho > 0 and 2 rho E > |m|^2 (<=> p > 0)
-                if (!((U[0] > 0.0) & (2.0 * U[0] * U[3] > fma(U[1], U[1], U[2] * U[2]))))
+            }
+            if (is_out) store4(a.out, PJ, v, jc, U);
+            // new-state validity: rho > 0 and 2 rho E > |m|^2 (<=> p > 0)
+            const bool st_ok = (U[0] > 0.0) & (2.0 * U[0] * U[3] > fma(U[1], U[1], U[2] * U[2]));
+            // rare path behind one warp vote: invalid face or new states (reading A-R28)
+            if (__any_sync(0xffffffffu, (is_out & (!okE | !st_ok)) | (jflux & !okS))) {
+                if (is_out && !okE) {
+                    int I = a.gi0 + v + 1;
+                    if (I > a.NI - 1) I = a.NI - 1;
+                    atomicMin(a.err, err_key(n, a.nstages, a.stage, 0, (long long)(a.gj0 + jc) * a.NI + I));
+                }
+                if (jflux && !okS) {
+                    int J = a.gj0 + jc;
+                    if (J > a.NJ - 1) J = a.NJ - 1;
+                    atomicMin(a.err, err_key(n, a.nstages, a.stage, 0, (long long)J * a.NI + a.gi0 + v));
+                }
+                if (is_out && !st_ok)
                     atomicMin(a.err, err_key(n, a.nstages, a.stage, 1, (long long)(a.gj0 + jc) * a.NI + a.gi0 + v));
-                // physical-boundary ghosts of the new state (reading A-R11)
+            }
+            // physical-boundary ghosts of the new state (reading A-R11), behind one
+            // warp-uniform test: only strips at the S / N walls and rows 0, 1, ni-2, ni-1
+            if ((ghost_sn || (ghost_w && v <= 1) || (ghost_e && v >= a.ni - 2)) && is_out) {
                 if (a.bc[2] == E_SLIP && jc <= 1) {
                     double g[4];
                     const int k0 = own - jc;  // column 0
@@ -488,29 +497,30 @@ __global__ void __launch_bounds__(NT, SFV_MINB) stage_kernel(const __grid_consta
                     store4(a.out, PJ, a.ni, jc, U);
                     store4(a.out, PJ, a.ni + 1, jc, U);
                 }
-                if constexpr (NORMS) {
+            }
+            if constexpr (NORMS) {
 #pragma unroll
-                    for (int c = 0; c < 4; ++c) {
-                        nrm[c] = fma(R[c], R[c], nrm[c]);
-                        nrm[4 + c] = fmax(nrm[4 + c], fabs(R[c]));
-                    }
+                for (int c = 0; c < 4; ++c) {
+                    nrm[c] = is_out ? fma(R[c], R[c], nrm[c]) : nrm[c];
+                    nrm[4 + c] = is_out ? fmax(nrm[4 + c], fabs(R[c])) : nrm[4 + c];
                 }
-                if constexpr (DTMAX) {
-                    // sigma/V of the new state for dt_{n+1} (reading A-R6)
-                    const double ir = frcp(U[0]);
-                    const double u = U[1] * ir, vv = U[2] * ir;
-                    const double p = P.gm1 * fma(-0.5, fma(U[1], u, U[2] * vv), U[3]);
-                    const double x = P.gamma * p * ir;
-                    const double snd = x * frsqrt(x);
-                    const double tW = (fabs(fma(u, wfx, vv * wfy)) + snd) * wfA;
-                    const double tE =
-                        (fabs(fma(u, mv[0 * WROW + own], vv * mv[1 * WROW + own])) + snd) * mv[2 * WROW + own];
-                    const double tS =
-                        (fabs(fma(u, mv[3 * WROW + own], vv * mv[4 * WROW + own])) + snd) * mv[5 * WROW + own];
-                    const double tN = (fabs(fma(u, mv[3 * WROW + own + 1], vv * mv[4 * WROW + own + 1])) + snd) *
-                                      mv[5 * WROW + own + 1];
-                    smax = fmax(smax, (((tW + tE) + tS) + tN) * iV);
-                }
+            }
+            if constexpr (DTMAX) {
+                // sigma/V of the new state for dt_{n+1} (reading A-R6)
+                const double ir = frcp(U[0]);
+                const double u = U[1] * ir, vv = U[2] * ir;
+                const double p = P.gm1 * fma(-0.5, fma(U[1], u, U[2] * vv), U[3]);
+                const double x = P.gamma * p * ir;
+                const double snd = x * frsqrt(x);
+                const double tW = (fabs(fma(u, wfx, vv * wfy)) + snd) * wfA;
+                const double tE =
+                    (fabs(fma(u, mv[0 * WROW + own], vv * mv[1 * WROW + own])) + snd) * mv[2 * WROW + own];
+                const double tS =
+                    (fabs(fma(u, mv[3 * WROW + own], vv * mv[4 * WROW + own])) + snd) * mv[5 * WROW + own];
+                const double tN = (fabs(fma(u, mv[3 * WROW + own + 1], vv * mv[4 * WROW + own + 1])) + snd) *
+                                  mv[5 * WROW + own + 1];
+                const double sv = (((tW + tE) + tS) + tN) * iV;
+                smax = (is_out && sv > smax) ? sv : smax;
             }
             if constexpr (DTMAX) {
                 wfx = mv[0 * WROW + own];
