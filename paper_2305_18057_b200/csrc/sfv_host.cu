@@ -71,7 +71,6 @@ struct Block {
     int nstrips = 1, nseg = 1;
     double *buf[4] = {nullptr, nullptr, nullptr, nullptr};
     double *met = nullptr, *nodes = nullptr, *stage = nullptr, *partials = nullptr;
-    unsigned *ticket = nullptr;
     double *xs[2] = {nullptr, nullptr}, *xr[2] = {nullptr, nullptr};  // j-cut pack buffers (S, N)
     CUtensorMap tm_buf[4], tm_met;  // 2D TMA descriptors (made at sfv_bind)
     size_t buf_elems() const { return (size_t)(ni + 4) * 4 * PJ + PADD; }
@@ -208,8 +207,8 @@ void build_params(sfv_ctx *c) {
     P.c1 = f.muscl_eps * (1.0 - f.muscl_kappa) / 4.0;
     P.c2 = f.muscl_eps * (1.0 + f.muscl_kappa) / 4.0;
     P.delta = f.lim_delta;
-    P.c1x2 = 2.0 * P.c1;
-    P.c1d = P.c1 * f.lim_delta;
+    P.c1h = P.c1;
+    P.c1dh = 0.5 * P.c1 * f.lim_delta;
     P.heps = f.harten_eps;
     P.hinv = f.harten_eps > 0.0 ? 0.5 / f.harten_eps : 0.0;
     P.cfl = f.cfl;
@@ -314,7 +313,6 @@ size_t layout(sfv_ctx *c, bool assign) {
             b.nodes = reinterpret_cast<double *>(c->ws + on);
             b.stage = reinterpret_cast<double *>(c->ws + os);
             b.partials = reinterpret_cast<double *>(c->ws + op);
-            b.ticket = reinterpret_cast<unsigned *>(c->ws + ot);
             b.xs[0] = reinterpret_cast<double *>(c->ws + ox[0]);
             b.xs[1] = reinterpret_cast<double *>(c->ws + ox[1]);
             b.xr[0] = reinterpret_cast<double *>(c->ws + ox[2]);
@@ -438,12 +436,9 @@ StageArgs make_args(sfv_ctx *c, Block &b, int k) {
     a.block_id = b.id;
     a.nblocks = c->nblocks_total;
     a.partials = b.partials;
-    a.ticket = b.ticket;
     a.err = c->err;
     a.stage = k;
     a.nstages = nstages_of(c->cfg.rk);
-    a.lead = (&b == &c->blocks.front()) ? 1 : 0;
-    a.bump = (k == a.nstages && &b == &c->blocks.back()) ? 1 : 0;
     a.P = c->P;
     return a;
 }
@@ -456,6 +451,25 @@ sfv_status enqueue_step(sfv_ctx *c, cudaStream_t st) {
         for (Block &b : c->blocks) {
             StageArgs a = make_args(c, b, k);
             CK(launch_stage(a, sp.mode, k == 1, k == s && cflmode, st));
+        }
+        if (k == 1) {  // norms of R(U^n), dt record, step counter (after every block's stage 1)
+            for (Block &b : c->blocks) {
+                FinalizeArgs f{};
+                f.partials = b.partials;
+                f.ncta = (b.nstrips * b.nseg + WPC - 1) / WPC;
+                f.norm_hist = c->norm_hist;
+                f.dt_hist = c->dt_hist;
+                f.sig = c->sig;
+                f.step_ctr = c->step_ctr;
+                f.cap = (int)c->cfg.max_history;
+                f.block_id = b.id;
+                f.nblocks = c->nblocks_total;
+                f.lead = (&b == &c->blocks.front()) ? 1 : 0;
+                f.bump = (&b == &c->blocks.back()) ? 1 : 0;
+                f.cfl = c->cfg.cfl;
+                f.dt_fixed = c->cfg.dt_fixed;
+                CK(launch_finalize(f, st));
+            }
         }
         sfv_status r = exchange(c, sp.out, st);
         if (r != SFV_OK) return r;
@@ -674,7 +688,6 @@ sfv_status sfv_set_state(sfv_ctx *c, const double *U) {
             CK(launch_bc_fill(b.buf[k], b.met, b.ni, b.nj, b.PJ, bcfill, c->cfg.inflow_U, st));
         }
         CK(launch_check_state(b.buf[0], b.ni, b.nj, b.PJ, b.i0, b.j0, NI, c->err, st));
-        CK(cudaMemsetAsync(b.ticket, 0, 256, st));
     }
     sfv_status r = exchange(c, 0, st);
     if (r != SFV_OK) return r;

@@ -21,7 +21,7 @@ constexpr int JOFF = 4;
 constexpr int NMET = 7;
 constexpr int SMEM_ROW = 132;     // doubles per staged row in shared memory
 constexpr int ROW_COLS = 130;     // columns staged per row: j0-2 .. j0+127
-constexpr int NT = 128;           // threads per CTA of the stage kernel
+constexpr int NT = 32;            // threads per CTA of the stage kernel: one independent warp
 constexpr int WPC = NT / 32;      // independent warps per CTA
 constexpr int WOUT = 30;          // output columns per warp strip (+1 halo lane each side)
 
@@ -32,7 +32,7 @@ enum Edge { E_INFLOW = 0, E_OUTFLOW = 1, E_SLIP = 2, E_CONNECTED = 3 };
 struct Params {
     double gamma, gm1;
     double c1, c2;          // eps(1-kappa)/4, eps(1+kappa)/4 (Eq. 7)
-    double c1x2, c1d;       // 2 c1, c1 delta (fast path: bounded van Albada, kappa = -1)
+    double c1h, c1dh;       // c1, c1 delta / 2 (fast path: bounded van Albada, kappa = -1)
     double delta;           // limiter guard
     double heps, hinv;      // Harten eps and 0.5/eps
     double cfl, dt_fixed;
@@ -57,12 +57,19 @@ struct StageArgs {
     double *dt_hist;        // [cap]
     double *norm_hist;      // [cap][nblocks][8]
     int cap, block_id, nblocks;
-    double *partials;       // [ncta][8]
-    unsigned int *ticket;
+    double *partials;       // [8][ncta] norm partials (stage 1)
     unsigned long long *err;
     int stage, nstages;
-    int lead, bump;
     Params P;
+};
+
+struct FinalizeArgs {
+    const double *partials;
+    int ncta;
+    double *norm_hist, *dt_hist, *sig;
+    long long *step_ctr;
+    int cap, block_id, nblocks, lead, bump;
+    double cfl, dt_fixed;
 };
 
 struct MetricsArgs {
@@ -74,6 +81,7 @@ struct MetricsArgs {
 
 // launchers (sfv_kernels.cu); all asynchronous on `st`
 cudaError_t launch_stage(const StageArgs &a, int mode, bool norms, bool dtmax, cudaStream_t st);
+cudaError_t launch_finalize(const FinalizeArgs &f, cudaStream_t st);
 cudaError_t stage_occupancy(int mode, bool norms, bool dtmax, bool fast, int *ctas_per_sm);
 bool fast_path(const Params &P);
 cudaError_t prepare_stage_kernels();

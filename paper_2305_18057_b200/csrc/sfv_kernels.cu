@@ -61,6 +61,23 @@ __device__ __forceinline__ void tma_2d(void *dst, const CUtensorMap *map, int x,
         : "memory");
 }
 
+// Whole-warp issue: one elected lane posts the expected bytes / the copy.
+__device__ __forceinline__ void elect_expect_tx(uint64_t *bar, unsigned bytes) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\telect.sync _|p, 0xffffffff;\n\t"
+        "@p mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n\t}" ::"r"(smem_u32(bar)),
+        "r"(bytes)
+        : "memory");
+}
+__device__ __forceinline__ void elect_tma_2d(void *dst, const CUtensorMap *map, int x, int y, uint64_t *bar) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\telect.sync _|p, 0xffffffff;\n\t"
+        "@p cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];"
+        "\n\t}" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(smem_u32(bar))
+        : "memory");
+}
+
 // Fast reciprocal / reciprocal square root: MUFU seed + one cubic-convergent
 // correction (relative error ~ seed^3 << 2^-53, i.e. within ~1 ulp).
 __device__ __forceinline__ double frcp(double d) {
@@ -97,9 +114,10 @@ __device__ __forceinline__ void muscl_cell(double w, double b, double f, const P
     if constexpr (FAST) {
         // bounded van Albada, kappa = -1 (c2 = 0): s1 = c1 max(0, (2bf+d)/(b^2+f^2+d))
         //   qU = w + s1 b,  qD = w - s1 f
+        // with h = s1/2 = c1 (bf + d/2) / (b^2+f^2+d): max(0, 2h) = h + |h| exactly
         const double r = frcp(fma(b, b, fma(f, f, P.delta)));
-        double s1 = fma(P.c1x2, b * f, P.c1d) * r;
-        s1 = s1 > 0.0 ? s1 : 0.0;
+        const double h = fma(P.c1h, b * f, P.c1dh) * r;
+        const double s1 = h + fabs(h);
         qU = fma(s1, b, w);
         qD = fma(-s1, f, w);
         return;
@@ -233,9 +251,10 @@ __host__ __device__ constexpr size_t stage_smem() {
     return sizeof(double) * ((size_t)WPC * StageTraits<MODE>::WARP_DBL + 8 * (NT / 32));
 }
 
-#ifndef SFV_MINB
-#define SFV_MINB 3  // resident CTAs per SM the register allocation targets (168 regs: no spills)
+#ifndef SFV_MIN_WARPS
+#define SFV_MIN_WARPS 12  // resident warps per SM the register allocation targets (168 regs: no spills)
 #endif
+constexpr int SFV_MINB = SFV_MIN_WARPS / WPC;
 #ifndef SFV_UNROLL
 #define SFV_UNROLL 1  // row-loop unroll: lets ptxas rename the carried window instead of moving it
 #endif
@@ -256,7 +275,8 @@ __global__ void __launch_bounds__(NT, SFV_MINB) stage_kernel(const __grid_consta
     double *red = smem + WPC * TR::WARP_DBL;    // [8][WPC]
 
     const Params &P = a.P;
-    const long long n = *a.step_ctr;
+    // step index: the finalize kernel after stage 1 advances the counter
+    const long long n = *a.step_ctr - (a.stage > 1 ? 1 : 0);
     const double dt = P.dt_fixed > 0.0 ? P.dt_fixed : P.cfl / a.sig[n & 1];
     const double coef = a.coef * dt;
     const int PJ = a.PJ;
@@ -284,29 +304,24 @@ __global__ void __launch_bounds__(NT, SFV_MINB) stage_kernel(const __grid_consta
 
         auto wslot = [&](int r) -> const double * { return wring + ((r - r0) & 3) * TR::W_SLOT; };
         auto mslot = [&](int r) -> const double * { return mring + ((r - m0) & 1) * TR::M_SLOT; };
-        // one 2D TMA box per ring row, issued by lane 0 (36 columns x 4 / 7 rows)
+        // one 2D TMA box per ring row (36 columns x 4 / 7 rows), issued by the
+        // whole warp through elect.sync (operands are warp-uniform: 1 warp/CTA)
         const int tx = j0 - 2 + JOFF;
         auto issue_w = [&](int r) {
-            if (lane == 0) {
-                const int s = (r - r0) & 3;
-                mbar_expect_tx(&wbar[s], 4u * ROWB);
-                tma_2d(wring + s * TR::W_SLOT, &a.tm_in, tx, (r + 2) * 4, &wbar[s]);
-            }
+            const int s = (r - r0) & 3;
+            elect_expect_tx(&wbar[s], 4u * ROWB);
+            elect_tma_2d(wring + s * TR::W_SLOT, &a.tm_in, tx, (r + 2) * 4, &wbar[s]);
         };
         auto issue_m = [&](int r) {
-            if (lane == 0) {
-                const int s = (r - m0) & 1;
-                mbar_expect_tx(&mbar[s], (unsigned)NMET * ROWB);
-                tma_2d(mring + s * TR::M_SLOT, &a.tm_met, tx, (r + 1) * NMET, &mbar[s]);
-            }
+            const int s = (r - m0) & 1;
+            elect_expect_tx(&mbar[s], (unsigned)NMET * ROWB);
+            elect_tma_2d(mring + s * TR::M_SLOT, &a.tm_met, tx, (r + 1) * NMET, &mbar[s]);
         };
         auto issue_p = [&](int r) {
             if constexpr (TR::NPW > 0) {
-                if (lane == 0) {
-                    mbar_expect_tx(pbar, 4u * TR::NPW * ROWB);
+                elect_expect_tx(pbar, 4u * TR::NPW * ROWB);
 #pragma unroll
-                    for (int p = 0; p < TR::NPW; ++p) tma_2d(pring + p * 4 * WROW, &a.tm_pw[p], tx, (r + 2) * 4, pbar);
-                }
+                for (int p = 0; p < TR::NPW; ++p) elect_tma_2d(pring + p * 4 * WROW, &a.tm_pw[p], tx, (r + 2) * 4, pbar);
             }
         };
         auto wait_w = [&](int r) { mbar_wait(&wbar[(r - r0) & 3], (unsigned)(((r - r0) >> 2) & 1)); };
@@ -375,7 +390,6 @@ __global__ void __launch_bounds__(NT, SFV_MINB) stage_kernel(const __grid_consta
             double qD[4], qU[4], qS[4], qN[4], Wv[4];
             {
                 const double *sn = wslot(v + 2);
-                const double *sv = wslot(v);
 #pragma unroll
                 for (int c = 0; c < 4; ++c) {  // i: reconstruct cell v+1
                     const double wn = sn[c * WROW + own];
@@ -384,6 +398,7 @@ __global__ void __launch_bounds__(NT, SFV_MINB) stage_kernel(const __grid_consta
                     fp[c] = f;
                     Wc[c] = wn;
                 }
+                const double *sv = wslot(v);
 #pragma unroll
                 for (int c = 0; c < 4; ++c) {  // j: reconstruct cell (v, jc)
                     const double wm = sv[c * WROW + own - 1];
@@ -533,7 +548,6 @@ __global__ void __launch_bounds__(NT, SFV_MINB) stage_kernel(const __grid_consta
     }
 
     // ---- CTA reductions --------------------------------------------------
-    const unsigned ncta = gridDim.x;
     if (DTMAX) {
         for (int o = 16; o > 0; o >>= 1) smax = fmax(smax, __shfl_xor_sync(0xffffffffu, smax, o));
         if (lane == 0) red[warp] = smax;
@@ -544,9 +558,9 @@ __global__ void __launch_bounds__(NT, SFV_MINB) stage_kernel(const __grid_consta
             atomicMax(reinterpret_cast<unsigned long long *>(&a.sig[(n + 1) & 1]),
                       (unsigned long long)__double_as_longlong(m));
         }
-        __syncthreads();
     }
     if (NORMS) {
+        // per-CTA partials, layout [8][ncta]; reduced in fixed order by finalize_kernel
 #pragma unroll
         for (int q = 0; q < 8; ++q) {
             double x = nrm[q];
@@ -560,53 +574,51 @@ __global__ void __launch_bounds__(NT, SFV_MINB) stage_kernel(const __grid_consta
         if (t < 8) {
             double x = red[t * WPC];
             for (int w = 1; w < WPC; ++w) x = t < 4 ? x + red[t * WPC + w] : fmax(x, red[t * WPC + w]);
-            a.partials[(size_t)blockIdx.x * 8 + t] = x;
+            a.partials[(size_t)t * gridDim.x + blockIdx.x] = x;
         }
     }
-    // ---- last-CTA epilogue: norms finalize, dt record, step counter ---------
-    if (NORMS || a.bump) {
-        __shared__ unsigned s_last;
-        __threadfence();
-        __syncthreads();
-        if (t == 0) s_last = (atomicAdd(a.ticket, 1u) == ncta - 1);
-        __syncthreads();
-        if (s_last) {
-            __threadfence();
-            if (NORMS) {
-                // deterministic: fixed strided assignment, fixed-order tree
-                double acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-                for (unsigned b = t; b < ncta; b += NT) {
+}
+
+// After stage 1 of each block: deterministic fixed-order reduction of the
+// norm partials into the history ("residual print"; reading
+// A-R20); the lead block records dt_n and clears the sigma slot the last
+// stage will fill; the last block advances the step counter.
+constexpr int FIN_T = 512;
+__global__ void __launch_bounds__(FIN_T) finalize_kernel(FinalizeArgs f) {
+    __shared__ double tree[8][FIN_T];
+    const int t = threadIdx.x;
+    const long long n = *f.step_ctr;
+    double acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    for (int b = t; b < f.ncta; b += FIN_T) {
 #pragma unroll
-                    for (int q = 0; q < 8; ++q) {
-                        const double x = __ldcg(&a.partials[(size_t)b * 8 + q]);
-                        acc[q] = q < 4 ? acc[q] + x : fmax(acc[q], x);
-                    }
-                }
-                double *tree = smem;  // rings are dead: [8][NT]
-#pragma unroll
-                for (int q = 0; q < 8; ++q) tree[q * NT + t] = acc[q];
-                __syncthreads();
-                for (int s = NT / 2; s > 0; s >>= 1) {
-                    if (t < s) {
-#pragma unroll
-                        for (int q = 0; q < 8; ++q)
-                            tree[q * NT + t] = q < 4 ? tree[q * NT + t] + tree[q * NT + t + s]
-                                                     : fmax(tree[q * NT + t], tree[q * NT + t + s]);
-                    }
-                    __syncthreads();
-                }
-                if (t < 8) a.norm_hist[((size_t)(n % a.cap) * a.nblocks + a.block_id) * 8 + t] = tree[t * NT];
-                if (t == 0 && a.lead) {
-                    a.dt_hist[n % a.cap] = dt;
-                    if (!(P.dt_fixed > 0.0)) a.sig[(n + 1) & 1] = 0.0;
-                }
-            }
-            if (t == 0) {
-                if (a.bump) *a.step_ctr = n + 1;
-                *a.ticket = 0u;
-            }
+        for (int q = 0; q < 8; ++q) {
+            const double x = f.partials[(size_t)q * f.ncta + b];
+            acc[q] = q < 4 ? acc[q] + x : fmax(acc[q], x);
         }
     }
+#pragma unroll
+    for (int q = 0; q < 8; ++q) tree[q][t] = acc[q];
+    __syncthreads();
+    for (int s = FIN_T / 2; s > 0; s >>= 1) {
+        if (t < s) {
+#pragma unroll
+            for (int q = 0; q < 8; ++q) tree[q][t] = q < 4 ? tree[q][t] + tree[q][t + s] : fmax(tree[q][t], tree[q][t + s]);
+        }
+        __syncthreads();
+    }
+    if (t < 8) f.norm_hist[((size_t)(n % f.cap) * f.nblocks + f.block_id) * 8 + t] = tree[t][0];
+    if (t == 0) {
+        if (f.lead) {
+            f.dt_hist[n % f.cap] = f.dt_fixed > 0.0 ? f.dt_fixed : f.cfl / f.sig[n & 1];
+            if (!(f.dt_fixed > 0.0)) f.sig[(n + 1) & 1] = 0.0;
+        }
+        if (f.bump) *f.step_ctr = n + 1;
+    }
+}
+
+cudaError_t launch_finalize(const FinalizeArgs &f, cudaStream_t st) {
+    finalize_kernel<<<1, FIN_T, 0, st>>>(f);
+    return cudaGetLastError();
 }
 
 template <int MODE, bool NORMS, bool DTMAX, bool FAST>
