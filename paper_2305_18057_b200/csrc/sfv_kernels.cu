@@ -61,6 +61,35 @@ __device__ __forceinline__ void tma_2d(void *dst, const CUtensorMap *map, int x,
         : "memory");
 }
 
+// 32-bit shared-window address variants (addresses precomputed once per warp)
+__device__ __forceinline__ void mbar_wait_s(unsigned bar, unsigned parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "SFV_WAITS_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra SFV_WAITS_%=;\n\t}" ::"r"(bar),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void elect_issue_s(unsigned dst, const CUtensorMap *map, int x, int y, unsigned bar,
+                                              unsigned bytes) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\telect.sync _|p, 0xffffffff;\n\t"
+        "@p mbarrier.arrive.expect_tx.shared::cta.b64 _, [%4], %5;\n\t"
+        "@p cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];"
+        "\n\t}" ::"r"(dst),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(bar), "r"(bytes)
+        : "memory");
+}
+__device__ __forceinline__ void elect_tma_s(unsigned dst, const CUtensorMap *map, int x, int y, unsigned bar) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\telect.sync _|p, 0xffffffff;\n\t"
+        "@p cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];"
+        "\n\t}" ::"r"(dst),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(bar)
+        : "memory");
+}
+
 // Whole-warp issue: one elected lane posts the expected bytes / the copy.
 __device__ __forceinline__ void elect_expect_tx(uint64_t *bar, unsigned bytes) {
     asm volatile(
@@ -243,7 +272,8 @@ struct StageTraits {
     static constexpr int W_SLOT = 4 * WROW;           // stencil ring: 4 rows (v..v+2 + 1 in flight), 1152 B
     static constexpr int M_SLOT = 256;                // metrics ring: 2 rows (v + 1 in flight), 7*288 B -> 2 KB
     static constexpr int P_SLOT = 4 * NPW * WROW;     // pointwise: row v
-    static constexpr int WARP_DBL = 4 * W_SLOT + 2 * M_SLOT + P_SLOT + 16;  // + 7 mbarriers, 128 B aligned
+    static constexpr int X_SLOT = 8 * 32;             // lane exchange: north states [4][32], south fluxes [4][32]
+    static constexpr int WARP_DBL = 4 * W_SLOT + 2 * M_SLOT + P_SLOT + X_SLOT + 16;  // + 7 mbarriers, 128 B aligned
 };
 
 template <int MODE>
@@ -269,7 +299,8 @@ __global__ void __launch_bounds__(NT, SFV_MINB) stage_kernel(const __grid_consta
     double *wring = wbase;                      // [4][4][WROW]
     double *mring = wring + 4 * TR::W_SLOT;     // [2][7][WROW]
     double *pring = mring + 2 * TR::M_SLOT;     // [4*NPW][WROW]
-    uint64_t *wbar = reinterpret_cast<uint64_t *>(pring + TR::P_SLOT);  // [4]
+    double *xch = pring + TR::P_SLOT;           // [8][32] lane exchange
+    uint64_t *wbar = reinterpret_cast<uint64_t *>(xch + TR::X_SLOT);   // [4]
     uint64_t *mbar = wbar + 4;                                           // [2]
     uint64_t *pbar = mbar + 2;                                           // [1]
     double *red = smem + WPC * TR::WARP_DBL;    // [8][WPC]
@@ -305,27 +336,34 @@ __global__ void __launch_bounds__(NT, SFV_MINB) stage_kernel(const __grid_consta
         auto wslot = [&](int r) -> const double * { return wring + ((r - r0) & 3) * TR::W_SLOT; };
         auto mslot = [&](int r) -> const double * { return mring + ((r - m0) & 1) * TR::M_SLOT; };
         // one 2D TMA box per ring row (36 columns x 4 / 7 rows), issued by the
-        // whole warp through elect.sync (operands are warp-uniform: 1 warp/CTA)
+        // whole warp through elect.sync (operands are warp-uniform: 1 warp/CTA);
+        // shared-window addresses are computed once
         const int tx = j0 - 2 + JOFF;
+        const unsigned wring_s = smem_u32(wring), mring_s = smem_u32(mring), pring_s = smem_u32(pring);
+        const unsigned wbar_s = smem_u32(wbar), mbar_s = smem_u32(mbar), pbar_s = smem_u32(pbar);
         auto issue_w = [&](int r) {
-            const int s = (r - r0) & 3;
-            elect_expect_tx(&wbar[s], 4u * ROWB);
-            elect_tma_2d(wring + s * TR::W_SLOT, &a.tm_in, tx, (r + 2) * 4, &wbar[s]);
+            const unsigned s = (unsigned)(r - r0) & 3u;
+            elect_issue_s(wring_s + s * (TR::W_SLOT * 8u), &a.tm_in, tx, (r + 2) * 4, wbar_s + 8u * s, 4u * ROWB);
         };
         auto issue_m = [&](int r) {
-            const int s = (r - m0) & 1;
-            elect_expect_tx(&mbar[s], (unsigned)NMET * ROWB);
-            elect_tma_2d(mring + s * TR::M_SLOT, &a.tm_met, tx, (r + 1) * NMET, &mbar[s]);
+            const unsigned s = (unsigned)(r - m0) & 1u;
+            elect_issue_s(mring_s + s * (TR::M_SLOT * 8u), &a.tm_met, tx, (r + 1) * NMET, mbar_s + 8u * s,
+                          (unsigned)NMET * ROWB);
         };
         auto issue_p = [&](int r) {
             if constexpr (TR::NPW > 0) {
-                elect_expect_tx(pbar, 4u * TR::NPW * ROWB);
+                elect_issue_s(pring_s, &a.tm_pw[0], tx, (r + 2) * 4, pbar_s, 4u * TR::NPW * ROWB);
 #pragma unroll
-                for (int p = 0; p < TR::NPW; ++p) elect_tma_2d(pring + p * 4 * WROW, &a.tm_pw[p], tx, (r + 2) * 4, pbar);
+                for (int p = 1; p < TR::NPW; ++p)
+                    elect_tma_s(pring_s + p * (4u * WROW * 8u), &a.tm_pw[p], tx, (r + 2) * 4, pbar_s);
             }
         };
-        auto wait_w = [&](int r) { mbar_wait(&wbar[(r - r0) & 3], (unsigned)(((r - r0) >> 2) & 1)); };
-        auto wait_m = [&](int r) { mbar_wait(&mbar[(r - m0) & 1], (unsigned)(((r - m0) >> 1) & 1)); };
+        auto wait_w = [&](int r) {
+            mbar_wait_s(wbar_s + 8u * ((unsigned)(r - r0) & 3u), (unsigned)(((r - r0) >> 2) & 1));
+        };
+        auto wait_m = [&](int r) {
+            mbar_wait_s(mbar_s + 8u * ((unsigned)(r - m0) & 1u), (unsigned)(((r - m0) >> 1) & 1));
+        };
 
         if (lane == 0) {
             for (int s = 0; s < 7; ++s) mbar_init(&wbar[s], 1);
@@ -333,9 +371,8 @@ __global__ void __launch_bounds__(NT, SFV_MINB) stage_kernel(const __grid_consta
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         }
         __syncwarp();
-        int next_w = r0, next_m = m0;
-        for (; next_w <= r0 + 3 && next_w <= r_last; ++next_w) issue_w(next_w);
-        for (; next_m <= m0 + 1 && next_m <= m_last; ++next_m) issue_m(next_m);
+        for (int r = r0; r <= r0 + 3 && r <= r_last; ++r) issue_w(r);
+        for (int r = m0; r <= m0 + 1 && r <= m_last; ++r) issue_m(r);
 
         double Wc[4], fp[4], QLp[4], GW[4];
         double nWx = 0.0, nWy = 0.0;             // i-face(0) normal (W-edge slip ghosts)
@@ -358,7 +395,7 @@ __global__ void __launch_bounds__(NT, SFV_MINB) stage_kernel(const __grid_consta
             }
         }
         __syncwarp();  // rows r0, r0+1 consumed
-        for (; next_w <= r0 + 5 && next_w <= r_last; ++next_w) issue_w(next_w);
+        for (int r = r0 + 4; r <= r0 + 5 && r <= r_last; ++r) issue_w(r);
         wait_w(r0 + 3);
         wait_m(m0);
         {
@@ -384,6 +421,7 @@ __global__ void __launch_bounds__(NT, SFV_MINB) stage_kernel(const __grid_consta
         }
 
         // ---- main loop: one output row per iteration ---------------------------
+        double *outp = a.out + (size_t)((i_start + 2) * 4) * PJ + (jc + JOFF);
 #pragma unroll kRowUnroll
         for (int v = i_start; v < i_end; ++v) {
             wait_w(v + 2);
@@ -406,19 +444,20 @@ __global__ void __launch_bounds__(NT, SFV_MINB) stage_kernel(const __grid_consta
                     const double wp = sv[c * WROW + own + 1];
                     double qn;
                     muscl_cell<FAST>(w, w - wm, wp - w, P, qn, qS[c]);
-                    qN[c] = __shfl_up_sync(0xffffffffu, qn, 1);  // north state of the cell below
+                    xch[c * 32 + lane] = qn;  // north state, read by the lane above
                     Wv[c] = w;
                 }
             }
             __syncwarp();  // stencil row v-1, metric row v-1, pointwise slot consumed
-            {
-                const int lw = min(v + 3, r_last), lm = min(v + 1, m_last);
-                for (; next_w <= lw; ++next_w) issue_w(next_w);
-                for (; next_m <= lm; ++next_m) issue_m(next_m);
-                issue_p(v);
-            }
+            // steady state: exactly one row per ring (rows up to r0+5 / m0+1 were
+            // issued in the prologue)
+            if (v + 3 >= r0 + 6 && v + 3 <= r_last) issue_w(v + 3);
+            if (v + 1 <= m_last) issue_m(v + 1);
+            issue_p(v);
             wait_m(v);
             const double *mv = mslot(v);
+#pragma unroll
+            for (int c = 0; c < 4; ++c) qN[c] = xch[c * 32 + (lane > 0 ? lane - 1 : 0)];
             double GE[4], GS[4];
             // both face fluxes of this row: two independent Roe evaluations
             const bool okE = roe_flux(QLp, qD, mv[0 * WROW + own], mv[1 * WROW + own], mv[2 * WROW + own], P, GE);
@@ -427,9 +466,12 @@ __global__ void __launch_bounds__(NT, SFV_MINB) stage_kernel(const __grid_consta
 #pragma unroll
             for (int c = 0; c < 4; ++c) {
                 QLp[c] = qU[c];
-                GN[c] = __shfl_down_sync(0xffffffffu, GS[c], 1);
+                xch[(4 + c) * 32 + lane] = GS[c];  // south flux = north flux of the lane below
             }
-            if constexpr (TR::NPW > 0) mbar_wait(pbar, (unsigned)((v - i_start) & 1));
+            __syncwarp();
+#pragma unroll
+            for (int c = 0; c < 4; ++c) GN[c] = xch[(4 + c) * 32 + (lane < 31 ? lane + 1 : 31)];
+            if constexpr (TR::NPW > 0) mbar_wait_s(pbar_s, (unsigned)((v - i_start) & 1));
             // ---- residual (Eq. 5) and stage update (Eq. 6): every lane computes,
             // output lanes store (no divergence in the common path)
             const double iV = mv[6 * WROW + own];
@@ -455,7 +497,11 @@ __global__ void __launch_bounds__(NT, SFV_MINB) stage_kernel(const __grid_consta
                     U[c] = un + fma(-coef, rv, 0.5 * (Wv[c] - un));
                 }
             }
-            if (is_out) store4(a.out, PJ, v, jc, U);
+            if (is_out) {
+#pragma unroll
+                for (int c = 0; c < 4; ++c) outp[(size_t)c * PJ] = U[c];
+            }
+            outp += (size_t)4 * PJ;
             // new-state validity: rho > 0 and 2 rho E > |m|^2 (<=> p > 0)
             const bool st_ok = (U[0] > 0.0) & (2.0 * U[0] * U[3] > fma(U[1], U[1], U[2] * U[2]));
             // rare path behind one warp vote: invalid face or new states (reading A-R28)
