@@ -107,6 +107,11 @@ __device__ __forceinline__ void elect_tma_2d(void *dst, const CUtensorMap *map, 
         : "memory");
 }
 
+// Programmatic dependent launch (PDL): let the next grid be scheduled, and
+// wait for the previous grid's completion + memory visibility.
+__device__ __forceinline__ void pdl_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 // Fast reciprocal / reciprocal square root: MUFU seed + one cubic-convergent
 // correction (relative error ~ seed^3 << 2^-53, i.e. within ~1 ulp).
 __device__ __forceinline__ double frcp(double d) {
@@ -306,10 +311,16 @@ __global__ void __launch_bounds__(NT, SFV_MINB) stage_kernel(const __grid_consta
     double *red = smem + WPC * TR::WARP_DBL;    // [8][WPC]
 
     const Params &P = a.P;
-    // step index: the finalize kernel after stage 1 advances the counter
-    const long long n = *a.step_ctr - (a.stage > 1 ? 1 : 0);
-    const double dt = P.dt_fixed > 0.0 ? P.dt_fixed : P.cfl / a.sig[n & 1];
-    const double coef = a.coef * dt;
+    // step index and dt are read after griddepcontrol.wait (programmatic
+    // dependent launch: the previous kernel may still be running until then)
+    long long n = 0;
+    double dt = 0.0, coef = 0.0;
+    auto read_step = [&]() {
+        // the finalize kernel after stage 1 advances the counter
+        n = *a.step_ctr - (a.stage > 1 ? 1 : 0);
+        dt = P.dt_fixed > 0.0 ? P.dt_fixed : P.cfl / a.sig[n & 1];
+        coef = a.coef * dt;
+    };
     const int PJ = a.PJ;
     double nrm[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     double smax = 0.0;
@@ -371,8 +382,14 @@ __global__ void __launch_bounds__(NT, SFV_MINB) stage_kernel(const __grid_consta
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         }
         __syncwarp();
-        for (int r = r0; r <= r0 + 3 && r <= r_last; ++r) issue_w(r);
+        // metrics are read-only: prefetch them before waiting for the previous grid
         for (int r = m0; r <= m0 + 1 && r <= m_last; ++r) issue_m(r);
+        pdl_wait();
+        // trigger only after the wait: at most one dependent grid is pending, so
+        // its waiting CTAs cannot hold slots this grid still needs
+        pdl_launch_dependents();
+        read_step();
+        for (int r = r0; r <= r0 + 3 && r <= r_last; ++r) issue_w(r);
 
         double Wc[4], fp[4], QLp[4], GW[4];
         double nWx = 0.0, nWy = 0.0;             // i-face(0) normal (W-edge slip ghosts)
@@ -593,6 +610,12 @@ __global__ void __launch_bounds__(NT, SFV_MINB) stage_kernel(const __grid_consta
         }
     }
 
+    else {
+        pdl_wait();
+        pdl_launch_dependents();
+        read_step();
+    }
+
     // ---- CTA reductions --------------------------------------------------
     if (DTMAX) {
         for (int o = 16; o > 0; o >>= 1) smax = fmax(smax, __shfl_xor_sync(0xffffffffu, smax, o));
@@ -633,6 +656,8 @@ constexpr int FIN_T = 512;
 __global__ void __launch_bounds__(FIN_T) finalize_kernel(FinalizeArgs f) {
     __shared__ double tree[8][FIN_T];
     const int t = threadIdx.x;
+    pdl_wait();
+    pdl_launch_dependents();
     const long long n = *f.step_ctr;
     double acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     for (int b = t; b < f.ncta; b += FIN_T) {
@@ -663,16 +688,32 @@ __global__ void __launch_bounds__(FIN_T) finalize_kernel(FinalizeArgs f) {
 }
 
 cudaError_t launch_finalize(const FinalizeArgs &f, cudaStream_t st) {
-    finalize_kernel<<<1, FIN_T, 0, st>>>(f);
-    return cudaGetLastError();
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(1);
+    cfg.blockDim = dim3(FIN_T);
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, finalize_kernel, f);
 }
 
 template <int MODE, bool NORMS, bool DTMAX, bool FAST>
 static cudaError_t launch_t(const StageArgs &a, cudaStream_t st) {
     auto k = stage_kernel<MODE, NORMS, DTMAX, FAST>;
-    const size_t sm = stage_smem<MODE>();  // attribute set by prepare_stage_kernels()
-    k<<<(a.nstrips * a.nseg + WPC - 1) / WPC, NT, sm, st>>>(a);
-    return cudaGetLastError();
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3((a.nstrips * a.nseg + WPC - 1) / WPC);
+    cfg.blockDim = dim3(NT);
+    cfg.dynamicSmemBytes = stage_smem<MODE>();  // attribute set by prepare_stage_kernels()
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, k, a);
 }
 
 template <int MODE, bool NORMS, bool DTMAX, bool FAST>
