@@ -69,6 +69,11 @@ struct Block {
     int nbr[4] = {-1, -1, -1, -1};
     int edge[4] = {0, 0, 0, 0};  // Edge kind per W, E, S, N
     int nstrips = 1, nseg = 1;
+    // launch plan of a stage: edge rows first (2 rows per connected i-cut,
+    // exchanged while the interior runs), then the interior rows
+    int nlaunch = 1, row_lo[3] = {0, 0, 0}, row_hi[3] = {0, 0, 0}, lseg[3] = {1, 1, 1}, lbase[3] = {0, 0, 0};
+    int ncta_total = 1;
+    bool split = false;
     double *buf[4] = {nullptr, nullptr, nullptr, nullptr};
     double *met = nullptr, *nodes = nullptr, *stage = nullptr, *partials = nullptr;
     double *xs[2] = {nullptr, nullptr}, *xr[2] = {nullptr, nullptr};  // j-cut pack buffers (S, N)
@@ -132,6 +137,8 @@ struct sfv_ctx {
     Params P{};
     long long steps_enq = 0;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    cudaStream_t comm_st = nullptr;                  // halo exchange stream (overlap)
+    cudaEvent_t ev_edge = nullptr, ev_comm = nullptr;
     bool timing_open = false;
     cudaGraphExec_t gexec = nullptr;
     bool graph_failed = false;
@@ -242,6 +249,37 @@ void choose_launch(sfv_ctx *c, Block &b) {
     }
 }
 
+// Stage launch plan of a block: with a connected i-cut and
+// overlap enabled, the 2 edge rows at each cut are computed first so their
+// exchange overlaps the interior launch.
+void plan_launches(sfv_ctx *c, Block &b) {
+    const bool cw = b.nbr[0] >= 0, ce = b.nbr[1] >= 0;
+    const char *ov = getenv("SFV_OVERLAP");
+    const bool overlap = !(ov && ov[0] == '0');
+    b.split = overlap && (cw || ce) && b.ni >= 8;
+    int n = 0;
+    int lo = 0, hi = b.ni;
+    if (b.split) {
+        if (cw) { b.row_lo[n] = 0; b.row_hi[n] = 2; b.lseg[n] = 1; ++n; lo = 2; }
+        if (ce) { b.row_lo[n] = b.ni - 2; b.row_hi[n] = b.ni; b.lseg[n] = 1; ++n; hi = b.ni - 2; }
+        // interior: re-run the segment choice on the interior rows
+        Block t = b;
+        t.ni = hi - lo;
+        choose_launch(c, t);
+        b.row_lo[n] = lo; b.row_hi[n] = hi; b.lseg[n] = t.nseg; ++n;
+    } else {
+        b.row_lo[0] = 0; b.row_hi[0] = b.ni; b.lseg[0] = b.nseg; n = 1;
+    }
+    b.nlaunch = n;
+    int base = 0;
+    for (int q = 0; q < n; ++q) {
+        b.lbase[q] = base;
+        base += (b.nstrips * b.lseg[q] + WPC - 1) / WPC;
+    }
+    b.ncta_total = base;
+    b.nseg = b.lseg[n - 1];
+}
+
 sfv_status build_blocks(sfv_ctx *c) {
     c->blocks.clear();
     const int nb = c->px * c->py;
@@ -302,7 +340,7 @@ size_t layout(sfv_ctx *c, bool assign) {
         size_t om = take(sizeof(double) * b.met_elems());
         size_t on = take(sizeof(double) * 2 * (size_t)(b.ni + 1) * (b.nj + 1));
         size_t os = take(sizeof(double) * 4 * (size_t)b.ni * b.nj);
-        const int max_cta = (((b.nj + WOUT - 1) / WOUT) * NSEG_MAX + WPC - 1) / WPC;
+        const int max_cta = (((b.nj + WOUT - 1) / WOUT) * (NSEG_MAX + 2) + WPC - 1) / WPC + 2;
         size_t op = take(sizeof(double) * 8 * (size_t)max_cta);
         size_t ot = take(256);
         size_t ox[4];
@@ -349,8 +387,12 @@ Block *local_block(sfv_ctx *c, int id) {
 // data exchange"; reading A-R16/A-R18: 2 layers, face neighbours only).
 // i-cuts: the 2 edge rows are one contiguous run in the [i][c][j] layout;
 // j-cuts: 2 columns, strided.
-sfv_status exchange(sfv_ctx *c, int k, cudaStream_t st) {
-    if (c->nblocks_total == 1) return SFV_OK;
+// Halo exchange of state buffer k after a stage ("boundary
+// data exchange"; reading A-R16/A-R18: 2 layers, face neighbours only).
+// i-cuts (rows): the 2 edge rows are one contiguous run in the [i][c][j]
+// layout (zero-copy); j-cuts (columns): strided, packed for NCCL.
+sfv_status exchange_rows(sfv_ctx *c, int k, cudaStream_t st) {
+    if (c->px == 1) return SFV_OK;
     if (c->nranks == 1) {
         for (Block &b : c->blocks) {
             if (b.nbr[1] >= 0) {  // E neighbour e: b rows ni-2,ni-1 -> e rows -2,-1; e rows 0,1 -> b rows ni,ni+1
@@ -360,6 +402,30 @@ sfv_status exchange(sfv_ctx *c, int k, cudaStream_t st) {
                 CK(cudaMemcpyAsync(b.buf[k] + (size_t)(b.ni + 2) * 4 * b.PJ, e.buf[k] + (size_t)2 * 4 * e.PJ, run * 8,
                                    cudaMemcpyDeviceToDevice, st));
             }
+        }
+        return SFV_OK;
+    }
+    // NCCL: one block per rank (block id == rank); executes halo_plan()'s i-cuts.
+    Block &b = c->blocks[0];
+    Nccl &N = nccl();
+    EdgePlan p[4];
+    halo_plan(c, b.id, p);
+    NK(N.GroupStart());
+    const size_t run = (size_t)2 * 4 * b.PJ;  // 2 rows x 4 comps x pitch: contiguous in [i][c][j]
+    for (int e = 0; e < 2; ++e) {
+        const EdgePlan &q = p[e];
+        if (q.nbr < 0) continue;
+        NK(N.Send(b.buf[k] + (size_t)(q.si0 - b.i0 + 2) * 4 * b.PJ, run, ncclDouble, q.nbr, c->comm, st));
+        NK(N.Recv(b.buf[k] + (size_t)(q.ri0 - b.i0 + 2) * 4 * b.PJ, run, ncclDouble, q.nbr, c->comm, st));
+    }
+    NK(N.GroupEnd());
+    return SFV_OK;
+}
+
+sfv_status exchange_cols(sfv_ctx *c, int k, cudaStream_t st) {
+    if (c->py == 1) return SFV_OK;
+    if (c->nranks == 1) {
+        for (Block &b : c->blocks) {
             if (b.nbr[3] >= 0) {  // N neighbour: b cols nj-2,nj-1 -> n cols -2,-1; n cols 0,1 -> b cols nj,nj+1
                 Block &n = *local_block(c, b.nbr[3]);
                 CK(cudaMemcpy2DAsync(n.buf[k] + (size_t)8 * n.PJ + (-2 + JOFF), (size_t)n.PJ * 8,
@@ -372,24 +438,16 @@ sfv_status exchange(sfv_ctx *c, int k, cudaStream_t st) {
         }
         return SFV_OK;
     }
-    // NCCL: one block per rank (block id == rank); executes halo_plan().
     Block &b = c->blocks[0];
     Nccl &N = nccl();
     EdgePlan p[4];
     halo_plan(c, b.id, p);
-    for (int s = 0; s < 2; ++s) {  // j-cuts: pack the 2 send columns
+    for (int s = 0; s < 2; ++s) {  // pack the 2 send columns
         const EdgePlan &q = p[2 + s];
         if (q.nbr < 0) continue;
         CK(launch_pack_cols(b.buf[k], b.xs[s], b.ni, b.PJ, q.sj0 - b.j0, st));
     }
     NK(N.GroupStart());
-    const size_t run = (size_t)2 * 4 * b.PJ;  // 2 rows x 4 comps x pitch: contiguous in [i][c][j]
-    for (int e = 0; e < 2; ++e) {  // i-cuts: zero-copy rows
-        const EdgePlan &q = p[e];
-        if (q.nbr < 0) continue;
-        NK(N.Send(b.buf[k] + (size_t)(q.si0 - b.i0 + 2) * 4 * b.PJ, run, ncclDouble, q.nbr, c->comm, st));
-        NK(N.Recv(b.buf[k] + (size_t)(q.ri0 - b.i0 + 2) * 4 * b.PJ, run, ncclDouble, q.nbr, c->comm, st));
-    }
     for (int s = 0; s < 2; ++s) {
         const EdgePlan &q = p[2 + s];
         if (q.nbr < 0) continue;
@@ -403,6 +461,12 @@ sfv_status exchange(sfv_ctx *c, int k, cudaStream_t st) {
         CK(launch_unpack_cols(b.xr[s], b.buf[k], b.ni, b.PJ, q.rj0 - b.j0, st));
     }
     return SFV_OK;
+}
+
+sfv_status exchange(sfv_ctx *c, int k, cudaStream_t st) {
+    sfv_status r = exchange_rows(c, k, st);
+    if (r != SFV_OK) return r;
+    return exchange_cols(c, k, st);
 }
 
 StageArgs make_args(sfv_ctx *c, Block &b, int k) {
@@ -426,6 +490,10 @@ StageArgs make_args(sfv_ctx *c, Block &b, int k) {
     a.NJ = c->cfg.nj;
     a.nstrips = b.nstrips;
     a.nseg = b.nseg;
+    a.row_lo = 0;
+    a.row_hi = b.ni;
+    a.part_base = 0;
+    a.part_stride = b.ncta_total;
     for (int e = 0; e < 4; ++e) a.bc[e] = b.edge[e];
     a.coef = sp.coef;
     a.sig = c->sig;
@@ -446,17 +514,46 @@ StageArgs make_args(sfv_ctx *c, Block &b, int k) {
 sfv_status enqueue_step(sfv_ctx *c, cudaStream_t st) {
     const int s = nstages_of(c->cfg.rk);
     const bool cflmode = !(c->cfg.dt_fixed > 0.0);
+    bool any_split = false;
+    for (Block &b : c->blocks) any_split |= b.split;
     for (int k = 1; k <= s; ++k) {
         const StageSpec sp = stage_spec(c->cfg.rk, k);
-        for (Block &b : c->blocks) {
+        auto launch_part = [&](Block &b, int q) -> sfv_status {
             StageArgs a = make_args(c, b, k);
+            a.row_lo = b.row_lo[q];
+            a.row_hi = b.row_hi[q];
+            a.nseg = b.lseg[q];
+            a.part_base = b.lbase[q];
             CK(launch_stage(a, sp.mode, k == 1, k == s && cflmode, st));
+            return SFV_OK;
+        };
+        if (any_split) {
+            // edge rows -> [comm stream: row exchange] || interior rows -> join
+            for (Block &b : c->blocks)
+                for (int q = 0; q + 1 < b.nlaunch; ++q) {
+                    sfv_status r = launch_part(b, q);
+                    if (r != SFV_OK) return r;
+                }
+            CK(cudaEventRecord(c->ev_edge, st));
+            CK(cudaStreamWaitEvent(c->comm_st, c->ev_edge, 0));
+            sfv_status r = exchange_rows(c, sp.out, c->comm_st);
+            if (r != SFV_OK) return r;
+            CK(cudaEventRecord(c->ev_comm, c->comm_st));
+            for (Block &b : c->blocks) {
+                r = launch_part(b, b.nlaunch - 1);
+                if (r != SFV_OK) return r;
+            }
+        } else {
+            for (Block &b : c->blocks) {
+                sfv_status r = launch_part(b, 0);
+                if (r != SFV_OK) return r;
+            }
         }
         if (k == 1) {  // norms of R(U^n), dt record, step counter (after every block's stage 1)
             for (Block &b : c->blocks) {
                 FinalizeArgs f{};
                 f.partials = b.partials;
-                f.ncta = (b.nstrips * b.nseg + WPC - 1) / WPC;
+                f.ncta = b.ncta_total;
                 f.norm_hist = c->norm_hist;
                 f.dt_hist = c->dt_hist;
                 f.sig = c->sig;
@@ -471,8 +568,14 @@ sfv_status enqueue_step(sfv_ctx *c, cudaStream_t st) {
                 CK(launch_finalize(f, st));
             }
         }
-        sfv_status r = exchange(c, sp.out, st);
-        if (r != SFV_OK) return r;
+        if (any_split) {
+            sfv_status r = exchange_cols(c, sp.out, st);
+            if (r != SFV_OK) return r;
+            CK(cudaStreamWaitEvent(st, c->ev_comm, 0));
+        } else {
+            sfv_status r = exchange(c, sp.out, st);
+            if (r != SFV_OK) return r;
+        }
     }
     if (c->nranks > 1 && cflmode) NK(nccl().AllReduce(c->sig, c->sig, 2, ncclDouble, ncclMax, c->comm, st));
     return SFV_OK;
@@ -640,6 +743,13 @@ sfv_status sfv_bind(sfv_ctx *c, void *ws, size_t bytes, void *stream) {
     c->occ = std::max(1, o);
     CK(cudaEventCreate(&c->ev0));
     CK(cudaEventCreate(&c->ev1));
+    CK(cudaEventCreateWithFlags(&c->ev_edge, cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&c->ev_comm, cudaEventDisableTiming));
+    {
+        int lo = 0, hi = 0;
+        CK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+        CK(cudaStreamCreateWithPriority(&c->comm_st, cudaStreamNonBlocking, hi));
+    }
     cudaStream_t st = c->st;
     CK(cudaMemsetAsync(c->ws, 0, need, st));
     CK(cudaMemsetAsync(c->geo_bad, 0xff, 8, st));
@@ -647,6 +757,7 @@ sfv_status sfv_bind(sfv_ctx *c, void *ws, size_t bytes, void *stream) {
     const int nbuf = nbuf_of(c->cfg.rk);
     for (Block &b : c->blocks) {
         choose_launch(c, b);
+        plan_launches(c, b);
         for (int k = 0; k < nbuf; ++k)
             CK(make_row_tensor_map(&b.tm_buf[k], b.buf[k], (unsigned long long)(b.ni + 4) * 4, b.PJ, 4));
         CK(make_row_tensor_map(&b.tm_met, b.met, (unsigned long long)(b.ni + 1) * NMET, b.PJ, NMET));
@@ -877,7 +988,7 @@ sfv_status sfv_error_info(const sfv_ctx *c, int64_t *out4) {
 sfv_status sfv_launch_info(const sfv_ctx *c, int32_t *out4) {
     if (!c || !out4 || c->blocks.empty()) return SFV_ERR_ARG;
     out4[0] = c->blocks[0].nstrips;
-    out4[1] = c->blocks[0].nseg;
+    out4[1] = c->blocks[0].lseg[c->blocks[0].nlaunch - 1];
     out4[2] = NT;
     out4[3] = c->occ;
     return SFV_OK;
@@ -897,6 +1008,9 @@ void sfv_destroy(sfv_ctx *c) {
     if (c->gexec) cudaGraphExecDestroy(c->gexec);
     if (c->ev0) cudaEventDestroy(c->ev0);
     if (c->ev1) cudaEventDestroy(c->ev1);
+    if (c->ev_edge) cudaEventDestroy(c->ev_edge);
+    if (c->ev_comm) cudaEventDestroy(c->ev_comm);
+    if (c->comm_st) cudaStreamDestroy(c->comm_st);
     if (c->comm && nccl().ok) nccl().CommDestroy(c->comm);
     delete c;
 }

@@ -50,6 +50,8 @@ struct StageArgs {
     int ni, nj, PJ;
     int gi0, gj0, NI, NJ;
     int nstrips, nseg;
+    int row_lo, row_hi;     // rows of this launch (edge strips / interior split)
+    int part_base, part_stride;  // column range of this launch in the norm partials
     int bc[4];              // Edge per W, E, S, N
     double coef;            // this stage's dt multiplier
     double *sig;            // [2] max over cells of sigma/V (bits, atomicMax)
@@ -57,7 +59,7 @@ struct StageArgs {
     double *dt_hist;        // [cap]
     double *norm_hist;      // [cap][nblocks][8]
     int cap, block_id, nblocks;
-    double *partials;       // [8][ncta] norm partials (stage 1)
+    double *partials;       // [8][part_stride] norm partials (stage 1)
     unsigned long long *err;
     int stage, nstages;
     Params P;

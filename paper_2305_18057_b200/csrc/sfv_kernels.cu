@@ -338,8 +338,9 @@ __global__ void __launch_bounds__(NT, SFV_MINB) stage_kernel(const __grid_consta
         auto writes_ghost = [&](int e) { return a.bc[e] == E_SLIP || a.bc[e] == E_OUTFLOW; };
         const bool ghost_sn = (writes_ghost(2) && j0 == 0) || (writes_ghost(3) && j1 >= a.nj - 1);
         const bool ghost_w = writes_ghost(0), ghost_e = writes_ghost(1);
-        const int i_start = (int)(((long long)a.ni * seg) / a.nseg);
-        const int i_end = (int)(((long long)a.ni * (seg + 1)) / a.nseg);
+        const int nrows = a.row_hi - a.row_lo;
+        const int i_start = a.row_lo + (int)(((long long)nrows * seg) / a.nseg);
+        const int i_end = a.row_lo + (int)(((long long)nrows * (seg + 1)) / a.nseg);
         const int r0 = i_start - 2, r_last = i_end + 1;  // stencil rows
         const int m0 = i_start - 1, m_last = i_end - 1;  // metric rows
         constexpr unsigned ROWB = WROW * 8u;
@@ -643,7 +644,7 @@ __global__ void __launch_bounds__(NT, SFV_MINB) stage_kernel(const __grid_consta
         if (t < 8) {
             double x = red[t * WPC];
             for (int w = 1; w < WPC; ++w) x = t < 4 ? x + red[t * WPC + w] : fmax(x, red[t * WPC + w]);
-            a.partials[(size_t)t * gridDim.x + blockIdx.x] = x;
+            a.partials[(size_t)t * a.part_stride + a.part_base + blockIdx.x] = x;
         }
     }
 }

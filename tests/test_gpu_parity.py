@@ -328,3 +328,43 @@ def test_c3_full_size_windows(sfv_mod, oracle_mod):
         Uo = o.get_state()[j0 - jlo:j1 - jlo, i0 - ilo:i1 - ilo]
         e = state_error(Ug[j0:j1, i0:i1], Uo)
         assert np.all(e <= 1e-12), ((i0, i1, j0, j1), e)
+
+
+def test_overlap_split_bitwise(sfv_mod):
+    """The edge-rows / interior split with the row exchange on a separate
+    stream gives bit-identical results to the unsplit
+    sequence (SFV_OVERLAP=0), and to the single-block run."""
+    import os
+    ni, nj = 160, 60
+    X, Y = I.ramp_nodes(ni, nj, 30.0)
+    cfg = I.default_config(ni, nj)
+    U0 = I.perturbed_state(ni, nj, 12)
+    out = {}
+    for ov in ("1", "0"):
+        os.environ["SFV_OVERLAP"] = ov
+        try:
+            g = sfv_mod.Solver(cfg, X, Y, px=4, py=2)
+        finally:
+            del os.environ["SFV_OVERLAP"]
+        g.set_state(U0); g.step(25); g.sync()
+        out[ov] = (g.get_state(), g.dt(), g.residual_norms())
+    g1 = sfv_mod.Solver(cfg, X, Y)
+    g1.set_state(U0); g1.step(25); g1.sync()
+    np.testing.assert_array_equal(out["1"][0], out["0"][0])
+    np.testing.assert_array_equal(out["1"][0], g1.get_state())
+    np.testing.assert_array_equal(out["1"][1], g1.dt())
+    assert norm_error(out["1"][2], g1.residual_norms()) < 1e-14
+
+
+def test_c2_eight_slab_loopback(sfv_mod, oracle_mod):
+    """C2 in 8 slabs (the 8-GPU slab layout of PAPER.md:174) on one device:
+    bitwise equal to the single block, and oracle parity after 3 steps."""
+    X, Y = I.config_nodes("C2")
+    c = I.CONFIGS["C2"]
+    cfg = I.default_config(c["ni"], c["nj"])
+    U0 = I.perturbed_state(c["ni"], c["nj"], 2)
+    g8 = sfv_mod.Solver(cfg, X, Y, px=8)
+    g8.set_state(U0); g8.step(3); g8.sync()
+    g1, o = run_pair(sfv_mod, oracle_mod, cfg, X, Y, U0, 3)
+    np.testing.assert_array_equal(g8.get_state(), g1.get_state())
+    check(g8, o, 1e-12)
