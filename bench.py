@@ -199,6 +199,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=50)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="C2", choices=["C2", "C3", "C4"])
+    ap.add_argument("--rk", default="rk4", choices=["rk4", "heun", "jst4"],
+                    help="RK tableau (reading A-R5; SURVEY §8(f) f1: per-substep cost RK2 vs RK4, PAPER.md:276)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     args = ap.parse_args()
@@ -226,7 +228,8 @@ def main():
 
     ni, nj, theta, desc, scaling, px = workload(args.workload, n_gpus)
     X, Y = I.ramp_nodes(ni, nj, theta)
-    cfg = I.default_config(ni, nj, max_history=max(args.steps + args.warmup + 16, 64))
+    rk = {"rk4": I.RK4_CLASSIC, "heun": I.RK2_HEUN, "jst4": I.RK4_JAMESON}[args.rk]
+    cfg = I.default_config(ni, nj, rk=rk, max_history=max(args.steps + args.warmup + 16, 64))
     U0 = I.uniform_state(ni, nj)
     nccl_id = None
     if world > 1:
@@ -256,15 +259,20 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms_max = float(t.item())
     cells_total = ni * nj
-    stages = 4
+    stages = I.RK_STAGES[rk]
     value = cells_total * stages * args.steps / (ms_max * 1e-3) / 1e6
     cells_rank = cells_total // world
-    launches = stages * args.steps
+    # our kernels per step: the stage kernels (plus 1-2 two-row edge launches per
+    # stage on a rank with neighbours, overlap split) and one finalize kernel
+    edges = (rank > 0) + (rank < world - 1) if world > 1 else 0
+    launches = (stages * (1 + edges) + 1) * args.steps
+    stage_launches = stages * args.steps
 
     # ---- roofline of the dominant kernel (the fused stage kernel) ----
-    # Every launch in the step is a stage kernel (4 per RK4 step, nothing else
-    # at N = 1), so the average launch duration is the timed region / launches.
-    avg_launch_s = ms_max * 1e-3 / launches
+    # At N = 1 a step is the stage kernels plus one tiny finalize kernel, so the
+    # timed region / stage launches is a (slightly conservative) average
+    # stage-kernel duration.
+    avg_launch_s = ms_max * 1e-3 / stage_launches
     alg_bytes = ALG_BYTES_PER_CELL_STAGE * cells_rank
     hbm_achieved = alg_bytes / avg_launch_s / 1e9
     peak, peak_src = measured_peak()
@@ -319,7 +327,7 @@ def main():
                 "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
                 "scaling": scaling, "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded inputs)",
                 "config": {"workload": desc, "global_cells": cells_total, "cells_per_gpu": cells_rank,
-                           "rk_stages": stages, "parallelism": f"slab{px}x1",
+                           "rk_stages": stages, "rk": args.rk, "parallelism": f"slab{px}x1",
                            "l2": f"no flush: working set {solver.ws.numel() / 1e6:.0f} MB per GPU vs 126 MB L2",
                            "launch": li,
                            "mcell_steps_per_s": value / stages,
