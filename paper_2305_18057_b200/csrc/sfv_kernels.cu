@@ -276,9 +276,9 @@ struct StageTraits {
     static constexpr int NPW = MODE == M_OWN ? 0 : (MODE == M_RK4F ? 3 : 1);
     static constexpr int W_SLOT = 4 * WROW;           // stencil ring: 4 rows (v..v+2 + 1 in flight), 1152 B
     static constexpr int M_SLOT = 256;                // metrics ring: 2 rows (v + 1 in flight), 7*288 B -> 2 KB
-    static constexpr int P_SLOT = 4 * NPW * WROW;     // pointwise: row v
+    static constexpr int P_SLOT = 4 * NPW * WROW;     // pointwise ring: 2 rows (v + 1 in flight)
     static constexpr int X_SLOT = 8 * 32;             // lane exchange: north states [4][32], south fluxes [4][32]
-    static constexpr int WARP_DBL = 4 * W_SLOT + 2 * M_SLOT + P_SLOT + X_SLOT + 16;  // + 7 mbarriers, 128 B aligned
+    static constexpr int WARP_DBL = 4 * W_SLOT + 2 * M_SLOT + 2 * P_SLOT + X_SLOT + 16;  // + 8 mbarriers, 128 B aligned
 };
 
 template <int MODE>
@@ -303,11 +303,11 @@ __global__ void __launch_bounds__(NT, SFV_MINB) stage_kernel(const __grid_consta
     double *wbase = smem + warp * TR::WARP_DBL;
     double *wring = wbase;                      // [4][4][WROW]
     double *mring = wring + 4 * TR::W_SLOT;     // [2][7][WROW]
-    double *pring = mring + 2 * TR::M_SLOT;     // [4*NPW][WROW]
-    double *xch = pring + TR::P_SLOT;           // [8][32] lane exchange
+    double *pring = mring + 2 * TR::M_SLOT;     // [2][4*NPW][WROW]
+    double *xch = pring + 2 * TR::P_SLOT;       // [8][32] lane exchange
     uint64_t *wbar = reinterpret_cast<uint64_t *>(xch + TR::X_SLOT);   // [4]
     uint64_t *mbar = wbar + 4;                                           // [2]
-    uint64_t *pbar = mbar + 2;                                           // [1]
+    uint64_t *pbar = mbar + 2;                                           // [2]
     double *red = smem + WPC * TR::WARP_DBL;    // [8][WPC]
 
     const Params &P = a.P;
@@ -362,12 +362,14 @@ __global__ void __launch_bounds__(NT, SFV_MINB) stage_kernel(const __grid_consta
             elect_issue_s(mring_s + s * (TR::M_SLOT * 8u), &a.tm_met, tx, (r + 1) * NMET, mbar_s + 8u * s,
                           (unsigned)NMET * ROWB);
         };
-        auto issue_p = [&](int r) {
+        auto issue_p = [&](int r) {  // pointwise rows: ring of 2, slot (r - i_start) & 1
             if constexpr (TR::NPW > 0) {
-                elect_issue_s(pring_s, &a.tm_pw[0], tx, (r + 2) * 4, pbar_s, 4u * TR::NPW * ROWB);
+                const unsigned s = (unsigned)(r - i_start) & 1u;
+                const unsigned dst = pring_s + s * (TR::P_SLOT * 8u), bar = pbar_s + 8u * s;
+                elect_issue_s(dst, &a.tm_pw[0], tx, (r + 2) * 4, bar, 4u * TR::NPW * ROWB);
 #pragma unroll
                 for (int p = 1; p < TR::NPW; ++p)
-                    elect_tma_s(pring_s + p * (4u * WROW * 8u), &a.tm_pw[p], tx, (r + 2) * 4, pbar_s);
+                    elect_tma_s(dst + p * (4u * WROW * 8u), &a.tm_pw[p], tx, (r + 2) * 4, bar);
             }
         };
         auto wait_w = [&](int r) {
@@ -378,7 +380,7 @@ __global__ void __launch_bounds__(NT, SFV_MINB) stage_kernel(const __grid_consta
         };
 
         if (lane == 0) {
-            for (int s = 0; s < 7; ++s) mbar_init(&wbar[s], 1);
+            for (int s = 0; s < 8; ++s) mbar_init(&wbar[s], 1);
             asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         }
@@ -391,6 +393,7 @@ __global__ void __launch_bounds__(NT, SFV_MINB) stage_kernel(const __grid_consta
         pdl_launch_dependents();
         read_step();
         for (int r = r0; r <= r0 + 3 && r <= r_last; ++r) issue_w(r);
+        issue_p(i_start);
 
         double Wc[4], fp[4], QLp[4], GW[4];
         double nWx = 0.0, nWy = 0.0;             // i-face(0) normal (W-edge slip ghosts)
@@ -471,7 +474,7 @@ __global__ void __launch_bounds__(NT, SFV_MINB) stage_kernel(const __grid_consta
             // issued in the prologue)
             if (v + 3 >= r0 + 6 && v + 3 <= r_last) issue_w(v + 3);
             if (v + 1 <= m_last) issue_m(v + 1);
-            issue_p(v);
+            if (v + 1 < i_end) issue_p(v + 1);
             wait_m(v);
             const double *mv = mslot(v);
 #pragma unroll
@@ -489,7 +492,9 @@ __global__ void __launch_bounds__(NT, SFV_MINB) stage_kernel(const __grid_consta
             __syncwarp();
 #pragma unroll
             for (int c = 0; c < 4; ++c) GN[c] = xch[(4 + c) * 32 + (lane < 31 ? lane + 1 : 31)];
-            if constexpr (TR::NPW > 0) mbar_wait_s(pbar_s, (unsigned)((v - i_start) & 1));
+            const double *prow = pring + ((v - i_start) & 1) * TR::P_SLOT;
+            if constexpr (TR::NPW > 0)
+                mbar_wait_s(pbar_s + 8u * ((unsigned)(v - i_start) & 1u), (unsigned)(((v - i_start) >> 1) & 1));
             // ---- residual (Eq. 5) and stage update (Eq. 6): every lane computes,
             // output lanes store (no divergence in the common path)
             const double iV = mv[6 * WROW + own];
@@ -502,16 +507,16 @@ __global__ void __launch_bounds__(NT, SFV_MINB) stage_kernel(const __grid_consta
                 if constexpr (MODE == M_OWN) {
                     U[c] = fma(-coef, rv, Wv[c]);
                 } else if constexpr (MODE == M_UN) {
-                    U[c] = fma(-coef, rv, pring[c * WROW + own]);
+                    U[c] = fma(-coef, rv, prow[c * WROW + own]);
                 } else if constexpr (MODE == M_RK4F) {
-                    const double un = pring[c * WROW + own];
-                    const double d2 = pring[(4 + c) * WROW + own] - un;
-                    const double d3 = pring[(8 + c) * WROW + own] - un;
+                    const double un = prow[c * WROW + own];
+                    const double d2 = prow[(4 + c) * WROW + own] - un;
+                    const double d3 = prow[(8 + c) * WROW + own] - un;
                     const double d4 = Wv[c] - un;
                     const double comb = (fma(2.0, d3, d2) + d4) * (1.0 / 3.0);
                     U[c] = un + fma(-coef, rv, comb);
                 } else {  // M_HEUNF
-                    const double un = pring[c * WROW + own];
+                    const double un = prow[c * WROW + own];
                     U[c] = un + fma(-coef, rv, 0.5 * (Wv[c] - un));
                 }
             }
