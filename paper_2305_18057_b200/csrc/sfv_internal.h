@@ -23,7 +23,12 @@ constexpr int SMEM_ROW = 132;     // doubles per staged row in shared memory
 constexpr int ROW_COLS = 130;     // columns staged per row: j0-2 .. j0+127
 constexpr int NT = 32;            // threads per CTA of the stage kernel: one independent warp
 constexpr int WPC = NT / 32;      // independent warps per CTA
-constexpr int WOUT = 30;          // output columns per warp strip (+1 halo lane each side)
+#ifndef SFV_CPL
+#define SFV_CPL 1                 // columns per lane of the stage kernel
+#endif
+constexpr int CPL = SFV_CPL;
+constexpr int WOUT = 32 * CPL - 2;  // output columns per warp strip (+1 halo column each side)
+constexpr int WROW = 32 * CPL + 4;  // staged doubles per row: columns j0-2 .. j0+32*CPL+1
 
 
 enum Mode { M_OWN = 0, M_UN = 1, M_RK4F = 2, M_HEUNF = 3 };

@@ -269,13 +269,12 @@ __device__ __forceinline__ void store4(double *buf, int PJ, int i, int j, const 
 // j0-1+l) and marches along i over a segment of rows with its own TMA rings
 // and mbarriers.  j-face states / fluxes move between lanes by __shfl, so the
 // main loop has no CTA-wide barrier; warps drift independently.
-constexpr int WROW = 36;  // staged doubles per row: columns j0-2 .. j0+33 (288 B)
 
 template <int MODE>
 struct StageTraits {
     static constexpr int NPW = MODE == M_OWN ? 0 : (MODE == M_RK4F ? 3 : 1);
     static constexpr int W_SLOT = 4 * WROW;           // stencil ring: 4 rows (v..v+2 + 1 in flight), 1152 B
-    static constexpr int M_SLOT = 256;                // metrics ring: 2 rows (v + 1 in flight), 7*288 B -> 2 KB
+    static constexpr int M_SLOT = (NMET * WROW + 15) / 16 * 16;  // metrics ring: 2 rows (v + 1 in flight), 128 B aligned
     static constexpr int P_SLOT = 4 * NPW * WROW;     // pointwise ring: 2 rows (v + 1 in flight)
     static constexpr int X_SLOT = 8 * 32;             // lane exchange: north states [4][32], south fluxes [4][32]
     static constexpr int WARP_DBL = 4 * W_SLOT + 2 * M_SLOT + 2 * P_SLOT + X_SLOT + 16;  // + 8 mbarriers, 128 B aligned
@@ -287,7 +286,7 @@ __host__ __device__ constexpr size_t stage_smem() {
 }
 
 #ifndef SFV_MIN_WARPS
-#define SFV_MIN_WARPS 12  // resident warps per SM the register allocation targets (168 regs: no spills)
+#define SFV_MIN_WARPS (CPL == 1 ? 12 : 8)  // resident warps per SM the register allocation targets (no spills)
 #endif
 constexpr int SFV_MINB = SFV_MIN_WARPS / WPC;
 #ifndef SFV_UNROLL
@@ -331,10 +330,15 @@ __global__ void __launch_bounds__(NT, SFV_MINB) stage_kernel(const __grid_consta
         const int seg = task / a.nstrips;
         const int j0 = strip * WOUT;
         const int j1 = min(j0 + WOUT, a.nj);
-        const int jc = j0 - 1 + lane;                // this lane's column
-        const bool is_out = (lane >= 1) && (jc < j1);
-        const bool jflux = (lane >= 1) && (jc <= j1);
-        const int own = lane + 1;                    // column index in a staged row
+        const int jc = j0 - 1 + CPL * lane;          // this lane's first column (CPL columns per lane)
+        const int own = CPL * lane + 1;              // its index in a staged row
+        bool is_out[CPL], jflux[CPL];                // owns output cell / its j-face is needed
+#pragma unroll
+        for (int k = 0; k < CPL; ++k) {
+            const int col = jc + k;
+            is_out[k] = col >= j0 && col < j1;
+            jflux[k] = col >= j0 && col <= j1;
+        }
         auto writes_ghost = [&](int e) { return a.bc[e] == E_SLIP || a.bc[e] == E_OUTFLOW; };
         const bool ghost_sn = (writes_ghost(2) && j0 == 0) || (writes_ghost(3) && j1 >= a.nj - 1);
         const bool ghost_w = writes_ghost(0), ghost_e = writes_ghost(1);
@@ -395,25 +399,27 @@ __global__ void __launch_bounds__(NT, SFV_MINB) stage_kernel(const __grid_consta
         for (int r = r0; r <= r0 + 3 && r <= r_last; ++r) issue_w(r);
         issue_p(i_start);
 
-        double Wc[4], fp[4], QLp[4], GW[4];
-        double nWx = 0.0, nWy = 0.0;             // i-face(0) normal (W-edge slip ghosts)
-        double wfx = 0.0, wfy = 0.0, wfA = 0.0;  // west face of the current row (dt)
-
         // ---- peeled prologue: rows i_start-2, i_start-1 (i direction only) ---
+        double Wc[CPL][4], fp[CPL][4], QLp[CPL][4], GW[CPL][4];
+        double nWx[CPL], nWy[CPL];            // i-face(0) normal (W-edge slip ghosts)
+        double wfx[CPL], wfy[CPL], wfA[CPL];  // west face of the current row (dt)
         wait_w(r0);
         wait_w(r0 + 1);
         wait_w(r0 + 2);
         {
             const double *s0 = wslot(r0), *s1 = wslot(r0 + 1), *s2 = wslot(r0 + 2);
 #pragma unroll
-            for (int c = 0; c < 4; ++c) {
-                const double w0 = s0[c * WROW + own], w1 = s1[c * WROW + own], w2 = s2[c * WROW + own];
-                double qU, qD;
-                muscl_cell<FAST>(w1, w1 - w0, w2 - w1, P, qU, qD);  // cell i_start-1
-                QLp[c] = qU;
-                fp[c] = w2 - w1;
-                Wc[c] = w2;
-            }
+            for (int k = 0; k < CPL; ++k)
+#pragma unroll
+                for (int c = 0; c < 4; ++c) {
+                    const int o = own + k;
+                    const double w0 = s0[c * WROW + o], w1 = s1[c * WROW + o], w2 = s2[c * WROW + o];
+                    double qU, qD;
+                    muscl_cell<FAST>(w1, w1 - w0, w2 - w1, P, qU, qD);  // cell i_start-1
+                    QLp[k][c] = qU;
+                    fp[k][c] = w2 - w1;
+                    Wc[k][c] = w2;
+                }
         }
         __syncwarp();  // rows r0, r0+1 consumed
         for (int r = r0 + 4; r <= r0 + 5 && r <= r_last; ++r) issue_w(r);
@@ -422,23 +428,28 @@ __global__ void __launch_bounds__(NT, SFV_MINB) stage_kernel(const __grid_consta
         {
             const double *s3 = wslot(r0 + 3);
             const double *m = mslot(m0);
-            double qU[4], qD[4];
 #pragma unroll
-            for (int c = 0; c < 4; ++c) {
-                const double wn = s3[c * WROW + own];
-                const double f = wn - Wc[c];
-                muscl_cell<FAST>(Wc[c], fp[c], f, P, qU[c], qD[c]);  // cell i_start
-                fp[c] = f;
-                Wc[c] = wn;
+            for (int k = 0; k < CPL; ++k) {
+                const int o = own + k;
+                double qU[4], qD[4];
+#pragma unroll
+                for (int c = 0; c < 4; ++c) {
+                    const double wn = s3[c * WROW + o];
+                    const double f = wn - Wc[k][c];
+                    muscl_cell<FAST>(Wc[k][c], fp[k][c], f, P, qU[c], qD[c]);  // cell i_start
+                    fp[k][c] = f;
+                    Wc[k][c] = wn;
+                }
+                const double nx = m[0 * WROW + o], ny = m[1 * WROW + o], A = m[2 * WROW + o];
+                const bool ok = roe_flux(QLp[k], qD, nx, ny, A, P, GW[k]);
+                if (!ok && is_out[k])
+                    atomicMin(a.err,
+                              err_key(n, a.nstages, a.stage, 0, (long long)(a.gj0 + jc + k) * a.NI + a.gi0 + i_start));
+                nWx[k] = nx; nWy[k] = ny;
+                wfx[k] = nx; wfy[k] = ny; wfA[k] = A;
+#pragma unroll
+                for (int c = 0; c < 4; ++c) QLp[k][c] = qU[c];
             }
-            const double nx = m[0 * WROW + own], ny = m[1 * WROW + own], A = m[2 * WROW + own];
-            const bool ok = roe_flux(QLp, qD, nx, ny, A, P, GW);
-            if (!ok && is_out)
-                atomicMin(a.err, err_key(n, a.nstages, a.stage, 0, (long long)(a.gj0 + jc) * a.NI + a.gi0 + i_start));
-            nWx = nx; nWy = ny;
-            wfx = nx; wfy = ny; wfA = A;
-#pragma unroll
-            for (int c = 0; c < 4; ++c) QLp[c] = qU[c];
         }
 
         // ---- main loop: one output row per iteration ---------------------------
@@ -446,27 +457,37 @@ __global__ void __launch_bounds__(NT, SFV_MINB) stage_kernel(const __grid_consta
 #pragma unroll kRowUnroll
         for (int v = i_start; v < i_end; ++v) {
             wait_w(v + 2);
-            double qD[4], qU[4], qS[4], qN[4], Wv[4];
+            double qD[CPL][4], qU[CPL][4], qS[CPL][4], qN[CPL][4], Wv[CPL][4];
             {
                 const double *sn = wslot(v + 2);
-#pragma unroll
-                for (int c = 0; c < 4; ++c) {  // i: reconstruct cell v+1
-                    const double wn = sn[c * WROW + own];
-                    const double f = wn - Wc[c];
-                    muscl_cell<FAST>(Wc[c], fp[c], f, P, qU[c], qD[c]);
-                    fp[c] = f;
-                    Wc[c] = wn;
-                }
                 const double *sv = wslot(v);
 #pragma unroll
-                for (int c = 0; c < 4; ++c) {  // j: reconstruct cell (v, jc)
-                    const double wm = sv[c * WROW + own - 1];
-                    const double w = sv[c * WROW + own];
-                    const double wp = sv[c * WROW + own + 1];
-                    double qn;
-                    muscl_cell<FAST>(w, w - wm, wp - w, P, qn, qS[c]);
-                    xch[c * 32 + lane] = qn;  // north state, read by the lane above
-                    Wv[c] = w;
+                for (int k = 0; k < CPL; ++k)
+#pragma unroll
+                    for (int c = 0; c < 4; ++c) {  // i: reconstruct cell (v+1, column k)
+                        const double wn = sn[c * WROW + own + k];
+                        const double f = wn - Wc[k][c];
+                        muscl_cell<FAST>(Wc[k][c], fp[k][c], f, P, qU[k][c], qD[k][c]);
+                        fp[k][c] = f;
+                        Wc[k][c] = wn;
+                    }
+                double qNup[CPL][4];
+#pragma unroll
+                for (int k = 0; k < CPL; ++k)
+#pragma unroll
+                    for (int c = 0; c < 4; ++c) {  // j: reconstruct cell (v, column k)
+                        const int o = own + k;
+                        const double wm = sv[c * WROW + o - 1];
+                        const double w = sv[c * WROW + o];
+                        const double wp = sv[c * WROW + o + 1];
+                        muscl_cell<FAST>(w, w - wm, wp - w, P, qNup[k][c], qS[k][c]);
+                        Wv[k][c] = w;
+                    }
+#pragma unroll
+                for (int c = 0; c < 4; ++c) {
+                    xch[c * 32 + lane] = qNup[CPL - 1][c];  // north state of the last column, read by the lane above
+#pragma unroll
+                    for (int k = 1; k < CPL; ++k) qN[k][c] = qNup[k - 1][c];
                 }
             }
             __syncwarp();  // stencil row v-1, metric row v-1, pointwise slot consumed
@@ -478,144 +499,166 @@ __global__ void __launch_bounds__(NT, SFV_MINB) stage_kernel(const __grid_consta
             wait_m(v);
             const double *mv = mslot(v);
 #pragma unroll
-            for (int c = 0; c < 4; ++c) qN[c] = xch[c * 32 + (lane > 0 ? lane - 1 : 0)];
-            double GE[4], GS[4];
-            // both face fluxes of this row: two independent Roe evaluations
-            const bool okE = roe_flux(QLp, qD, mv[0 * WROW + own], mv[1 * WROW + own], mv[2 * WROW + own], P, GE);
-            const bool okS = roe_flux(qN, qS, mv[3 * WROW + own], mv[4 * WROW + own], mv[5 * WROW + own], P, GS);
-            double GN[4];
+            for (int c = 0; c < 4; ++c) qN[0][c] = xch[c * 32 + (lane > 0 ? lane - 1 : 0)];
+            double GE[CPL][4], GS[CPL][4];
+            bool okE[CPL], okS[CPL];
+            // all face fluxes of this row: 2 x CPL independent Roe evaluations
+#pragma unroll
+            for (int k = 0; k < CPL; ++k) {
+                const int o = own + k;
+                okE[k] = roe_flux(QLp[k], qD[k], mv[0 * WROW + o], mv[1 * WROW + o], mv[2 * WROW + o], P, GE[k]);
+                okS[k] = roe_flux(qN[k], qS[k], mv[3 * WROW + o], mv[4 * WROW + o], mv[5 * WROW + o], P, GS[k]);
+            }
+            double GN[CPL][4];
 #pragma unroll
             for (int c = 0; c < 4; ++c) {
-                QLp[c] = qU[c];
-                xch[(4 + c) * 32 + lane] = GS[c];  // south flux = north flux of the lane below
+#pragma unroll
+                for (int k = 0; k < CPL; ++k) QLp[k][c] = qU[k][c];
+                xch[(4 + c) * 32 + lane] = GS[0][c];  // south flux of column 0 = north flux of the lane below
+#pragma unroll
+                for (int k = 0; k + 1 < CPL; ++k) GN[k][c] = GS[k + 1][c];
             }
             __syncwarp();
 #pragma unroll
-            for (int c = 0; c < 4; ++c) GN[c] = xch[(4 + c) * 32 + (lane < 31 ? lane + 1 : 31)];
+            for (int c = 0; c < 4; ++c) GN[CPL - 1][c] = xch[(4 + c) * 32 + (lane < 31 ? lane + 1 : 31)];
             const double *prow = pring + ((v - i_start) & 1) * TR::P_SLOT;
             if constexpr (TR::NPW > 0)
                 mbar_wait_s(pbar_s + 8u * ((unsigned)(v - i_start) & 1u), (unsigned)(((v - i_start) >> 1) & 1));
-            // ---- residual (Eq. 5) and stage update (Eq. 6): every lane computes,
-            // output lanes store (no divergence in the common path)
-            const double iV = mv[6 * WROW + own];
-            double R[4], U[4];
+            bool bad = false;
 #pragma unroll
-            for (int c = 0; c < 4; ++c) R[c] = ((GE[c] - GW[c]) + GN[c]) - GS[c];
+            for (int k = 0; k < CPL; ++k) {
+                const int o = own + k;
+                // ---- residual (Eq. 5) and stage update (Eq. 6): every lane computes,
+                // output lanes store (no divergence in the common path)
+                const double iV = mv[6 * WROW + o];
+                double R[4], U[4];
 #pragma unroll
-            for (int c = 0; c < 4; ++c) {
-                const double rv = R[c] * iV;
-                if constexpr (MODE == M_OWN) {
-                    U[c] = fma(-coef, rv, Wv[c]);
-                } else if constexpr (MODE == M_UN) {
-                    U[c] = fma(-coef, rv, prow[c * WROW + own]);
-                } else if constexpr (MODE == M_RK4F) {
-                    const double un = prow[c * WROW + own];
-                    const double d2 = prow[(4 + c) * WROW + own] - un;
-                    const double d3 = prow[(8 + c) * WROW + own] - un;
-                    const double d4 = Wv[c] - un;
-                    const double comb = (fma(2.0, d3, d2) + d4) * (1.0 / 3.0);
-                    U[c] = un + fma(-coef, rv, comb);
-                } else {  // M_HEUNF
-                    const double un = prow[c * WROW + own];
-                    U[c] = un + fma(-coef, rv, 0.5 * (Wv[c] - un));
-                }
-            }
-            if (is_out) {
-#pragma unroll
-                for (int c = 0; c < 4; ++c) outp[(size_t)c * PJ] = U[c];
-            }
-            outp += (size_t)4 * PJ;
-            // new-state validity: rho > 0 and 2 rho E > |m|^2 (<=> p > 0)
-            const bool st_ok = (U[0] > 0.0) & (2.0 * U[0] * U[3] > fma(U[1], U[1], U[2] * U[2]));
-            // rare path behind one warp vote: invalid face or new states (reading A-R28)
-            if (__any_sync(0xffffffffu, (is_out & (!okE | !st_ok)) | (jflux & !okS))) {
-                if (is_out && !okE) {
-                    int I = a.gi0 + v + 1;
-                    if (I > a.NI - 1) I = a.NI - 1;
-                    atomicMin(a.err, err_key(n, a.nstages, a.stage, 0, (long long)(a.gj0 + jc) * a.NI + I));
-                }
-                if (jflux && !okS) {
-                    int J = a.gj0 + jc;
-                    if (J > a.NJ - 1) J = a.NJ - 1;
-                    atomicMin(a.err, err_key(n, a.nstages, a.stage, 0, (long long)J * a.NI + a.gi0 + v));
-                }
-                if (is_out && !st_ok)
-                    atomicMin(a.err, err_key(n, a.nstages, a.stage, 1, (long long)(a.gj0 + jc) * a.NI + a.gi0 + v));
-            }
-            // physical-boundary ghosts of the new state (reading A-R11), behind one
-            // warp-uniform test: only strips at the S / N walls and rows 0, 1, ni-2, ni-1
-            if ((ghost_sn || (ghost_w && v <= 1) || (ghost_e && v >= a.ni - 2)) && is_out) {
-                if (a.bc[2] == E_SLIP && jc <= 1) {
-                    double g[4];
-                    const int k0 = own - jc;  // column 0
-                    mirror(U, mv[3 * WROW + k0], mv[4 * WROW + k0], g);
-                    store4(a.out, PJ, v, -1 - jc, g);
-                } else if (a.bc[2] == E_OUTFLOW && jc == 0) {
-                    store4(a.out, PJ, v, -1, U);
-                    store4(a.out, PJ, v, -2, U);
-                }
-                if (a.bc[3] == E_SLIP && jc >= a.nj - 2) {
-                    double g[4];
-                    const int kN = own + (a.nj - jc);  // column nj
-                    mirror(U, mv[3 * WROW + kN], mv[4 * WROW + kN], g);
-                    store4(a.out, PJ, v, a.nj + (a.nj - 1 - jc), g);
-                } else if (a.bc[3] == E_OUTFLOW && jc == a.nj - 1) {
-                    store4(a.out, PJ, v, a.nj, U);
-                    store4(a.out, PJ, v, a.nj + 1, U);
-                }
-                if (a.bc[0] == E_SLIP && v <= 1) {  // segments start at 0 or >= 4 (choose_launch)
-                    double g[4];
-                    mirror(U, nWx, nWy, g);
-                    store4(a.out, PJ, -1 - v, jc, g);
-                } else if (a.bc[0] == E_OUTFLOW && v == 0) {
-                    store4(a.out, PJ, -1, jc, U);
-                    store4(a.out, PJ, -2, jc, U);
-                }
-                if (a.bc[1] == E_SLIP && v >= a.ni - 2) {
-                    double g[4];
-                    wait_m(a.ni - 1);  // i-face(ni) lives in metric row ni-1 (issued: <= v+1)
-                    const double *mE = mslot(a.ni - 1);
-                    mirror(U, mE[0 * WROW + own], mE[1 * WROW + own], g);
-                    store4(a.out, PJ, a.ni + (a.ni - 1 - v), jc, g);
-                } else if (a.bc[1] == E_OUTFLOW && v == a.ni - 1) {
-                    store4(a.out, PJ, a.ni, jc, U);
-                    store4(a.out, PJ, a.ni + 1, jc, U);
-                }
-            }
-            if constexpr (NORMS) {
+                for (int c = 0; c < 4; ++c) R[c] = ((GE[k][c] - GW[k][c]) + GN[k][c]) - GS[k][c];
 #pragma unroll
                 for (int c = 0; c < 4; ++c) {
-                    nrm[c] = is_out ? fma(R[c], R[c], nrm[c]) : nrm[c];
-                    nrm[4 + c] = is_out ? fmax(nrm[4 + c], fabs(R[c])) : nrm[4 + c];
+                    const double rv = R[c] * iV;
+                    if constexpr (MODE == M_OWN) {
+                        U[c] = fma(-coef, rv, Wv[k][c]);
+                    } else if constexpr (MODE == M_UN) {
+                        U[c] = fma(-coef, rv, prow[c * WROW + o]);
+                    } else if constexpr (MODE == M_RK4F) {
+                        const double un = prow[c * WROW + o];
+                        const double d2 = prow[(4 + c) * WROW + o] - un;
+                        const double d3 = prow[(8 + c) * WROW + o] - un;
+                        const double d4 = Wv[k][c] - un;
+                        const double comb = (fma(2.0, d3, d2) + d4) * (1.0 / 3.0);
+                        U[c] = un + fma(-coef, rv, comb);
+                    } else {  // M_HEUNF
+                        const double un = prow[c * WROW + o];
+                        U[c] = un + fma(-coef, rv, 0.5 * (Wv[k][c] - un));
+                    }
+                }
+                if (is_out[k]) {
+#pragma unroll
+                    for (int c = 0; c < 4; ++c) outp[(size_t)c * PJ + k] = U[c];
+                }
+                // new-state validity: rho > 0 and 2 rho E > |m|^2 (<=> p > 0)
+                const bool st_ok = (U[0] > 0.0) & (2.0 * U[0] * U[3] > fma(U[1], U[1], U[2] * U[2]));
+                const int jk = jc + k;
+                bad |= (is_out[k] & (!okE[k] | !st_ok)) | (jflux[k] & !okS[k]);
+                // physical-boundary ghosts of the new state (reading A-R11), behind one
+                // warp-uniform test: only strips at the S / N walls and rows 0, 1, ni-2, ni-1
+                if ((ghost_sn || (ghost_w && v <= 1) || (ghost_e && v >= a.ni - 2)) && is_out[k]) {
+                    if (a.bc[2] == E_SLIP && jk <= 1) {
+                        double g[4];
+                        const int k0 = o - jk;  // column 0
+                        mirror(U, mv[3 * WROW + k0], mv[4 * WROW + k0], g);
+                        store4(a.out, PJ, v, -1 - jk, g);
+                    } else if (a.bc[2] == E_OUTFLOW && jk == 0) {
+                        store4(a.out, PJ, v, -1, U);
+                        store4(a.out, PJ, v, -2, U);
+                    }
+                    if (a.bc[3] == E_SLIP && jk >= a.nj - 2) {
+                        double g[4];
+                        const int kN = o + (a.nj - jk);  // column nj
+                        mirror(U, mv[3 * WROW + kN], mv[4 * WROW + kN], g);
+                        store4(a.out, PJ, v, a.nj + (a.nj - 1 - jk), g);
+                    } else if (a.bc[3] == E_OUTFLOW && jk == a.nj - 1) {
+                        store4(a.out, PJ, v, a.nj, U);
+                        store4(a.out, PJ, v, a.nj + 1, U);
+                    }
+                    if (a.bc[0] == E_SLIP && v <= 1) {  // segments start at 0 or >= 4 (choose_launch)
+                        double g[4];
+                        mirror(U, nWx[k], nWy[k], g);
+                        store4(a.out, PJ, -1 - v, jk, g);
+                    } else if (a.bc[0] == E_OUTFLOW && v == 0) {
+                        store4(a.out, PJ, -1, jk, U);
+                        store4(a.out, PJ, -2, jk, U);
+                    }
+                    if (a.bc[1] == E_SLIP && v >= a.ni - 2) {
+                        double g[4];
+                        wait_m(a.ni - 1);  // i-face(ni) lives in metric row ni-1 (issued: <= v+1)
+                        const double *mE = mslot(a.ni - 1);
+                        mirror(U, mE[0 * WROW + o], mE[1 * WROW + o], g);
+                        store4(a.out, PJ, a.ni + (a.ni - 1 - v), jk, g);
+                    } else if (a.bc[1] == E_OUTFLOW && v == a.ni - 1) {
+                        store4(a.out, PJ, a.ni, jk, U);
+                        store4(a.out, PJ, a.ni + 1, jk, U);
+                    }
+                }
+                if constexpr (NORMS) {
+#pragma unroll
+                    for (int c = 0; c < 4; ++c) {
+                        nrm[c] = is_out[k] ? fma(R[c], R[c], nrm[c]) : nrm[c];
+                        nrm[4 + c] = is_out[k] ? fmax(nrm[4 + c], fabs(R[c])) : nrm[4 + c];
+                    }
+                }
+                if constexpr (DTMAX) {
+                    // sigma/V of the new state for dt_{n+1} (reading A-R6)
+                    const double ir = frcp(U[0]);
+                    const double u = U[1] * ir, vv = U[2] * ir;
+                    const double p = P.gm1 * fma(-0.5, fma(U[1], u, U[2] * vv), U[3]);
+                    const double x = P.gamma * p * ir;
+                    const double snd = x * frsqrt(x);
+                    const double tW = (fabs(fma(u, wfx[k], vv * wfy[k])) + snd) * wfA[k];
+                    const double tE =
+                        (fabs(fma(u, mv[0 * WROW + o], vv * mv[1 * WROW + o])) + snd) * mv[2 * WROW + o];
+                    const double tS =
+                        (fabs(fma(u, mv[3 * WROW + o], vv * mv[4 * WROW + o])) + snd) * mv[5 * WROW + o];
+                    const double tN = (fabs(fma(u, mv[3 * WROW + o + 1], vv * mv[4 * WROW + o + 1])) + snd) *
+                                      mv[5 * WROW + o + 1];
+                    const double sv = (((tW + tE) + tS) + tN) * iV;
+                    smax = (is_out[k] && sv > smax) ? sv : smax;
+                    wfx[k] = mv[0 * WROW + o];
+                    wfy[k] = mv[1 * WROW + o];
+                    wfA[k] = mv[2 * WROW + o];
+                }
+#pragma unroll
+                for (int c = 0; c < 4; ++c) GW[k][c] = GE[k][c];
+            }
+            outp += (size_t)4 * PJ;
+            // rare path behind one warp vote: invalid face or new states (reading A-R28)
+            if (__any_sync(0xffffffffu, bad)) {
+#pragma unroll
+                for (int k = 0; k < CPL; ++k) {
+                    const int jk = jc + k;
+                    if (is_out[k] && !okE[k]) {
+                        int I = a.gi0 + v + 1;
+                        if (I > a.NI - 1) I = a.NI - 1;
+                        atomicMin(a.err, err_key(n, a.nstages, a.stage, 0, (long long)(a.gj0 + jk) * a.NI + I));
+                    }
+                    if (jflux[k] && !okS[k]) {
+                        int J = a.gj0 + jk;
+                        if (J > a.NJ - 1) J = a.NJ - 1;
+                        atomicMin(a.err, err_key(n, a.nstages, a.stage, 0, (long long)J * a.NI + a.gi0 + v));
+                    }
+                    if (is_out[k]) {
+                        const double *pr = outp - (size_t)4 * PJ;  // the row just stored
+                        const double u0 = pr[k], u3 = pr[(size_t)3 * PJ + k];
+                        const double u1 = pr[(size_t)PJ + k], u2 = pr[(size_t)2 * PJ + k];
+                        if (!((u0 > 0.0) & (2.0 * u0 * u3 > fma(u1, u1, u2 * u2))))
+                            atomicMin(a.err,
+                                      err_key(n, a.nstages, a.stage, 1, (long long)(a.gj0 + jk) * a.NI + a.gi0 + v));
+                    }
                 }
             }
-            if constexpr (DTMAX) {
-                // sigma/V of the new state for dt_{n+1} (reading A-R6)
-                const double ir = frcp(U[0]);
-                const double u = U[1] * ir, vv = U[2] * ir;
-                const double p = P.gm1 * fma(-0.5, fma(U[1], u, U[2] * vv), U[3]);
-                const double x = P.gamma * p * ir;
-                const double snd = x * frsqrt(x);
-                const double tW = (fabs(fma(u, wfx, vv * wfy)) + snd) * wfA;
-                const double tE =
-                    (fabs(fma(u, mv[0 * WROW + own], vv * mv[1 * WROW + own])) + snd) * mv[2 * WROW + own];
-                const double tS =
-                    (fabs(fma(u, mv[3 * WROW + own], vv * mv[4 * WROW + own])) + snd) * mv[5 * WROW + own];
-                const double tN = (fabs(fma(u, mv[3 * WROW + own + 1], vv * mv[4 * WROW + own + 1])) + snd) *
-                                  mv[5 * WROW + own + 1];
-                const double sv = (((tW + tE) + tS) + tN) * iV;
-                smax = (is_out && sv > smax) ? sv : smax;
-            }
-            if constexpr (DTMAX) {
-                wfx = mv[0 * WROW + own];
-                wfy = mv[1 * WROW + own];
-                wfA = mv[2 * WROW + own];
-            }
-#pragma unroll
-            for (int c = 0; c < 4; ++c) GW[c] = GE[c];
         }
     }
-
     else {
         pdl_wait();
         pdl_launch_dependents();
