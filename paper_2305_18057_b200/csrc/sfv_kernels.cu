@@ -701,13 +701,15 @@ __global__ void __launch_bounds__(NT, SFV_MINB) stage_kernel(const __grid_consta
 // norm partials into the history ("residual print"; reading
 // A-R20); the lead block records dt_n and clears the sigma slot the last
 // stage will fill; the last block advances the step counter.
-constexpr int FIN_T = 512;
+constexpr int FIN_T = 256;
 __global__ void __launch_bounds__(FIN_T) finalize_kernel(FinalizeArgs f) {
-    __shared__ double tree[8][FIN_T];
-    const int t = threadIdx.x;
+    __shared__ double part[8][FIN_T / 32];
+    const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
     pdl_wait();
     pdl_launch_dependents();
     const long long n = *f.step_ctr;
+    // fixed assignment (thread t: partials t, t+256, ...) and fixed-order
+    // shuffle / warp trees: deterministic for a given launch geometry
     double acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     for (int b = t; b < f.ncta; b += FIN_T) {
 #pragma unroll
@@ -717,16 +719,20 @@ __global__ void __launch_bounds__(FIN_T) finalize_kernel(FinalizeArgs f) {
         }
     }
 #pragma unroll
-    for (int q = 0; q < 8; ++q) tree[q][t] = acc[q];
-    __syncthreads();
-    for (int s = FIN_T / 2; s > 0; s >>= 1) {
-        if (t < s) {
-#pragma unroll
-            for (int q = 0; q < 8; ++q) tree[q][t] = q < 4 ? tree[q][t] + tree[q][t + s] : fmax(tree[q][t], tree[q][t + s]);
+    for (int q = 0; q < 8; ++q) {
+        double x = acc[q];
+        for (int o = 16; o > 0; o >>= 1) {
+            const double y = __shfl_xor_sync(0xffffffffu, x, o);
+            x = q < 4 ? x + y : fmax(x, y);
         }
-        __syncthreads();
+        if (lane == 0) part[q][warp] = x;
     }
-    if (t < 8) f.norm_hist[((size_t)(n % f.cap) * f.nblocks + f.block_id) * 8 + t] = tree[t][0];
+    __syncthreads();
+    if (t < 8) {
+        double x = part[t][0];
+        for (int w = 1; w < FIN_T / 32; ++w) x = t < 4 ? x + part[t][w] : fmax(x, part[t][w]);
+        f.norm_hist[((size_t)(n % f.cap) * f.nblocks + f.block_id) * 8 + t] = x;
+    }
     if (t == 0) {
         if (f.lead) {
             f.dt_hist[n % f.cap] = f.dt_fixed > 0.0 ? f.dt_fixed : f.cfl / f.sig[n & 1];
