@@ -908,11 +908,14 @@ sfv_status sfv_get_residual_norms(sfv_ctx *c, int64_t first, int64_t count, doub
     const int nb = c->nblocks_total;
     const long long cap = c->cfg.max_history;
     std::vector<double> h((size_t)count * nb * 8);
-    // per step: nb x 8 partials (sum of squares, max |R|)
-    for (long long q = 0; q < count; ++q) {
+    // per step: nb x 8 partials (sum of squares, max |R|); the ring is copied in
+    // at most two contiguous pieces
+    for (long long q = 0; q < count;) {
         const long long slot = (first + q) % cap;
-        CK(cudaMemcpy(h.data() + (size_t)q * nb * 8, c->norm_hist + (size_t)slot * nb * 8, sizeof(double) * nb * 8,
-                      cudaMemcpyDeviceToHost));
+        const long long m = std::min(count - q, cap - slot);
+        CK(cudaMemcpy(h.data() + (size_t)q * nb * 8, c->norm_hist + (size_t)slot * nb * 8,
+                      sizeof(double) * nb * 8 * m, cudaMemcpyDeviceToHost));
+        q += m;
     }
     if (c->nranks > 1) {  // non-local blocks are zero: a sum all-reduce gathers them
         for (long long q0 = 0; q0 < count; q0 += 4096) {
@@ -947,8 +950,12 @@ sfv_status sfv_get_dt(sfv_ctx *c, int64_t first, int64_t count, double *out) {
     sfv_status s = hist_range(c, first, count, &done);
     if (s != SFV_OK) return s;
     const long long cap = c->cfg.max_history;
-    for (long long q = 0; q < count; ++q)
-        CK(cudaMemcpy(out + q, c->dt_hist + (first + q) % cap, 8, cudaMemcpyDeviceToHost));
+    for (long long q = 0; q < count;) {
+        const long long slot = (first + q) % cap;
+        const long long m = std::min(count - q, cap - slot);
+        CK(cudaMemcpy(out + q, c->dt_hist + slot, 8 * m, cudaMemcpyDeviceToHost));
+        q += m;
+    }
     return check_device_error(c);
 }
 
