@@ -228,16 +228,18 @@ void build_params(sfv_ctx *c) {
 void choose_launch(sfv_ctx *c, Block &b) {
     b.nstrips = (b.nj + WOUT - 1) / WOUT;
     const int slots = c->nsm * std::max(1, c->occ) * WPC;  // resident warps
+    // minimise (longest segment + prologue) x waves: a segment's time is its
+    // row count plus ~1.5 rows of prologue / pipeline fill, and a launch lasts
+    // as long as its longest segment in each wave
     int best = 1;
-    double best_score = -1.0;
+    double best_cost = 1e300;
     const int cap = std::min(NSEG_MAX, std::max(1, b.ni / 4));
     for (int s = 1; s <= cap; ++s) {
-        const double waves = (double)b.nstrips * s / slots;
-        const double eff = waves / std::ceil(waves);
-        const double L = (double)b.ni / s;
-        const double score = eff * (L / (L + 1.5));
-        if (score > best_score + 1e-9) {
-            best_score = score;
+        const double rows = std::ceil((double)b.ni / s);
+        const double waves = std::ceil((double)b.nstrips * s / slots);
+        const double cost = (rows + 1.5) * waves;
+        if (cost <= best_cost + 1e-9) {  // ties: more segments (less contention per SM)
+            best_cost = cost;
             best = s;
         }
     }
