@@ -8,17 +8,19 @@
 // (PAPER.md:138-139), the residual-norm partials ("residual print",
 // PAPER.md:120) and the CFL reduction for the next step (reading A-R6).
 //
-// Design: a CTA of NT threads owns a strip of up to NT-2
-// contiguous j columns (+1 halo column each side) and marches along i over
-// a segment of rows.  Each row (state, metrics, pointwise RK inputs) is
-// staged into a 4-slot shared-memory ring by cp.async.bulk (TMA bulk copies,
-// mbarrier completion) issued by one thread, 3 rows ahead of use.  Along i
-// every thread keeps its column's stencil window in registers, so each
+// Design: every CTA is one independent warp that owns a
+// strip of 32*CPL-2 contiguous j columns (+1 halo column each side) and
+// marches along i over a segment of rows.  Each row (state, metrics,
+// pointwise RK inputs) is staged into small per-warp shared-memory rings by
+// 2D TMA tensor copies (cp.async.bulk.tensor.2d, mbarrier complete_tx),
+// issued by the whole warp via elect.sync, at least one row ahead of use.
+// Along i every lane keeps its column's stencil window in registers, so each
 // i-face flux is evaluated once and carried to the next row; along j the
-// face states and fluxes are exchanged through shared memory, so each j-face
-// is evaluated once too.  Each limiter value Psi is computed once per cell,
-// direction and component (the paper's §5 de-duplication),
-// on chip.
+// face states and fluxes move between neighbouring lanes through shared
+// memory, so each j-face is evaluated once too.  Each limiter value Psi is
+// computed once per cell, direction and component (the paper's §5
+// de-duplication), on chip.  No CTA-wide barrier in the main
+// loop; kernels chain with programmatic dependent launch.
 #include "sfv_internal.h"
 
 #include <cstdio>
@@ -32,35 +34,6 @@ __device__ __forceinline__ unsigned smem_u32(const void *p) {
 __device__ __forceinline__ void mbar_init(uint64_t *bar, unsigned count) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
 }
-__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, unsigned bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
-                 : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t *bar, unsigned parity) {
-    asm volatile(
-        "{\n\t.reg .pred p;\n\t"
-        "SFV_WAIT_%=:\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
-        "@!p bra SFV_WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
-        "r"(parity)
-        : "memory");
-}
-__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, unsigned bytes, uint64_t *bar) {
-    asm volatile(
-        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-            smem_u32(dst)),
-        "l"(src), "r"(bytes), "r"(smem_u32(bar))
-        : "memory");
-}
-
-__device__ __forceinline__ void tma_2d(void *dst, const CUtensorMap *map, int x, int y, uint64_t *bar) {
-    asm volatile(
-        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
-            smem_u32(dst)),
-        "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(smem_u32(bar))
-        : "memory");
-}
-
 // 32-bit shared-window address variants (addresses precomputed once per warp)
 __device__ __forceinline__ void mbar_wait_s(unsigned bar, unsigned parity) {
     asm volatile(
@@ -87,23 +60,6 @@ __device__ __forceinline__ void elect_tma_s(unsigned dst, const CUtensorMap *map
         "@p cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];"
         "\n\t}" ::"r"(dst),
         "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(bar)
-        : "memory");
-}
-
-// Whole-warp issue: one elected lane posts the expected bytes / the copy.
-__device__ __forceinline__ void elect_expect_tx(uint64_t *bar, unsigned bytes) {
-    asm volatile(
-        "{\n\t.reg .pred p;\n\telect.sync _|p, 0xffffffff;\n\t"
-        "@p mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n\t}" ::"r"(smem_u32(bar)),
-        "r"(bytes)
-        : "memory");
-}
-__device__ __forceinline__ void elect_tma_2d(void *dst, const CUtensorMap *map, int x, int y, uint64_t *bar) {
-    asm volatile(
-        "{\n\t.reg .pred p;\n\telect.sync _|p, 0xffffffff;\n\t"
-        "@p cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];"
-        "\n\t}" ::"r"(smem_u32(dst)),
-        "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(smem_u32(bar))
         : "memory");
 }
 
