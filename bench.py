@@ -218,6 +218,18 @@ def main():
     from paper_2305_18057_b200 import sfv
 
     assert torch.cuda.is_available(), "bench.py needs a GPU (no CPU fallback)"
+    ndev = torch.cuda.device_count()
+    sim = world > ndev
+    if sim:
+        # more ranks than GPUs: only as a functional check of the N > 1 path
+        # (SFV_SIM_HOSTS=1 gives each rank its own NCCL host id, as in
+        # tests/test_gpu_nccl.py); the numbers of such a run are not a bench value
+        assert os.environ.get("SFV_SIM_HOSTS") == "1", f"WORLD_SIZE {world} > {ndev} GPUs"
+        os.environ["NCCL_HOSTID"] = f"sfv-sim-host-{rank}"
+        os.environ.setdefault("NCCL_SOCKET_IFNAME", "lo")
+        os.environ.setdefault("NCCL_IB_DISABLE", "1")
+        os.environ.setdefault("NCCL_NVLS_ENABLE", "0")
+    local_rank = local_rank % ndev
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
     if world > 1:
@@ -293,11 +305,8 @@ def main():
     # ---- end to end through the public API with host buffers ----
     e2e = None
     if not args.no_e2e:
-        Uh = torch.from_numpy(np.ascontiguousarray(U0)).pin_memory() if world == 1 else None
-        Uout = torch.empty_like(Uh) if Uh is not None else None
-        if Uh is None:
-            Uh = torch.from_numpy(np.ascontiguousarray(U0)).pin_memory()
-            Uout = torch.empty_like(Uh)
+        Uh = torch.from_numpy(np.ascontiguousarray(U0)).pin_memory()
+        Uout = torch.empty_like(Uh)
         K = args.steps
         barrier()
         t0 = time.perf_counter()
@@ -328,6 +337,7 @@ def main():
                 "scaling": scaling, "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded inputs)",
                 "config": {"workload": desc, "global_cells": cells_total, "cells_per_gpu": cells_rank,
                            "rk_stages": stages, "rk": args.rk, "parallelism": f"slab{px}x1",
+                           **({"simulated_ranks_on_one_gpu": True} if sim else {}),
                            "l2": f"no flush: working set {solver.ws.numel() / 1e6:.0f} MB per GPU vs 126 MB L2",
                            "launch": li,
                            "mcell_steps_per_s": value / stages,

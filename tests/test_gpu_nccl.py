@@ -1,0 +1,110 @@
+"""The NCCL path (nranks > 1) on ONE GPU.
+
+Every gpurun box and the round-end tiers have a single B200, so the
+multi-rank path is exercised by running `world` processes on cuda:0 that
+NCCL believes live on different hosts (a distinct NCCL_HOSTID per rank ->
+the socket network transport over loopback; NCCL forbids two ranks of one
+communicator on one GPU of one host).  Everything above the transport --
+sfv_partition's communicator, the grouped send/recv of the row halos on the
+comm stream, the pack/unpack of column halos, the sigma max all-reduce, the
+zero-padded sum all-reduces of get_state / get_residual_norms, graph
+capture with NCCL calls, the edge/interior overlap split -- is the code a
+multi-GPU run executes.  The result must be bitwise equal to the same
+decomposition run in loopback mode (which is bitwise equal to one block,
+test_gpu_parity.py::test_loopback_decomposition_invariance) and match the
+oracle within the 1e-12/50-step gates."""
+import os
+import socket
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, px, py, ni, nj, steps, overlap, out_q):
+    os.environ.update({"MASTER_ADDR": "127.0.0.1", "MASTER_PORT": str(port),
+                       "NCCL_HOSTID": f"sfv-sim-host-{rank}", "NCCL_SOCKET_IFNAME": "lo",
+                       "NCCL_IB_DISABLE": "1", "NCCL_NVLS_ENABLE": "0", "SFV_OVERLAP": str(overlap)})
+    import sys
+    sys.path.insert(0, ROOT)
+    import torch
+    import torch.distributed as dist
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2305_18057_b200 import inputs as I
+        from paper_2305_18057_b200 import sfv
+        X, Y = I.ramp_nodes(ni, nj, 30.0)
+        cfg = I.default_config(ni, nj)
+        obj = [sfv.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        s = sfv.Solver(cfg, X, Y, px=px, py=py, rank=rank, nranks=world, nccl_id=obj[0], device=0)
+        s.set_state(I.perturbed_state(ni, nj, 7))
+        s.step(steps)
+        s.sync()
+        U = s.get_state()
+        nrm = s.residual_norms()
+        dts = s.dt()
+        s.close()
+        out_q.put((rank, "ok", U if rank == 0 else None, nrm, dts))
+    except Exception as ex:  # surface to the parent
+        out_q.put((rank, repr(ex), None, None, None))
+    finally:
+        dist.destroy_process_group()
+
+
+def _run(world, px, py, ni, nj, steps, overlap):
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    ps = [ctx.Process(target=_worker, args=(r, world, port, px, py, ni, nj, steps, overlap, q))
+          for r in range(world)]
+    for p in ps:
+        p.start()
+    try:
+        res = sorted((q.get(timeout=300) for _ in range(world)), key=lambda r: r[0])
+    finally:
+        for p in ps:
+            p.join(timeout=60)
+            if p.is_alive():
+                p.kill()
+    for rank, status, *_ in res:
+        assert status == "ok", (rank, status)
+    return res
+
+
+@pytest.mark.parametrize("world,px,py,overlap", [(2, 2, 1, 1), (2, 2, 1, 0), (2, 1, 2, 1), (4, 2, 2, 1)])
+def test_nccl_ranks_match_loopback_and_oracle(oracle_mod, world, px, py, overlap):
+    from paper_2305_18057_b200 import inputs as I
+    from paper_2305_18057_b200 import sfv
+    from parity_util import dt_error, norm_error, state_error
+    ni, nj, steps = 160, 64, 50
+    res = _run(world, px, py, ni, nj, steps, overlap)
+    U = res[0][2]
+    X, Y = I.ramp_nodes(ni, nj, 30.0)
+    cfg = I.default_config(ni, nj)
+    U0 = I.perturbed_state(ni, nj, 7)
+    g = sfv.Solver(cfg, X, Y, px=px, py=py)
+    g.set_state(U0); g.step(steps); g.sync()
+    np.testing.assert_array_equal(U, g.get_state())
+    for rank, _, _, nrm, dts in res:  # every rank holds the global histories
+        np.testing.assert_array_equal(dts, g.dt())
+        # the per-block partial sums group cells by launch (the overlap split
+        # adds edge launches), so the norms agree to rounding, not bitwise
+        assert norm_error(nrm, g.residual_norms()) < 1e-14
+    o = oracle_mod.Oracle(cfg, X, Y)
+    o.set_state(U0); o.step(steps)
+    assert np.all(state_error(U, o.get_state()) <= 1e-11)
+    assert norm_error(res[0][3], o.residual_norms()) <= 1e-10
+    assert dt_error(res[0][4], o.dt()) <= 1e-13
