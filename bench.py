@@ -275,15 +275,17 @@ def main():
     value = cells_total * stages * args.steps / (ms_max * 1e-3) / 1e6
     cells_rank = cells_total // world
     # our kernels per step: the stage kernels (plus 1-2 two-row edge launches per
-    # stage on a rank with neighbours, overlap split) and one finalize kernel
+    # stage on a rank with neighbours, overlap split); one norms-reduction kernel
+    # per block after every 32nd step since set_state (history >= 32)
     edges = (rank > 0) + (rank < world - 1) if world > 1 else 0
-    launches = (stages * (1 + edges) + 1) * args.steps
+    nbatch = (args.warmup + args.steps) // 32 - args.warmup // 32
+    launches = stages * (1 + edges) * args.steps + nbatch
     stage_launches = stages * args.steps
 
     # ---- roofline of the dominant kernel (the fused stage kernel) ----
-    # At N = 1 a step is the stage kernels plus one tiny finalize kernel, so the
-    # timed region / stage launches is a (slightly conservative) average
-    # stage-kernel duration.
+    # At N = 1 a step is the stage kernels (plus a tiny norms kernel every 32
+    # steps), so the timed region / stage launches is a (slightly conservative)
+    # average stage-kernel duration.
     avg_launch_s = ms_max * 1e-3 / stage_launches
     alg_bytes = ALG_BYTES_PER_CELL_STAGE * cells_rank
     hbm_achieved = alg_bytes / avg_launch_s / 1e9

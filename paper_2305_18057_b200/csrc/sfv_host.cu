@@ -130,6 +130,8 @@ struct sfv_ctx {
     cudaStream_t st = nullptr;
     double *sig = nullptr;
     long long *step_ctr = nullptr;
+    unsigned *done = nullptr;
+    int pring = 1;  // steps of norm partials kept before a batched reduction
     unsigned long long *err = nullptr, *geo_bad = nullptr;
     double *dt_hist = nullptr, *norm_hist = nullptr, *gbuf = nullptr;
     size_t gbuf_elems = 0;
@@ -140,7 +142,7 @@ struct sfv_ctx {
     cudaStream_t comm_st = nullptr;                  // halo exchange stream (overlap)
     cudaEvent_t ev_edge = nullptr, ev_comm = nullptr;
     bool timing_open = false;
-    cudaGraphExec_t gexec = nullptr;
+    cudaGraphExec_t gexec = nullptr, gexec_norms = nullptr;  // step; step + norms batch
     bool graph_failed = false;
     ncclComm_t comm = nullptr;
     std::string msg;
@@ -320,6 +322,7 @@ size_t layout(sfv_ctx *c, bool assign) {
     };
     const int cap = (int)c->cfg.max_history;
     const int nbuf = nbuf_of(c->cfg.rk);
+    c->pring = std::min(32, cap);
     size_t o_misc = take(256);
     size_t o_dt = take(sizeof(double) * cap);
     size_t o_norm = take(sizeof(double) * (size_t)cap * c->nblocks_total * 8);
@@ -331,6 +334,7 @@ size_t layout(sfv_ctx *c, bool assign) {
         c->step_ctr = reinterpret_cast<long long *>(c->ws + o_misc + 16);
         c->err = reinterpret_cast<unsigned long long *>(c->ws + o_misc + 24);
         c->geo_bad = reinterpret_cast<unsigned long long *>(c->ws + o_misc + 32);
+        c->done = reinterpret_cast<unsigned *>(c->ws + o_misc + 40);
         c->dt_hist = reinterpret_cast<double *>(c->ws + o_dt);
         c->norm_hist = reinterpret_cast<double *>(c->ws + o_norm);
         c->gbuf = gb ? reinterpret_cast<double *>(c->ws + o_g) : nullptr;
@@ -343,7 +347,7 @@ size_t layout(sfv_ctx *c, bool assign) {
         size_t on = take(sizeof(double) * 2 * (size_t)(b.ni + 1) * (b.nj + 1));
         size_t os = take(sizeof(double) * 4 * (size_t)b.ni * b.nj);
         const int max_cta = (((b.nj + WOUT - 1) / WOUT) * (NSEG_MAX + 2) + WPC - 1) / WPC + 2;
-        size_t op = take(sizeof(double) * 8 * (size_t)max_cta);
+        size_t op = take(sizeof(double) * 8 * (size_t)max_cta * c->pring);
         size_t ot = take(256);
         size_t ox[4];
         for (int k = 0; k < 4; ++k) ox[k] = take(c->nranks > 1 ? sizeof(double) * 8 * (size_t)b.ni : 0);
@@ -506,6 +510,9 @@ StageArgs make_args(sfv_ctx *c, Block &b, int k) {
     a.block_id = b.id;
     a.nblocks = c->nblocks_total;
     a.partials = b.partials;
+    a.pring = c->pring;
+    a.done = c->done;
+    a.bump = 0;
     a.err = c->err;
     a.stage = k;
     a.nstages = nstages_of(c->cfg.rk);
@@ -513,7 +520,27 @@ StageArgs make_args(sfv_ctx *c, Block &b, int k) {
     return a;
 }
 
-sfv_status enqueue_step(sfv_ctx *c, cudaStream_t st) {
+// Norm partials of `count` steps -> history, every local block (first < 0:
+// the `count` steps before the device step counter).
+sfv_status enqueue_norms(sfv_ctx *c, long long first, int count, cudaStream_t st) {
+    for (Block &b : c->blocks) {
+        NormsArgs f{};
+        f.partials = b.partials;
+        f.ncta = b.ncta_total;
+        f.pring = c->pring;
+        f.norm_hist = c->norm_hist;
+        f.step_ctr = c->step_ctr;
+        f.first = first;
+        f.count = count;
+        f.cap = (int)c->cfg.max_history;
+        f.block_id = b.id;
+        f.nblocks = c->nblocks_total;
+        CK(launch_norms(f, st));
+    }
+    return SFV_OK;
+}
+
+sfv_status enqueue_step(sfv_ctx *c, cudaStream_t st, bool norms_batch) {
     const int s = nstages_of(c->cfg.rk);
     const bool cflmode = !(c->cfg.dt_fixed > 0.0);
     bool any_split = false;
@@ -522,6 +549,8 @@ sfv_status enqueue_step(sfv_ctx *c, cudaStream_t st) {
         const StageSpec sp = stage_spec(c->cfg.rk, k);
         auto launch_part = [&](Block &b, int q) -> sfv_status {
             StageArgs a = make_args(c, b, k);
+            // the step's last launch in stream order advances the step counter
+            a.bump = (k == s && &b == &c->blocks.back() && q == b.nlaunch - 1) ? 1 : 0;
             a.row_lo = b.row_lo[q];
             a.row_hi = b.row_hi[q];
             a.nseg = b.lseg[q];
@@ -551,25 +580,6 @@ sfv_status enqueue_step(sfv_ctx *c, cudaStream_t st) {
                 if (r != SFV_OK) return r;
             }
         }
-        if (k == 1) {  // norms of R(U^n), dt record, step counter (after every block's stage 1)
-            for (Block &b : c->blocks) {
-                FinalizeArgs f{};
-                f.partials = b.partials;
-                f.ncta = b.ncta_total;
-                f.norm_hist = c->norm_hist;
-                f.dt_hist = c->dt_hist;
-                f.sig = c->sig;
-                f.step_ctr = c->step_ctr;
-                f.cap = (int)c->cfg.max_history;
-                f.block_id = b.id;
-                f.nblocks = c->nblocks_total;
-                f.lead = (&b == &c->blocks.front()) ? 1 : 0;
-                f.bump = (&b == &c->blocks.back()) ? 1 : 0;
-                f.cfl = c->cfg.cfl;
-                f.dt_fixed = c->cfg.dt_fixed;
-                CK(launch_finalize(f, st));
-            }
-        }
         if (any_split) {
             sfv_status r = exchange_cols(c, sp.out, st);
             if (r != SFV_OK) return r;
@@ -580,6 +590,7 @@ sfv_status enqueue_step(sfv_ctx *c, cudaStream_t st) {
         }
     }
     if (c->nranks > 1 && cflmode) NK(nccl().AllReduce(c->sig, c->sig, 2, ncclDouble, ncclMax, c->comm, st));
+    if (norms_batch) return enqueue_norms(c, -1, c->pring, st);
     return SFV_OK;
 }
 
@@ -805,6 +816,7 @@ sfv_status sfv_set_state(sfv_ctx *c, const double *U) {
     sfv_status r = exchange(c, 0, st);
     if (r != SFV_OK) return r;
     CK(cudaMemsetAsync(c->sig, 0, 24, st));  // sig[2], step counter
+    CK(cudaMemsetAsync(c->done, 0, sizeof(unsigned), st));
     CK(cudaMemsetAsync(c->dt_hist, 0, sizeof(double) * c->cfg.max_history, st));
     CK(cudaMemsetAsync(c->norm_hist, 0, sizeof(double) * c->cfg.max_history * c->nblocks_total * 8, st));
     CK(cudaStreamSynchronize(st));
@@ -832,22 +844,31 @@ sfv_status sfv_step(sfv_ctx *c, int32_t nsteps) {
     if (nsteps < 0) return fail(c, SFV_ERR_ARG, "nsteps < 0");
     if (nsteps == 0) return SFV_OK;
     if (!c->gexec && !c->graph_failed) {
-        cudaStream_t cap;
-        CK(cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking));
-        cudaGraph_t g = nullptr;
-        bool ok = cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal) == cudaSuccess;
-        sfv_status r = SFV_OK;
-        if (ok) {
-            r = enqueue_step(c, cap);
-            ok = (cudaStreamEndCapture(cap, &g) == cudaSuccess) && r == SFV_OK;
-        }
-        if (ok) ok = cudaGraphInstantiate(&c->gexec, g, 0) == cudaSuccess;
-        if (g) cudaGraphDestroy(g);
-        cudaStreamDestroy(cap);
-        if (!ok) {
-            c->gexec = nullptr;
-            c->graph_failed = true;
-            cudaGetLastError();
+        // two graphs: one step, and one step followed by the batched norms
+        // reduction (every pring-th step)
+        for (int v = 0; v < 2; ++v) {
+            cudaStream_t cap;
+            CK(cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking));
+            cudaGraph_t g = nullptr;
+            cudaGraphExec_t ge = nullptr;
+            bool ok = cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal) == cudaSuccess;
+            sfv_status r = SFV_OK;
+            if (ok) {
+                r = enqueue_step(c, cap, v == 1);
+                ok = (cudaStreamEndCapture(cap, &g) == cudaSuccess) && r == SFV_OK;
+            }
+            if (ok) ok = cudaGraphInstantiate(&ge, g, 0) == cudaSuccess;
+            if (g) cudaGraphDestroy(g);
+            cudaStreamDestroy(cap);
+            if (!ok) {
+                c->graph_failed = true;
+                cudaGetLastError();
+                if (ge) cudaGraphExecDestroy(ge);
+                if (c->gexec) cudaGraphExecDestroy(c->gexec);
+                c->gexec = nullptr;
+                break;
+            }
+            (v == 0 ? c->gexec : c->gexec_norms) = ge;
         }
     }
     if (!c->timing_open) {
@@ -855,10 +876,11 @@ sfv_status sfv_step(sfv_ctx *c, int32_t nsteps) {
         c->timing_open = true;
     }
     for (int s = 0; s < nsteps; ++s) {
+        const bool batch = (c->steps_enq + s + 1) % c->pring == 0;
         if (c->gexec) {
-            CK(cudaGraphLaunch(c->gexec, c->st));
+            CK(cudaGraphLaunch(batch ? c->gexec_norms : c->gexec, c->st));
         } else {
-            sfv_status r = enqueue_step(c, c->st);
+            sfv_status r = enqueue_step(c, c->st, batch);
             if (r != SFV_OK) return r;
         }
     }
@@ -907,6 +929,12 @@ sfv_status sfv_get_residual_norms(sfv_ctx *c, int64_t first, int64_t count, doub
     if (s != SFV_OK) return s;
     s = check_device_error(c);
     if (s != SFV_OK) return s;
+    // steps after the last batched reduction: reduce them now (idempotent)
+    if (done % c->pring) {
+        s = enqueue_norms(c, done - done % c->pring, (int)(done % c->pring), c->st);
+        if (s != SFV_OK) return s;
+        CK(cudaStreamSynchronize(c->st));
+    }
     const int nb = c->nblocks_total;
     const long long cap = c->cfg.max_history;
     std::vector<double> h((size_t)count * nb * 8);
@@ -1015,6 +1043,7 @@ const char *sfv_last_error(const sfv_ctx *c) { return c ? c->msg.c_str() : "null
 void sfv_destroy(sfv_ctx *c) {
     if (!c) return;
     if (c->gexec) cudaGraphExecDestroy(c->gexec);
+    if (c->gexec_norms) cudaGraphExecDestroy(c->gexec_norms);
     if (c->ev0) cudaEventDestroy(c->ev0);
     if (c->ev1) cudaEventDestroy(c->ev1);
     if (c->ev_edge) cudaEventDestroy(c->ev_edge);

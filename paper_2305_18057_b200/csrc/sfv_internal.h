@@ -64,19 +64,24 @@ struct StageArgs {
     double *dt_hist;        // [cap]
     double *norm_hist;      // [cap][nblocks][8]
     int cap, block_id, nblocks;
-    double *partials;       // [8][part_stride] norm partials (stage 1)
+    double *partials;       // [pring][8][part_stride] norm partials ring (stage 1 of step n: slot n % pring)
+    int pring;
+    unsigned *done;         // CTA arrival counter of the step's last launch (bump)
+    int bump;               // last launch of the step: record dt_n, clear its sigma slot, advance the counter
     unsigned long long *err;
     int stage, nstages;
     Params P;
 };
 
-struct FinalizeArgs {
-    const double *partials;
-    int ncta;
-    double *norm_hist, *dt_hist, *sig;
-    long long *step_ctr;
-    int cap, block_id, nblocks, lead, bump;
-    double cfl, dt_fixed;
+// Reduction of `count` steps of one block's norm partials into the history:
+// steps first .. first+count-1 (first < 0: the `count` steps before *step_ctr).
+struct NormsArgs {
+    const double *partials;  // ring [pring][8][ncta]
+    int ncta, pring;
+    double *norm_hist;
+    const long long *step_ctr;
+    long long first;
+    int count, cap, block_id, nblocks;
 };
 
 struct MetricsArgs {
@@ -88,7 +93,7 @@ struct MetricsArgs {
 
 // launchers (sfv_kernels.cu); all asynchronous on `st`
 cudaError_t launch_stage(const StageArgs &a, int mode, bool norms, bool dtmax, cudaStream_t st);
-cudaError_t launch_finalize(const FinalizeArgs &f, cudaStream_t st);
+cudaError_t launch_norms(const NormsArgs &f, cudaStream_t st);
 cudaError_t stage_occupancy(int mode, bool norms, bool dtmax, bool fast, int *ctas_per_sm);
 bool fast_path(const Params &P);
 cudaError_t prepare_stage_kernels();

@@ -271,8 +271,8 @@ __global__ void __launch_bounds__(NT, SFV_MINB) stage_kernel(const __grid_consta
     long long n = 0;
     double dt = 0.0, coef = 0.0;
     auto read_step = [&]() {
-        // the finalize kernel after stage 1 advances the counter
-        n = *a.step_ctr - (a.stage > 1 ? 1 : 0);
+        // the last CTA of the step's last launch advances the counter
+        n = *a.step_ctr;
         dt = P.dt_fixed > 0.0 ? P.dt_fixed : P.cfl / a.sig[n & 1];
         coef = a.coef * dt;
     };
@@ -634,7 +634,8 @@ __global__ void __launch_bounds__(NT, SFV_MINB) stage_kernel(const __grid_consta
         }
     }
     if (NORMS) {
-        // per-CTA partials, layout [8][ncta]; reduced in fixed order by finalize_kernel
+        // per-CTA partials, ring slot n % pring of [8][ncta]; reduced in fixed
+        // order by norms_kernel (batched, off the per-step critical path)
 #pragma unroll
         for (int q = 0; q < 8; ++q) {
             double x = nrm[q];
@@ -648,29 +649,50 @@ __global__ void __launch_bounds__(NT, SFV_MINB) stage_kernel(const __grid_consta
         if (t < 8) {
             double x = red[t * WPC];
             for (int w = 1; w < WPC; ++w) x = t < 4 ? x + red[t * WPC + w] : fmax(x, red[t * WPC + w]);
-            a.partials[(size_t)t * a.part_stride + a.part_base + blockIdx.x] = x;
+            a.partials[((size_t)(n % a.pring) * 8 + t) * a.part_stride + a.part_base + blockIdx.x] = x;
+        }
+    }
+    if (a.bump) {
+        // end of step n: the last CTA to arrive records dt_n, clears sigma slot
+        // n&1 (the slot step n+1's last stage fills) and advances the counter.
+        // Every CTA of every launch of the step has read the counter and the
+        // slot by then (earlier launches completed before this grid's
+        // griddepcontrol.wait; this grid's CTAs before their arrival).
+        __syncthreads();
+        if (t == 0) {
+            __threadfence();
+            if (atomicAdd(a.done, 1u) == gridDim.x - 1) {
+                __threadfence();
+                if (P.dt_fixed > 0.0) {
+                    a.dt_hist[n % a.cap] = P.dt_fixed;
+                } else {
+                    a.dt_hist[n % a.cap] = P.cfl / a.sig[n & 1];
+                    a.sig[n & 1] = 0.0;
+                }
+                *a.done = 0u;
+                *a.step_ctr = n + 1;
+            }
         }
     }
 }
 
-// After stage 1 of each block: deterministic fixed-order reduction of the
-// norm partials into the history ("residual print"; reading
-// A-R20); the lead block records dt_n and clears the sigma slot the last
-// stage will fill; the last block advances the step counter.
+// Deterministic fixed-order reduction of a block's per-CTA norm partials
+// into the history ("residual print"; reading A-R20): one CTA
+// per step, batched every `pring` steps and on demand at query time, so it is
+// not on the per-step critical path.
 constexpr int FIN_T = 256;
-__global__ void __launch_bounds__(FIN_T) finalize_kernel(FinalizeArgs f) {
+__global__ void __launch_bounds__(FIN_T) norms_kernel(NormsArgs f) {
     __shared__ double part[8][FIN_T / 32];
     const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
-    pdl_wait();
-    pdl_launch_dependents();
-    const long long n = *f.step_ctr;
+    const long long n = (f.first >= 0 ? f.first : *f.step_ctr - f.count) + blockIdx.x;
+    const double *src = f.partials + (size_t)(n % f.pring) * 8 * f.ncta;
     // fixed assignment (thread t: partials t, t+256, ...) and fixed-order
     // shuffle / warp trees: deterministic for a given launch geometry
     double acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     for (int b = t; b < f.ncta; b += FIN_T) {
 #pragma unroll
         for (int q = 0; q < 8; ++q) {
-            const double x = f.partials[(size_t)q * f.ncta + b];
+            const double x = src[(size_t)q * f.ncta + b];
             acc[q] = q < 4 ? acc[q] + x : fmax(acc[q], x);
         }
     }
@@ -689,26 +711,12 @@ __global__ void __launch_bounds__(FIN_T) finalize_kernel(FinalizeArgs f) {
         for (int w = 1; w < FIN_T / 32; ++w) x = t < 4 ? x + part[t][w] : fmax(x, part[t][w]);
         f.norm_hist[((size_t)(n % f.cap) * f.nblocks + f.block_id) * 8 + t] = x;
     }
-    if (t == 0) {
-        if (f.lead) {
-            f.dt_hist[n % f.cap] = f.dt_fixed > 0.0 ? f.dt_fixed : f.cfl / f.sig[n & 1];
-            if (!(f.dt_fixed > 0.0)) f.sig[(n + 1) & 1] = 0.0;
-        }
-        if (f.bump) *f.step_ctr = n + 1;
-    }
 }
 
-cudaError_t launch_finalize(const FinalizeArgs &f, cudaStream_t st) {
-    cudaLaunchConfig_t cfg{};
-    cfg.gridDim = dim3(1);
-    cfg.blockDim = dim3(FIN_T);
-    cfg.stream = st;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    attr[0].val.programmaticStreamSerializationAllowed = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    return cudaLaunchKernelEx(&cfg, finalize_kernel, f);
+cudaError_t launch_norms(const NormsArgs &f, cudaStream_t st) {
+    if (f.count <= 0) return cudaSuccess;
+    norms_kernel<<<f.count, FIN_T, 0, st>>>(f);
+    return cudaGetLastError();
 }
 
 template <int MODE, bool NORMS, bool DTMAX, bool FAST>

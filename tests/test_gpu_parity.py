@@ -368,3 +368,33 @@ def test_c2_eight_slab_loopback(sfv_mod, oracle_mod):
     g1, o = run_pair(sfv_mod, oracle_mod, cfg, X, Y, U0, 3)
     np.testing.assert_array_equal(g8.get_state(), g1.get_state())
     check(g8, o, 1e-12)
+
+
+@pytest.mark.parametrize("cap", [5, 32, 100])
+def test_history_batches_and_ring(sfv_mod, oracle_mod, cap):
+    """Norm partials are reduced every min(32, cap) steps and on demand at a
+    query; queries between steps, counts that are not a multiple of the batch
+    and a wrapped history ring must all give the oracle's histories."""
+    ni, nj = 96, 40
+    X, Y = I.ramp_nodes(ni, nj, 30.0)
+    cfg = I.default_config(ni, nj, max_history=cap)
+    U0 = I.perturbed_state(ni, nj, 11)
+    g = sfv_mod.Solver(cfg, X, Y)
+    o = oracle_mod.Oracle(cfg, X, Y)
+    g.set_state(U0); o.set_state(U0)
+    done = 0
+    for n in (3, 1, 30, 7, 40):
+        g.step(n); o.step(n); done += n
+        g.sync()
+        assert g.steps_done == done
+        first = max(0, done - cap)
+        ng, no = g.residual_norms(first), o.residual_norms(first)
+        assert ng.shape == no.shape
+        assert norm_error(ng, no) <= 1e-10
+        assert dt_error(g.dt(first), o.dt(first)) <= 1e-13
+    # a query before the batch boundary must not change what the batch writes
+    g2 = sfv_mod.Solver(cfg, X, Y)
+    g2.set_state(U0); g2.step(done); g2.sync()
+    first = max(0, done - cap)
+    np.testing.assert_array_equal(g2.residual_norms(first), g.residual_norms(first))
+    np.testing.assert_array_equal(g2.get_state(), g.get_state())
