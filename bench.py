@@ -201,6 +201,12 @@ def main():
     ap.add_argument("--workload", default="C2", choices=["C2", "C3", "C4"])
     ap.add_argument("--rk", default="rk4", choices=["rk4", "heun", "jst4"],
                     help="RK tableau (reading A-R5; SURVEY §8(f) f1: per-substep cost RK2 vs RK4, PAPER.md:276)")
+    ap.add_argument("--halo", default="peer", choices=["copy", "peer"],
+                    help="halo exchange: peer = device-initiated stores into the neighbour's ghost frame from "
+                         "the stage kernel (DESIGN.md §5.2); copy = NCCL send/recv / device copies on a comm stream")
+    ap.add_argument("--blocks", type=int, default=1,
+                    help="N = 1 only: decompose the grid into this many slabs on the one GPU (loopback "
+                         "partition-overhead experiment; not the headline configuration)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     args = ap.parse_args()
@@ -239,6 +245,9 @@ def main():
         print(f"# note: --gpus {args.gpus} but WORLD_SIZE {world}; using {world}", file=sys.stderr)
 
     ni, nj, theta, desc, scaling, px = workload(args.workload, n_gpus)
+    if world == 1 and args.blocks > 1:
+        px = args.blocks
+        desc += f"; {px} loopback slabs on one GPU"
     X, Y = I.ramp_nodes(ni, nj, theta)
     rk = {"rk4": I.RK4_CLASSIC, "heun": I.RK2_HEUN, "jst4": I.RK4_JAMESON}[args.rk]
     cfg = I.default_config(ni, nj, rk=rk, max_history=max(args.steps + args.warmup + 16, 64))
@@ -251,6 +260,27 @@ def main():
     stream = torch.cuda.Stream(device=dev)
     solver = sfv.Solver(cfg, X, Y, px=px, py=1, rank=rank, nranks=world, nccl_id=nccl_id,
                         device=local_rank, stream=stream)
+    nblk = px if world == 1 else 1
+    halo_note = args.halo
+    if args.halo == "peer" and px > 1:
+        if world == 1:
+            solver.enable_peer_halo()
+        else:
+            # collective: peer mode only if every rank could map its neighbours
+            hs = [None] * world
+            dist.all_gather_object(hs, solver.peer_handle())
+            ok, why = 1, ""
+            try:
+                solver.peer_connect(hs)
+            except sfv.SfvError as ex:
+                ok, why = 0, str(ex)
+            flag = torch.tensor([ok], dtype=torch.int32, device=dev)
+            dist.all_reduce(flag, op=dist.ReduceOp.MIN)
+            if int(flag.item()) == 1:
+                solver.set_halo_mode(sfv.HALO_PEER)
+            else:
+                args.halo = "copy"
+                halo_note = f"copy (peer mapping unavailable on some rank: {why or 'other rank'})"
     solver.set_state(U0)
     solver.step(args.warmup)
     solver.sync()
@@ -274,30 +304,37 @@ def main():
     stages = I.RK_STAGES[rk]
     value = cells_total * stages * args.steps / (ms_max * 1e-3) / 1e6
     cells_rank = cells_total // world
+    cells_launch = cells_rank // nblk
     # our kernels per step: the stage kernels (plus 1-2 two-row edge launches per
     # stage on a rank with neighbours, overlap split); one norms-reduction kernel
     # per block after every 32nd step since set_state (history >= 32)
-    edges = (rank > 0) + (rank < world - 1) if world > 1 else 0
+    # (peer mode: one launch per stage and block, the edge tasks store the halos)
+    if world > 1:
+        edges = (rank > 0) + (rank < world - 1)
+    else:
+        edges = 0 if nblk == 1 else 2 * (nblk - 1) / nblk  # average per loopback block
+    if args.halo == "peer":
+        edges = 0
     nbatch = (args.warmup + args.steps) // 32 - args.warmup // 32
-    launches = stages * (1 + edges) * args.steps + nbatch
-    stage_launches = stages * args.steps
+    launches = int(round(nblk * (stages * (1 + edges) * args.steps + nbatch)))
+    stage_launches = stages * args.steps * nblk
 
     # ---- roofline of the dominant kernel (the fused stage kernel) ----
     # At N = 1 a step is the stage kernels (plus a tiny norms kernel every 32
     # steps), so the timed region / stage launches is a (slightly conservative)
     # average stage-kernel duration.
     avg_launch_s = ms_max * 1e-3 / stage_launches
-    alg_bytes = ALG_BYTES_PER_CELL_STAGE * cells_rank
+    alg_bytes = ALG_BYTES_PER_CELL_STAGE * cells_launch
     hbm_achieved = alg_bytes / avg_launch_s / 1e9
     peak, peak_src = measured_peak()
     traffic_pc, prof = load_profile_traffic()
     hbm = {"bound": "hbm", "achieved": hbm_achieved, "peak": peak, "unit": "GB/s", "frac": hbm_achieved / peak,
-           "traffic": (traffic_pc * cells_rank) if traffic_pc else None,
+           "traffic": (traffic_pc * cells_launch) if traffic_pc else None,
            "alg_bytes_per_cell_stage": ALG_BYTES_PER_CELL_STAGE, "peak_source": peak_src}
     roof = dict(hbm, kernel="sfv::stage_kernel (4 launches per step, averaged)")
     if prof and prof.get("fp64_inst_per_cell_stage"):
         # FP64 pipe is the nearer roof: report it as the bound, HBM alongside
-        fp64_rate = prof["fp64_inst_per_cell_stage"] * cells_rank / avg_launch_s
+        fp64_rate = prof["fp64_inst_per_cell_stage"] * cells_launch / avg_launch_s
         roof = {"bound": "alu", "achieved": fp64_rate / 1e12, "peak": FP64_PEAK_INST_S / 1e12,
                 "unit": "T FP64-inst/s", "frac": fp64_rate / FP64_PEAK_INST_S,
                 "traffic": hbm["traffic"], "fp64_inst_per_cell_stage": prof["fp64_inst_per_cell_stage"],
@@ -339,6 +376,7 @@ def main():
                 "scaling": scaling, "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded inputs)",
                 "config": {"workload": desc, "global_cells": cells_total, "cells_per_gpu": cells_rank,
                            "rk_stages": stages, "rk": args.rk, "parallelism": f"slab{px}x1",
+                           "halo": halo_note if px > 1 else "none",
                            **({"simulated_ranks_on_one_gpu": True} if sim else {}),
                            "l2": f"no flush: working set {solver.ws.numel() / 1e6:.0f} MB per GPU vs 126 MB L2",
                            "launch": li,

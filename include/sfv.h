@@ -58,12 +58,23 @@ typedef enum {
     SFV_ERR_CUDA = 5,        /* CUDA runtime failure (incl. no device) */
     SFV_ERR_NCCL = 6,        /* NCCL failure or NCCL library not loadable */
     SFV_ERR_OOM = 7,         /* workspace too small */
-    SFV_ERR_UNSUPPORTED = 8
+    SFV_ERR_UNSUPPORTED = 8,
+    SFV_ERR_HALO = 9         /* device-initiated halo exchange: a neighbour never signalled */
 } sfv_status;
 
 typedef enum { SFV_BC_INFLOW = 0, SFV_BC_OUTFLOW = 1, SFV_BC_SLIP_WALL = 2 } sfv_bc;
 typedef enum { SFV_LIM_VAN_ALBADA = 0, SFV_LIM_VAN_ALBADA2 = 1, SFV_LIM_NONE = 2 } sfv_limiter;
 typedef enum { SFV_RK4_CLASSIC = 0, SFV_RK2_HEUN = 1, SFV_RK4_JAMESON = 2 } sfv_rk;
+/* How the ghost layers of connected edges are refreshed after each stage
+ * ("boundary data exchange"):
+ *   COPY : device copies between local blocks / NCCL send/recv between ranks
+ *          on a high-priority stream, overlapped with the interior launch;
+ *   PEER : device-initiated -- the stage kernel's edge tasks store the new
+ *          state's 2 edge layers straight into the neighbour's ghost frame
+ *          (loopback: same device; ranks: CUDA-IPC mapping over NVLink) and
+ *          publish the stage sequence number to the neighbour's inbound flag;
+ *          the neighbour's edge tasks wait on it before staging ghosts. */
+typedef enum { SFV_HALO_COPY = 0, SFV_HALO_PEER = 1 } sfv_halo;
 
 typedef struct {
     int32_t ni, nj;              /* interior cells (paper N_l, N_w; N_d = 1), each >= 2 */
@@ -179,6 +190,34 @@ sfv_status sfv_launch_info(const sfv_ctx *ctx, int32_t *out4);
  * n device doubles (which: 0 = reciprocal, 1 = reciprocal square root,
  * 2 = square root) into out (device), on the bound stream; synchronising. */
 sfv_status sfv_debug_math(sfv_ctx *ctx, int32_t which, const double *in_dev, double *out_dev, int64_t n);
+
+/* Select the halo-exchange mode (sfv_halo; default COPY).  After sfv_bind;
+ * synchronises the stream and requires a new sfv_set_state (the step counter
+ * and the peer flags restart there).  PEER with nranks > 1 needs
+ * sfv_peer_connect first.  ARG: unknown mode.  SEQUENCE: order violated.
+ * A peer that never signals is reported by the next synchronising call as
+ * SFV_ERR_HALO (after a 20 s device-side timeout; no hang). */
+sfv_status sfv_set_halo_mode(sfv_ctx *ctx, int32_t mode);
+
+/* nranks > 1, after sfv_bind: 128 opaque bytes describing this rank's block
+ * for its neighbours (CUDA-IPC handle of the allocation holding the
+ * workspace, the workspace offset, buffer and flag offsets, ni, nj, pitch,
+ * block id).  The workspace must come from cudaMalloc (e.g. PyTorch's default
+ * caching allocator), not from a VMM / expandable segment.  CUDA: no IPC. */
+sfv_status sfv_peer_handle(sfv_ctx *ctx, void *out128);
+
+/* nranks > 1: map the face neighbours' workspaces.  handles = nranks x 128
+ * bytes, entry r = sfv_peer_handle of rank r (all-gathered by the caller).
+ * ARG: an entry inconsistent with the partition.  CUDA: IPC open failed
+ * (no peer access between the devices). */
+sfv_status sfv_peer_connect(sfv_ctx *ctx, const void *handles);
+
+/* Diagnostic: copy state buffer k (0 = U^n, 1.. = stage buffers of the
+ * tableau) of local block `block`, ghost frame included, to the host:
+ * out[((i+2)*4 + c)*(nj_b+4) + (j+2)] for i in [-2, ni_b+2), c in 0..3,
+ * j in [-2, nj_b+2) (block-local indices; corner ghosts are NaN).
+ * Synchronising.  ARG: block not local or k out of range. */
+sfv_status sfv_debug_block_buffer(sfv_ctx *ctx, int32_t block, int32_t k, double *out);
 
 /* Text of the last error on ctx (ctx-owned, valid until the next call). */
 const char *sfv_last_error(const sfv_ctx *ctx);

@@ -63,6 +63,25 @@ Nccl &nccl() {
     return n;
 }
 
+// A neighbour's state buffers and inbound flags as this process sees them
+// (its own pointers in loopback mode, CUDA-IPC mappings across ranks).
+struct PeerView {
+    double *buf[4] = {nullptr, nullptr, nullptr, nullptr};
+    unsigned long long *flags = nullptr;
+    int PJ = 0, ni = 0, nj = 0;
+};
+
+// 128-byte descriptor one rank publishes for device-initiated halo exchange
+// (sfv_peer_handle / sfv_peer_connect).
+struct PeerHandle {
+    cudaIpcMemHandle_t ipc;      // the allocation containing the workspace
+    int64_t ws_off;              // workspace offset in that allocation
+    int64_t flags_off;           // block's inbound flags, offset in the workspace
+    int64_t buf_off[4];          // state buffers, offsets in the workspace
+    int32_t ni, nj, PJ, block;
+};
+static_assert(sizeof(PeerHandle) == 128, "PeerHandle must be 128 bytes");
+
 struct Block {
     int id = 0, bx = 0, by = 0;
     int i0 = 0, i1 = 0, j0 = 0, j1 = 0, ni = 0, nj = 0, PJ = 0;
@@ -77,6 +96,9 @@ struct Block {
     double *buf[4] = {nullptr, nullptr, nullptr, nullptr};
     double *met = nullptr, *nodes = nullptr, *stage = nullptr, *partials = nullptr;
     double *xs[2] = {nullptr, nullptr}, *xr[2] = {nullptr, nullptr};  // j-cut pack buffers (S, N)
+    unsigned long long *flags = nullptr;  // inbound halo flags [4 * FLAG_STRIDE] (peer mode)
+    unsigned *ecnt = nullptr;             // writer arrival counters [4 * CNT_STRIDE]
+    PeerView pv[4];                       // neighbour per edge (peer mode)
     CUtensorMap tm_buf[4], tm_met;  // 2D TMA descriptors (made at sfv_bind)
     size_t buf_elems() const { return (size_t)(ni + 4) * 4 * PJ + PADD; }
     size_t met_elems() const { return (size_t)(ni + 1) * NMET * PJ + PADD; }
@@ -145,6 +167,10 @@ struct sfv_ctx {
     cudaGraphExec_t gexec = nullptr, gexec_norms = nullptr;  // step; step + norms batch
     bool graph_failed = false;
     ncclComm_t comm = nullptr;
+    int halo = SFV_HALO_COPY;                // halo-exchange mode
+    bool peer_ready = false;                 // sfv_peer_connect done (nranks > 1)
+    unsigned *halo_err = nullptr;            // sticky peer-wait timeout
+    std::vector<void *> ipc_open;            // CUDA-IPC mappings to close
     std::string msg;
     long long einfo[4] = {-1, -1, -1, -1};
 };
@@ -260,7 +286,9 @@ void plan_launches(sfv_ctx *c, Block &b) {
     const bool cw = b.nbr[0] >= 0, ce = b.nbr[1] >= 0;
     const char *ov = getenv("SFV_OVERLAP");
     const bool overlap = !(ov && ov[0] == '0');
-    b.split = overlap && (cw || ce) && b.ni >= 8;
+    // peer mode: one launch per stage; the edge tasks store into the
+    // neighbours' ghost frames themselves
+    b.split = overlap && (cw || ce) && b.ni >= 8 && c->halo != SFV_HALO_PEER;
     int n = 0;
     int lo = 0, hi = b.ni;
     if (b.split) {
@@ -335,6 +363,7 @@ size_t layout(sfv_ctx *c, bool assign) {
         c->err = reinterpret_cast<unsigned long long *>(c->ws + o_misc + 24);
         c->geo_bad = reinterpret_cast<unsigned long long *>(c->ws + o_misc + 32);
         c->done = reinterpret_cast<unsigned *>(c->ws + o_misc + 40);
+        c->halo_err = reinterpret_cast<unsigned *>(c->ws + o_misc + 48);
         c->dt_hist = reinterpret_cast<double *>(c->ws + o_dt);
         c->norm_hist = reinterpret_cast<double *>(c->ws + o_norm);
         c->gbuf = gb ? reinterpret_cast<double *>(c->ws + o_g) : nullptr;
@@ -348,7 +377,7 @@ size_t layout(sfv_ctx *c, bool assign) {
         size_t os = take(sizeof(double) * 4 * (size_t)b.ni * b.nj);
         const int max_cta = (((b.nj + WOUT - 1) / WOUT) * (NSEG_MAX + 2) + WPC - 1) / WPC + 2;
         size_t op = take(sizeof(double) * 8 * (size_t)max_cta * c->pring);
-        size_t ot = take(256);
+        size_t of = take(PEER_SYNC_BYTES);
         size_t ox[4];
         for (int k = 0; k < 4; ++k) ox[k] = take(c->nranks > 1 ? sizeof(double) * 8 * (size_t)b.ni : 0);
         if (assign) {
@@ -361,6 +390,8 @@ size_t layout(sfv_ctx *c, bool assign) {
             b.xs[1] = reinterpret_cast<double *>(c->ws + ox[1]);
             b.xr[0] = reinterpret_cast<double *>(c->ws + ox[2]);
             b.xr[1] = reinterpret_cast<double *>(c->ws + ox[3]);
+            b.flags = reinterpret_cast<unsigned long long *>(c->ws + of);
+            b.ecnt = reinterpret_cast<unsigned *>(c->ws + of + PEER_SYNC_BYTES / 2);
         }
     }
     return off;
@@ -517,7 +548,34 @@ StageArgs make_args(sfv_ctx *c, Block &b, int k) {
     a.stage = k;
     a.nstages = nstages_of(c->cfg.rk);
     a.P = c->P;
+    if (c->halo == SFV_HALO_PEER) {
+        static const int opp[4] = {1, 0, 3, 2};
+        for (int e = 0; e < 4; ++e) {
+            const PeerView &v = b.pv[e];
+            if (b.nbr[e] < 0 || !v.flags) continue;
+            a.peer_out[e] = v.buf[sp.out];
+            a.peer_flag[e] = v.flags + opp[e] * FLAG_STRIDE;
+            a.peer_PJ[e] = v.PJ;
+            a.peer_n[e] = e == 0 ? v.ni : (e == 2 ? v.nj : 0);
+        }
+        a.in_flag = b.flags;
+        a.edge_cnt = b.ecnt;
+        a.halo_err = c->halo_err;
+    }
     return a;
+}
+
+// Tasks of a launch (nseg segments over all rows) that touch edge e: the same
+// predicate as the stage kernel's `touch` (segments at i = 0 / ni; strip 0;
+// strips whose columns reach nj - 1).
+int edge_writers(const Block &b, int nseg, int e) {
+    if (e < 2) return b.nstrips;
+    int strips = 0;
+    for (int s = 0; s < b.nstrips; ++s) {
+        const int j0 = s * WOUT, j1 = std::min(j0 + WOUT, b.nj);
+        strips += e == 2 ? (j0 == 0) : (j1 >= b.nj - 1);
+    }
+    return strips * nseg;
 }
 
 // Norm partials of `count` steps -> history, every local block (first < 0:
@@ -555,7 +613,8 @@ sfv_status enqueue_step(sfv_ctx *c, cudaStream_t st, bool norms_batch) {
             a.row_hi = b.row_hi[q];
             a.nseg = b.lseg[q];
             a.part_base = b.lbase[q];
-            CK(launch_stage(a, sp.mode, k == 1, k == s && cflmode, st));
+            for (int e = 0; e < 4; ++e) a.edge_writers[e] = a.peer_out[e] ? edge_writers(b, a.nseg, e) : 0;
+            CK(launch_stage(a, sp.mode, k == 1, k == s && cflmode, c->halo == SFV_HALO_PEER, st));
             return SFV_OK;
         };
         if (any_split) {
@@ -580,6 +639,7 @@ sfv_status enqueue_step(sfv_ctx *c, cudaStream_t st, bool norms_batch) {
                 if (r != SFV_OK) return r;
             }
         }
+        if (c->halo == SFV_HALO_PEER) continue;  // the stage kernels exchanged the halos
         if (any_split) {
             sfv_status r = exchange_cols(c, sp.out, st);
             if (r != SFV_OK) return r;
@@ -595,6 +655,15 @@ sfv_status enqueue_step(sfv_ctx *c, cudaStream_t st, bool norms_batch) {
 }
 
 sfv_status check_device_error(sfv_ctx *c) {
+    if (c->halo == SFV_HALO_PEER) {
+        unsigned h = 0;
+        CK(cudaMemcpy(&h, c->halo_err, sizeof h, cudaMemcpyDeviceToHost));
+        if (h) {
+            c->have_state = false;
+            return fail(c, SFV_ERR_HALO, "device-initiated halo exchange: a neighbour did not signal within %llu s",
+                        (unsigned long long)20);
+        }
+    }
     unsigned long long e = ~0ull;
     CK(cudaMemcpy(&e, c->err, sizeof e, cudaMemcpyDeviceToHost));
     if (e == ~0ull) return SFV_OK;
@@ -752,7 +821,7 @@ sfv_status sfv_bind(sfv_ctx *c, void *ws, size_t bytes, void *stream) {
     c->nsm = prop.multiProcessorCount;
     int o = 1;
     CK(prepare_stage_kernels());
-    CK(stage_occupancy(M_UN, false, false, fast_path(c->P), &o));
+    CK(stage_occupancy(M_UN, false, false, fast_path(c->P), false, &o));
     c->occ = std::max(1, o);
     CK(cudaEventCreate(&c->ev0));
     CK(cudaEventCreate(&c->ev1));
@@ -801,6 +870,14 @@ sfv_status sfv_set_state(sfv_ctx *c, const double *U) {
     const int nbuf = nbuf_of(c->cfg.rk);
     const int NI = c->cfg.ni;
     int bcfill[4];
+    if (c->halo == SFV_HALO_PEER) {
+        // every rank's earlier steps (which signal into this rank's flags)
+        // complete before any rank resets its flags: an all-reduce barrier here,
+        // and the sigma all-reduce below before anyone steps again
+        if (c->nranks > 1) NK(nccl().AllReduce(c->sig, c->sig, 1, ncclDouble, ncclMax, c->comm, st));
+        for (Block &b : c->blocks) CK(cudaMemsetAsync(b.flags, 0, PEER_SYNC_BYTES, st));
+        CK(cudaMemsetAsync(c->halo_err, 0, sizeof(unsigned), st));
+    }
     CK(cudaMemsetAsync(c->err, 0xff, 8, st));
     for (Block &b : c->blocks) {
         CK(cudaMemcpy2DAsync(b.stage, (size_t)b.ni * 32, U + ((size_t)b.j0 * NI + b.i0) * 4, (size_t)NI * 32,
@@ -829,8 +906,8 @@ sfv_status sfv_set_state(sfv_ctx *c, const double *U) {
     }
     if (!(c->cfg.dt_fixed > 0.0)) {
         for (Block &b : c->blocks) CK(launch_sigma(b.buf[0], b.met, b.ni, b.nj, b.PJ, c->P, c->sig, st));
-        if (c->nranks > 1) NK(nccl().AllReduce(c->sig, c->sig, 2, ncclDouble, ncclMax, c->comm, st));
     }
+    if (c->nranks > 1) NK(nccl().AllReduce(c->sig, c->sig, 2, ncclDouble, ncclMax, c->comm, st));
     CK(cudaStreamSynchronize(st));
     c->steps_enq = 0;
     c->have_state = true;
@@ -1038,6 +1115,109 @@ sfv_status sfv_debug_math(sfv_ctx *c, int32_t which, const double *in, double *o
     return SFV_OK;
 }
 
+sfv_status sfv_peer_handle(sfv_ctx *c, void *out128) {
+    if (!c || !out128) return SFV_ERR_ARG;
+    if (!c->bound) return fail(c, SFV_ERR_SEQUENCE, "sfv_peer_handle before sfv_bind");
+    if (c->nranks < 2 || c->blocks.size() != 1) return fail(c, SFV_ERR_ARG, "sfv_peer_handle needs nranks > 1");
+    static CUresult (*range)(CUdeviceptr *, size_t *, CUdeviceptr) = nullptr;
+    if (!range) {
+        cudaDriverEntryPointQueryResult q;
+        void *p = nullptr;
+        if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &p, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess || !p)
+            return fail(c, SFV_ERR_CUDA, "cuMemGetAddressRange unavailable");
+        range = reinterpret_cast<decltype(range)>(p);
+    }
+    CUdeviceptr base = 0;
+    size_t sz = 0;
+    if (range(&base, &sz, reinterpret_cast<CUdeviceptr>(c->ws)) != CUDA_SUCCESS)
+        return fail(c, SFV_ERR_CUDA, "cuMemGetAddressRange failed on the workspace");
+    PeerHandle h{};
+    CK(cudaIpcGetMemHandle(&h.ipc, reinterpret_cast<void *>(base)));
+    const Block &b = c->blocks[0];
+    h.ws_off = (int64_t)(reinterpret_cast<CUdeviceptr>(c->ws) - base);
+    h.flags_off = reinterpret_cast<uint8_t *>(b.flags) - c->ws;
+    for (int k = 0; k < 4; ++k) h.buf_off[k] = b.buf[k] ? reinterpret_cast<uint8_t *>(b.buf[k]) - c->ws : -1;
+    h.ni = b.ni;
+    h.nj = b.nj;
+    h.PJ = b.PJ;
+    h.block = b.id;
+    memcpy(out128, &h, 128);
+    return SFV_OK;
+}
+
+sfv_status sfv_peer_connect(sfv_ctx *c, const void *handles) {
+    if (!c || !handles) return SFV_ERR_ARG;
+    if (!c->bound) return fail(c, SFV_ERR_SEQUENCE, "sfv_peer_connect before sfv_bind");
+    if (c->nranks < 2 || c->blocks.size() != 1) return fail(c, SFV_ERR_ARG, "sfv_peer_connect needs nranks > 1");
+    if (c->peer_ready) return fail(c, SFV_ERR_SEQUENCE, "already connected");
+    Block &b = c->blocks[0];
+    const PeerHandle *H = static_cast<const PeerHandle *>(handles);
+    for (int e = 0; e < 4; ++e) {
+        if (b.nbr[e] < 0) continue;
+        const PeerHandle &h = H[b.nbr[e]];
+        const bool along_i = e < 2;
+        if (h.block != b.nbr[e] || (along_i ? h.nj != b.nj : h.ni != b.ni) || h.PJ < h.nj + JOFF + 2)
+            return fail(c, SFV_ERR_ARG, "peer handle of block %d inconsistent with the partition", b.nbr[e]);
+        void *p = nullptr;
+        CK(cudaIpcOpenMemHandle(&p, h.ipc, cudaIpcMemLazyEnablePeerAccess));
+        c->ipc_open.push_back(p);
+        uint8_t *ws = static_cast<uint8_t *>(p) + h.ws_off;
+        PeerView &v = b.pv[e];
+        for (int k = 0; k < 4; ++k) v.buf[k] = h.buf_off[k] >= 0 ? reinterpret_cast<double *>(ws + h.buf_off[k]) : nullptr;
+        v.flags = reinterpret_cast<unsigned long long *>(ws + h.flags_off);
+        v.PJ = h.PJ;
+        v.ni = h.ni;
+        v.nj = h.nj;
+    }
+    c->peer_ready = true;
+    return SFV_OK;
+}
+
+sfv_status sfv_set_halo_mode(sfv_ctx *c, int32_t mode) {
+    if (!c) return SFV_ERR_ARG;
+    if (!c->bound) return fail(c, SFV_ERR_SEQUENCE, "sfv_set_halo_mode before sfv_bind");
+    if (mode != SFV_HALO_COPY && mode != SFV_HALO_PEER) return fail(c, SFV_ERR_ARG, "unknown halo mode %d", mode);
+    if (mode == SFV_HALO_PEER && c->nranks > 1 && !c->peer_ready)
+        return fail(c, SFV_ERR_SEQUENCE, "SFV_HALO_PEER across ranks needs sfv_peer_connect first");
+    CK(cudaStreamSynchronize(c->st));
+    c->halo = mode;
+    if (mode == SFV_HALO_PEER && c->nranks == 1)
+        for (Block &b : c->blocks)
+            for (int e = 0; e < 4; ++e) {
+                b.pv[e] = PeerView{};
+                if (b.nbr[e] < 0) continue;
+                const Block &n = *local_block(c, b.nbr[e]);
+                for (int k = 0; k < 4; ++k) b.pv[e].buf[k] = n.buf[k];
+                b.pv[e].flags = n.flags;
+                b.pv[e].PJ = n.PJ;
+                b.pv[e].ni = n.ni;
+                b.pv[e].nj = n.nj;
+            }
+    for (Block &b : c->blocks) {
+        choose_launch(c, b);
+        plan_launches(c, b);
+    }
+    if (c->gexec) cudaGraphExecDestroy(c->gexec);
+    if (c->gexec_norms) cudaGraphExecDestroy(c->gexec_norms);
+    c->gexec = c->gexec_norms = nullptr;
+    c->graph_failed = false;
+    c->have_state = false;  // flags and step counter restart at sfv_set_state
+    return SFV_OK;
+}
+
+sfv_status sfv_debug_block_buffer(sfv_ctx *c, int32_t block, int32_t k, double *out) {
+    if (!c || !out) return SFV_ERR_ARG;
+    if (!c->bound) return fail(c, SFV_ERR_SEQUENCE, "not bound");
+    Block *b = local_block(c, block);
+    if (!b || k < 0 || k >= nbuf_of(c->cfg.rk)) return fail(c, SFV_ERR_ARG, "no local block %d / buffer %d", block, k);
+    CK(cudaStreamSynchronize(c->st));
+    // rows i = -2 .. ni+1, components, columns j = -2 .. nj+1
+    CK(cudaMemcpy2D(out, sizeof(double) * (b->nj + 4), b->buf[k] + (JOFF - 2), sizeof(double) * b->PJ,
+                    sizeof(double) * (b->nj + 4), (size_t)(b->ni + 4) * 4, cudaMemcpyDeviceToHost));
+    return SFV_OK;
+}
+
 const char *sfv_last_error(const sfv_ctx *c) { return c ? c->msg.c_str() : "null ctx"; }
 
 void sfv_destroy(sfv_ctx *c) {
@@ -1050,6 +1230,7 @@ void sfv_destroy(sfv_ctx *c) {
     if (c->ev_comm) cudaEventDestroy(c->ev_comm);
     if (c->comm_st) cudaStreamDestroy(c->comm_st);
     if (c->comm && nccl().ok) nccl().CommDestroy(c->comm);
+    for (void *p : c->ipc_open) cudaIpcCloseMemHandle(p);
     delete c;
 }
 

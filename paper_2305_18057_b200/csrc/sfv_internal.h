@@ -70,8 +70,24 @@ struct StageArgs {
     int bump;               // last launch of the step: record dt_n, clear its sigma slot, advance the counter
     unsigned long long *err;
     int stage, nstages;
+    // device-initiated halo exchange (halo mode SFV_HALO_PEER):
+    // per edge W, E, S, N the neighbour's copy of this stage's output buffer
+    // (NULL = not a peer edge), its pitch and its ni (W) / nj (S), the
+    // neighbour's inbound flag for the shared edge (signalled with the stage
+    // sequence number), this block's own inbound flags and writer arrival
+    // counters, and the number of CTAs of this launch that touch each edge
+    double *peer_out[4];
+    unsigned long long *peer_flag[4];
+    int peer_PJ[4], peer_n[4];
+    unsigned long long *in_flag;  // [4 * FLAG_STRIDE]
+    unsigned *edge_cnt;           // [4 * CNT_STRIDE]
+    int edge_writers[4];
+    unsigned *halo_err;           // sticky: a peer never signalled (timeout)
     Params P;
 };
+constexpr int FLAG_STRIDE = 16;   // u64 per inbound flag (own 128-B line)
+constexpr int CNT_STRIDE = 32;    // u32 per arrival counter
+constexpr size_t PEER_SYNC_BYTES = 1024;  // per block: flags [0, 512), counters [512, 1024)
 
 // Reduction of `count` steps of one block's norm partials into the history:
 // steps first .. first+count-1 (first < 0: the `count` steps before *step_ctr).
@@ -92,9 +108,9 @@ struct MetricsArgs {
 };
 
 // launchers (sfv_kernels.cu); all asynchronous on `st`
-cudaError_t launch_stage(const StageArgs &a, int mode, bool norms, bool dtmax, cudaStream_t st);
+cudaError_t launch_stage(const StageArgs &a, int mode, bool norms, bool dtmax, bool peer, cudaStream_t st);
 cudaError_t launch_norms(const NormsArgs &f, cudaStream_t st);
-cudaError_t stage_occupancy(int mode, bool norms, bool dtmax, bool fast, int *ctas_per_sm);
+cudaError_t stage_occupancy(int mode, bool norms, bool dtmax, bool fast, bool peer, int *ctas_per_sm);
 bool fast_path(const Params &P);
 cudaError_t prepare_stage_kernels();
 size_t stage_smem_bytes(int mode);

@@ -68,6 +68,48 @@ __device__ __forceinline__ void elect_tma_s(unsigned dst, const CUtensorMap *map
 __device__ __forceinline__ void pdl_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 
+// ------------------------------------------ device-initiated halo exchange
+// System-scope acquire / release on flags that a peer GPU writes over
+// NVLink (or another block of this process in loopback peer mode).
+__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long *p) {
+    unsigned long long v;
+    asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release_sys(unsigned long long *p, unsigned long long v) {
+    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned atom_add_acq_rel_gpu(unsigned *p, unsigned v) {
+    unsigned old;
+    asm volatile("atom.add.acq_rel.gpu.global.u32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
+    return old;
+}
+__device__ __forceinline__ unsigned long long globaltimer_ns() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+constexpr unsigned long long HALO_TIMEOUT_NS = 20ull * 1000 * 1000 * 1000;
+// Wait (all lanes) until the neighbour has published stage sequence >= need
+// for this edge, then make its data visible to the async (TMA) proxy.  A
+// neighbour that never signals sets the sticky halo error after
+// HALO_TIMEOUT_NS instead of hanging the device; later waits then return at
+// once (the step's results are invalid and sfv_sync reports SFV_ERR_HALO).
+__device__ __forceinline__ void wait_flag(const unsigned long long *f, unsigned long long need, unsigned *herr) {
+    if (ld_acquire_sys(f) < need) {
+        const unsigned long long t0 = globaltimer_ns();
+        while (ld_acquire_sys(f) < need) {
+            if (*(volatile unsigned *)herr) break;
+            if (globaltimer_ns() - t0 > HALO_TIMEOUT_NS) {
+                atomicExch(herr, 1u);
+                break;
+            }
+            __nanosleep(100);
+        }
+    }
+    asm volatile("fence.proxy.async.global;" ::: "memory");
+}
+
 // Fast reciprocal / reciprocal square root: MUFU seed + one cubic-convergent
 // correction (relative error ~ seed^3 << 2^-53, i.e. within ~1 ulp).
 __device__ __forceinline__ double frcp(double d) {
@@ -250,7 +292,8 @@ constexpr int SFV_MINB = SFV_MIN_WARPS / WPC;
 #endif
 constexpr int kRowUnroll = SFV_UNROLL;
 
-template <int MODE, bool NORMS, bool DTMAX, bool FAST>
+
+template <int MODE, bool NORMS, bool DTMAX, bool FAST, bool PEER>
 __global__ void __launch_bounds__(NT, SFV_MINB) stage_kernel(const __grid_constant__ StageArgs a) {
     using TR = StageTraits<MODE>;
     extern __shared__ __align__(128) double smem[];
@@ -296,12 +339,36 @@ __global__ void __launch_bounds__(NT, SFV_MINB) stage_kernel(const __grid_consta
             jflux[k] = col >= j0 && col <= j1;
         }
         auto writes_ghost = [&](int e) { return a.bc[e] == E_SLIP || a.bc[e] == E_OUTFLOW; };
+        // edges whose ghost frame this task reads (and, for peer edges, whose
+        // neighbour ghost frame it writes): segments at i = 0 / ni, strips
+        // whose staged columns reach j = -1 / nj
         const bool ghost_sn = (writes_ghost(2) && j0 == 0) || (writes_ghost(3) && j1 >= a.nj - 1);
         const bool ghost_w = writes_ghost(0), ghost_e = writes_ghost(1);
         const int nrows = a.row_hi - a.row_lo;
         const int i_start = a.row_lo + (int)(((long long)nrows * seg) / a.nseg);
         const int i_end = a.row_lo + (int)(((long long)nrows * (seg + 1)) / a.nseg);
         const int r0 = i_start - 2, r_last = i_end + 1;  // stencil rows
+        unsigned touch = 0;  // bit e: peer edge e (W, E, S, N) touched by this task
+        if constexpr (PEER) {
+            touch = (a.peer_out[0] != nullptr && i_start == 0 ? 1u : 0u) |
+                    (a.peer_out[1] != nullptr && i_end == a.ni ? 2u : 0u) |
+                    (a.peer_out[2] != nullptr && j0 == 0 ? 4u : 0u) |
+                    (a.peer_out[3] != nullptr && j1 >= a.nj - 1 ? 8u : 0u);
+        }
+        // j-cut peer columns of this lane, bits 2k (S: columns 0, 1) and 2k+1
+        // (N: columns nj-2, nj-1), precomputed once (a combined in-loop test
+        // `(touch & 12) && is_out` was mis-evaluated for tasks touching both S
+        // and N by ptxas 12.9 in the peer variants: stores skipped, caught by
+        // tests/test_gpu_peer.py with py = 3)
+        unsigned pcol = 0;
+        if constexpr (PEER) {
+#pragma unroll
+            for (int k = 0; k < CPL; ++k) {
+                const int col = jc + k;
+                if ((touch & 4u) && is_out[k] && col <= 1) pcol |= 1u << (2 * k);
+                if ((touch & 8u) && is_out[k] && col >= a.nj - 2) pcol |= 2u << (2 * k);
+            }
+        }
         const int m0 = i_start - 1, m_last = i_end - 1;  // metric rows
         constexpr unsigned ROWB = WROW * 8u;
 
@@ -352,6 +419,14 @@ __global__ void __launch_bounds__(NT, SFV_MINB) stage_kernel(const __grid_consta
         // its waiting CTAs cannot hold slots this grid still needs
         pdl_launch_dependents();
         read_step();
+        if constexpr (PEER) {
+            // the stage input's ghost layers on a peer edge are the neighbour's
+            // previous-stage edge layers: wait for its signal (sequence n*s + k - 1)
+            const unsigned long long need = (unsigned long long)(n * a.nstages + a.stage - 1);
+#pragma unroll
+            for (int e = 0; e < 4; ++e)
+                if (touch & (1u << e)) wait_flag(a.in_flag + e * FLAG_STRIDE, need, a.halo_err);
+        }
         for (int r = r0; r <= r0 + 3 && r <= r_last; ++r) issue_w(r);
         issue_p(i_start);
 
@@ -557,6 +632,13 @@ __global__ void __launch_bounds__(NT, SFV_MINB) stage_kernel(const __grid_consta
                         store4(a.out, PJ, a.ni + 1, jk, U);
                     }
                 }
+                if constexpr (PEER) {
+                    // peer edges: the new state's 2 edge layers go straight into the
+                    // neighbour's ghost frame ("boundary data exchange")
+                    // (j-cut columns here; i-cut rows after the loop)
+                    if (pcol & (1u << (2 * k))) store4(a.peer_out[2], a.peer_PJ[2], v, a.peer_n[2] + jk, U);
+                    if (pcol & (2u << (2 * k))) store4(a.peer_out[3], a.peer_PJ[3], v, jk - a.nj, U);
+                }
                 if constexpr (NORMS) {
 #pragma unroll
                     for (int c = 0; c < 4; ++c) {
@@ -610,6 +692,46 @@ __global__ void __launch_bounds__(NT, SFV_MINB) stage_kernel(const __grid_consta
                         if (!((u0 > 0.0) & (2.0 * u0 * u3 > fma(u1, u1, u2 * u2))))
                             atomicMin(a.err,
                                       err_key(n, a.nstages, a.stage, 1, (long long)(a.gj0 + jk) * a.NI + a.gi0 + v));
+                    }
+                }
+            }
+        }
+        if constexpr (PEER) {
+            // arrival of this task on every peer edge it touches; the last of
+            // the launch's writers on an edge publishes the stage sequence
+            // n*s + k to the neighbour's inbound flag (release, system scope)
+            if (touch & 3u) {
+                // i-cut edge rows: each lane forwards the 2 rows it just stored
+                // (its own writes, L2-resident) to the neighbour's ghost rows
+                const int r_lo = (touch & 1u) ? 0 : a.ni - 2, r_hi = (touch & 2u) ? a.ni : 2;
+#pragma unroll
+                for (int k = 0; k < CPL; ++k) {
+                    if (!is_out[k]) continue;
+                    const int jk = jc + k;
+                    for (int v = r_lo; v < r_hi; ++v) {
+                        if (v >= 2 && v < a.ni - 2) continue;
+                        const double *src = a.out + (size_t)((v + 2) * 4) * PJ + (jk + JOFF);
+                        double u[4];
+#pragma unroll
+                        for (int c = 0; c < 4; ++c) u[c] = src[(size_t)c * PJ];
+                        if ((touch & 1u) && v <= 1) store4(a.peer_out[0], a.peer_PJ[0], a.peer_n[0] + v, jk, u);
+                        if ((touch & 2u) && v >= a.ni - 2) store4(a.peer_out[1], a.peer_PJ[1], v - a.ni, jk, u);
+                    }
+                }
+            }
+            if (touch) {  // warp-uniform
+                __threadfence_system();  // every lane: its peer stores before the arrival
+                __syncwarp();
+                if (lane == 0) {
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) {
+                        if (!(touch & (1u << e))) continue;
+                        unsigned *cnt = a.edge_cnt + e * CNT_STRIDE;
+                        if (atom_add_acq_rel_gpu(cnt, 1u) == (unsigned)a.edge_writers[e] - 1u) {
+                            *cnt = 0u;
+                            __threadfence_system();
+                            st_release_sys(a.peer_flag[e], (unsigned long long)(n * a.nstages + a.stage));
+                        }
                     }
                 }
             }
@@ -719,9 +841,9 @@ cudaError_t launch_norms(const NormsArgs &f, cudaStream_t st) {
     return cudaGetLastError();
 }
 
-template <int MODE, bool NORMS, bool DTMAX, bool FAST>
+template <int MODE, bool NORMS, bool DTMAX, bool FAST, bool PEER>
 static cudaError_t launch_t(const StageArgs &a, cudaStream_t st) {
-    auto k = stage_kernel<MODE, NORMS, DTMAX, FAST>;
+    auto k = stage_kernel<MODE, NORMS, DTMAX, FAST, PEER>;
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3((a.nstrips * a.nseg + WPC - 1) / WPC);
     cfg.blockDim = dim3(NT);
@@ -735,48 +857,52 @@ static cudaError_t launch_t(const StageArgs &a, cudaStream_t st) {
     return cudaLaunchKernelEx(&cfg, k, a);
 }
 
-template <int MODE, bool NORMS, bool DTMAX, bool FAST>
+template <int MODE, bool NORMS, bool DTMAX, bool FAST, bool PEER>
 static cudaError_t occ_t(int *n) {
-    auto k = stage_kernel<MODE, NORMS, DTMAX, FAST>;
+    auto k = stage_kernel<MODE, NORMS, DTMAX, FAST, PEER>;
     const size_t sm = stage_smem<MODE>();
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     if (e != cudaSuccess) return e;
     return cudaOccupancyMaxActiveBlocksPerMultiprocessor(n, k, NT, sm);
 }
 
-#define SFV_DISPATCH_F(FN, F, ...)                                                    \
-    switch (mode * 4 + (norms ? 2 : 0) + (dtmax ? 1 : 0)) {                          \
-        case M_OWN * 4 + 2: return FN<M_OWN, true, false, F>(__VA_ARGS__);           \
-        case M_OWN * 4 + 0: return FN<M_OWN, false, false, F>(__VA_ARGS__);          \
-        case M_UN * 4 + 0: return FN<M_UN, false, false, F>(__VA_ARGS__);            \
-        case M_UN * 4 + 1: return FN<M_UN, false, true, F>(__VA_ARGS__);             \
-        case M_RK4F * 4 + 1: return FN<M_RK4F, false, true, F>(__VA_ARGS__);         \
-        case M_RK4F * 4 + 0: return FN<M_RK4F, false, false, F>(__VA_ARGS__);        \
-        case M_HEUNF * 4 + 1: return FN<M_HEUNF, false, true, F>(__VA_ARGS__);       \
-        case M_HEUNF * 4 + 0: return FN<M_HEUNF, false, false, F>(__VA_ARGS__);      \
-        default: return cudaErrorInvalidValue;                                       \
+#define SFV_DISPATCH_F(FN, F, Q, ...)                                                  \
+    switch (mode * 4 + (norms ? 2 : 0) + (dtmax ? 1 : 0)) {                              \
+        case M_OWN * 4 + 2: return FN<M_OWN, true, false, F, Q>(__VA_ARGS__);            \
+        case M_OWN * 4 + 0: return FN<M_OWN, false, false, F, Q>(__VA_ARGS__);           \
+        case M_UN * 4 + 0: return FN<M_UN, false, false, F, Q>(__VA_ARGS__);             \
+        case M_UN * 4 + 1: return FN<M_UN, false, true, F, Q>(__VA_ARGS__);              \
+        case M_RK4F * 4 + 1: return FN<M_RK4F, false, true, F, Q>(__VA_ARGS__);          \
+        case M_RK4F * 4 + 0: return FN<M_RK4F, false, false, F, Q>(__VA_ARGS__);         \
+        case M_HEUNF * 4 + 1: return FN<M_HEUNF, false, true, F, Q>(__VA_ARGS__);        \
+        case M_HEUNF * 4 + 0: return FN<M_HEUNF, false, false, F, Q>(__VA_ARGS__);       \
+        default: return cudaErrorInvalidValue;                                           \
     }
-#define SFV_DISPATCH(FN, ...)                                                         \
-    if (fast) {                                                                       \
-        SFV_DISPATCH_F(FN, true, __VA_ARGS__)                                         \
-    } else {                                                                          \
-        SFV_DISPATCH_F(FN, false, __VA_ARGS__)                                        \
+#define SFV_DISPATCH(FN, ...)                                                             \
+    if (fast) {                                                                           \
+        if (peer) { SFV_DISPATCH_F(FN, true, true, __VA_ARGS__) }                         \
+        else { SFV_DISPATCH_F(FN, true, false, __VA_ARGS__) }                             \
+    } else {                                                                              \
+        if (peer) { SFV_DISPATCH_F(FN, false, true, __VA_ARGS__) }                        \
+        else { SFV_DISPATCH_F(FN, false, false, __VA_ARGS__) }                            \
     }
 
 // fast = bounded van Albada with kappa = -1 (the default scheme, reading A-R3/A-R7)
 bool fast_path(const Params &P) { return P.limiter == 1 && P.c2 == 0.0; }
-cudaError_t launch_stage(const StageArgs &a, int mode, bool norms, bool dtmax, cudaStream_t st) {
+cudaError_t launch_stage(const StageArgs &a, int mode, bool norms, bool dtmax, bool peer, cudaStream_t st) {
     const bool fast = fast_path(a.P);
     SFV_DISPATCH(launch_t, a, st)
 }
-cudaError_t stage_occupancy(int mode, bool norms, bool dtmax, bool fast, int *n) { SFV_DISPATCH(occ_t, n) }
+cudaError_t stage_occupancy(int mode, bool norms, bool dtmax, bool fast, bool peer, int *n) {
+    SFV_DISPATCH(occ_t, n)
+}
 cudaError_t prepare_stage_kernels() {
     const int variants[8][3] = {{M_OWN, 1, 0}, {M_OWN, 0, 0}, {M_UN, 0, 0}, {M_UN, 0, 1},
                                 {M_RK4F, 0, 1}, {M_RK4F, 0, 0}, {M_HEUNF, 0, 1}, {M_HEUNF, 0, 0}};
     for (auto &v : variants)
-        for (int f = 0; f < 2; ++f) {
+        for (int f = 0; f < 4; ++f) {
             int n = 0;
-            cudaError_t e = stage_occupancy(v[0], v[1] != 0, v[2] != 0, f != 0, &n);
+            cudaError_t e = stage_occupancy(v[0], v[1] != 0, v[2] != 0, (f & 1) != 0, (f & 2) != 0, &n);
             if (e != cudaSuccess) return e;
         }
     return cudaSuccess;

@@ -17,15 +17,18 @@ from . import inputs as _inputs
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("SFV_LIB") or os.path.join(HERE, "libsfv.so")  # SFV_LIB: A/B builds only
 
-OK, ERR_ARG, ERR_GEOMETRY, ERR_STATE, ERR_SEQUENCE, ERR_CUDA, ERR_NCCL, ERR_OOM, ERR_UNSUPPORTED = range(9)
-_NAMES = ["OK", "ARG", "GEOMETRY", "STATE", "SEQUENCE", "CUDA", "NCCL", "OOM", "UNSUPPORTED"]
+OK, ERR_ARG, ERR_GEOMETRY, ERR_STATE, ERR_SEQUENCE, ERR_CUDA, ERR_NCCL, ERR_OOM, ERR_UNSUPPORTED, ERR_HALO = range(10)
+_NAMES = ["OK", "ARG", "GEOMETRY", "STATE", "SEQUENCE", "CUDA", "NCCL", "OOM", "UNSUPPORTED", "HALO"]
+HALO_COPY, HALO_PEER = 0, 1
 
 # every entry point declared in include/sfv.h
 ABI_SYMBOLS = ["sfv_create", "sfv_partition", "sfv_nccl_unique_id", "sfv_partition_map", "sfv_halo_plan",
                "sfv_split",
                "sfv_workspace_size", "sfv_bind", "sfv_set_state", "sfv_step", "sfv_sync", "sfv_steps_done",
                "sfv_get_residual_norms", "sfv_get_dt", "sfv_get_state", "sfv_error_info", "sfv_launch_info",
-               "sfv_debug_math", "sfv_last_error", "sfv_destroy"]
+               "sfv_debug_math", "sfv_set_halo_mode", "sfv_peer_handle", "sfv_peer_connect",
+               "sfv_debug_block_buffer",
+               "sfv_last_error", "sfv_destroy"]
 
 
 class SfvError(RuntimeError):
@@ -77,6 +80,10 @@ def lib():
         L.sfv_error_info.argtypes = [_VP, _I64]
         L.sfv_launch_info.argtypes = [_VP, _I32]
         L.sfv_debug_math.argtypes = [_VP, C.c_int32, _VP, _VP, C.c_int64]
+        L.sfv_set_halo_mode.argtypes = [_VP, C.c_int32]
+        L.sfv_peer_handle.argtypes = [_VP, _VP]
+        L.sfv_peer_connect.argtypes = [_VP, _VP]
+        L.sfv_debug_block_buffer.argtypes = [_VP, C.c_int32, C.c_int32, _D]
         L.sfv_last_error.argtypes = [_VP]
         L.sfv_last_error.restype = C.c_char_p
         L.sfv_destroy.argtypes = [_VP]
@@ -144,6 +151,7 @@ class Solver:
             raise SfvError(st, msg, info)
         self._h = h
         self.px, self.py = px, py
+        self.rank, self.nranks = rank, nranks
         wxa = None if wx is None else np.ascontiguousarray(wx, np.int32)
         wya = None if wy is None else np.ascontiguousarray(wy, np.int32)
         idbuf = None
@@ -183,6 +191,30 @@ class Solver:
         self._check(lib().sfv_bind(self._h, C.c_void_p(self.ws.data_ptr()), n.value,
                                    C.c_void_p(stream.cuda_stream)))
         return n.value
+
+    def set_halo_mode(self, mode):
+        """sfv_set_halo_mode; call set_state afterwards."""
+        self._check(lib().sfv_set_halo_mode(self._h, int(mode)))
+
+    def peer_handle(self):
+        buf = (C.c_char * 128)()
+        self._check(lib().sfv_peer_handle(self._h, C.cast(buf, _VP)))
+        return bytes(buf)
+
+    def peer_connect(self, handles):
+        """handles: list of nranks 128-byte descriptors (rank order)."""
+        blob = C.create_string_buffer(b"".join(bytes(h) for h in handles), 128 * len(handles))
+        self._check(lib().sfv_peer_connect(self._h, C.cast(blob, _VP)))
+
+    def enable_peer_halo(self, group=None):
+        """Device-initiated halo exchange (SFV_HALO_PEER).  With nranks > 1 the
+        128-byte descriptors are all-gathered over torch.distributed first."""
+        if self.nranks > 1:
+            import torch.distributed as dist
+            hs = [None] * self.nranks
+            dist.all_gather_object(hs, self.peer_handle(), group=group)
+            self.peer_connect(hs)
+        self.set_halo_mode(HALO_PEER)
 
     def partition_map(self, block):
         out = np.zeros(8, np.int32)
@@ -249,6 +281,15 @@ class Solver:
     def debug_math(self, which, x_dev, out_dev):
         self._check(lib().sfv_debug_math(self._h, which, C.c_void_p(x_dev.data_ptr()),
                                          C.c_void_p(out_dev.data_ptr()), x_dev.numel()))
+
+    def block_buffer(self, block, k):
+        """Diagnostic: state buffer k of local block `block` with its ghost
+        frame, as an array [ni_b+4, 4, nj_b+4] (index i+2, c, j+2)."""
+        m = self.partition_map(block)
+        nib, njb = int(m[1] - m[0]), int(m[3] - m[2])
+        out = np.empty((nib + 4, 4, njb + 4))
+        self._check(lib().sfv_debug_block_buffer(self._h, block, k, _dp(out)))
+        return out
 
     @property
     def error_info(self):

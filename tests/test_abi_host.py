@@ -103,3 +103,17 @@ def test_bind_without_gpu_fails_loudly():
     with pytest.raises(sfv.SfvError) as ei:
         s.bind()
     assert ei.value.code == sfv.ERR_CUDA
+
+
+def test_halo_mode_calls_need_bind():
+    """sfv_set_halo_mode / sfv_peer_handle / sfv_peer_connect before sfv_bind
+    are sequence errors (host-side checks, no device needed)."""
+    import ctypes as C
+    X, Y = I.ramp_nodes(8, 4, 30.0)
+    s = sfv.Solver(I.default_config(8, 4), X, Y, px=2, bind=False)
+    L = sfv.lib()
+    assert L.sfv_set_halo_mode(s._h, sfv.HALO_PEER) == sfv.ERR_SEQUENCE
+    buf = (C.c_char * 128)()
+    assert L.sfv_peer_handle(s._h, C.cast(buf, C.c_void_p)) == sfv.ERR_SEQUENCE
+    assert L.sfv_peer_connect(s._h, C.cast(buf, C.c_void_p)) == sfv.ERR_SEQUENCE
+    assert L.sfv_peer_handle(None, C.cast(buf, C.c_void_p)) == sfv.ERR_ARG
