@@ -1,10 +1,18 @@
-# A/B round: parity subset, bench for each library variant, ncu on the default build
+# A/B of two libsfv builds on C2 and C3: gpu_ab.sh TAG VARIANT_A VARIANT_B  (variant "" = libsfv.so)
+TAG=${1:-ab}; A=${2:-base}; B=${3:-}
 set -x
-timeout 300 python __graft_entry__.py smoke > gpurun_out/smoke3.log 2>&1; echo rc=$? >> gpurun_out/smoke3.log
-timeout 900 python -m pytest tests -m gpu -q -x --timeout=600 -p no:cacheprovider > gpurun_out/gpu_tests3.log 2>&1; echo rc=$? >> gpurun_out/gpu_tests3.log
-for v in "" b3; do
-  if [ -n "$v" ]; then export SFV_LIB=$PWD/paper_2305_18057_b200/libsfv_$v.so; else unset SFV_LIB; fi
-  timeout 300 python bench.py --no-cpu-baseline --no-e2e > gpurun_out/bench_ab_${v:-b4}.json 2> gpurun_out/bench_ab_${v:-b4}.err
+B_="python bench.py --no-cpu-baseline --no-e2e"
+lib() { if [ -z "$1" ]; then echo paper_2305_18057_b200/libsfv.so; else echo paper_2305_18057_b200/libsfv_$1.so; fi; }
+for rep in 1 2; do
+for v in "$A" "$B"; do
+  n=${v:-new}
+  SFV_LIB=$(lib "$v") timeout 300 $B_ --steps 3000 > gpurun_out/ab_${TAG}_c2_${n}_$rep.json 2>&1
+  SFV_LIB=$(lib "$v") timeout 300 $B_ --workload C3 --steps 60 --warmup 5 > gpurun_out/ab_${TAG}_c3_${n}_$rep.json 2>&1
 done
-unset SFV_LIB
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:stage_kernel -s 40 -c 4 -o gpurun_out/prof_stage3 python bench.py --steps 20 --warmup 10 --no-cpu-baseline --no-e2e > gpurun_out/ncu_full3.log 2>&1
+done
+for f in gpurun_out/ab_${TAG}_*.json; do python -c "
+import json
+L=[l for l in open('$f').read().splitlines() if l.startswith('{')]
+d=json.loads(L[-1]) if L else {}
+print('$f', round(d.get('value',0)), d.get('clocks',{}).get('sm_mhz'), d.get('clocks',{}).get('reasons'))
+"; done > gpurun_out/ab_${TAG}_summary.txt
