@@ -73,7 +73,9 @@ typedef enum { SFV_RK4_CLASSIC = 0, SFV_RK2_HEUN = 1, SFV_RK4_JAMESON = 2 } sfv_
  *          state's 2 edge layers straight into the neighbour's ghost frame
  *          (loopback: same device; ranks: CUDA-IPC mapping over NVLink) and
  *          publish the stage sequence number to the neighbour's inbound flag;
- *          the neighbour's edge tasks wait on it before staging ghosts. */
+ *          the neighbour's edge tasks wait on it before staging ghosts.  With
+ *          nranks <= 32 the CFL max across ranks also goes through peer
+ *          memory (no per-step NCCL call). */
 typedef enum { SFV_HALO_COPY = 0, SFV_HALO_PEER = 1 } sfv_halo;
 
 typedef struct {

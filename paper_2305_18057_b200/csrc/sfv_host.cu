@@ -171,6 +171,11 @@ struct sfv_ctx {
     bool peer_ready = false;                 // sfv_peer_connect done (nranks > 1)
     unsigned *halo_err = nullptr;            // sticky peer-wait timeout
     std::vector<void *> ipc_open;            // CUDA-IPC mappings to close
+    bool sig_dev = false;                    // dt max across ranks through peer memory (peer mode)
+    double *sig_tab = nullptr;               // [2][SIG_RANKS_MAX]
+    unsigned long long *sig_flag = nullptr;  // [SIG_RANKS_MAX]
+    double **rtab = nullptr;                 // device array [nranks]
+    unsigned long long **rflag = nullptr;    // device array [nranks]
     std::string msg;
     long long einfo[4] = {-1, -1, -1, -1};
 };
@@ -351,7 +356,7 @@ size_t layout(sfv_ctx *c, bool assign) {
     const int cap = (int)c->cfg.max_history;
     const int nbuf = nbuf_of(c->cfg.rk);
     c->pring = std::min(32, cap);
-    size_t o_misc = take(256);
+    size_t o_misc = take(MISC_BYTES);
     size_t o_dt = take(sizeof(double) * cap);
     size_t o_norm = take(sizeof(double) * (size_t)cap * c->nblocks_total * 8);
     size_t gb = 0;
@@ -364,6 +369,10 @@ size_t layout(sfv_ctx *c, bool assign) {
         c->geo_bad = reinterpret_cast<unsigned long long *>(c->ws + o_misc + 32);
         c->done = reinterpret_cast<unsigned *>(c->ws + o_misc + 40);
         c->halo_err = reinterpret_cast<unsigned *>(c->ws + o_misc + 48);
+        c->sig_tab = reinterpret_cast<double *>(c->ws + o_misc + MISC_SIGTAB);
+        c->sig_flag = reinterpret_cast<unsigned long long *>(c->ws + o_misc + MISC_SIGFLAG);
+        c->rtab = reinterpret_cast<double **>(c->ws + o_misc + MISC_RTAB);
+        c->rflag = reinterpret_cast<unsigned long long **>(c->ws + o_misc + MISC_RFLAG);
         c->dt_hist = reinterpret_cast<double *>(c->ws + o_dt);
         c->norm_hist = reinterpret_cast<double *>(c->ws + o_norm);
         c->gbuf = gb ? reinterpret_cast<double *>(c->ws + o_g) : nullptr;
@@ -561,6 +570,14 @@ StageArgs make_args(sfv_ctx *c, Block &b, int k) {
         a.in_flag = b.flags;
         a.edge_cnt = b.ecnt;
         a.halo_err = c->halo_err;
+        if (c->sig_dev) {
+            a.sig_ranks = c->nranks;
+            a.rank = c->rank;
+            a.sig_tab = c->sig_tab;
+            a.sig_flag = c->sig_flag;
+            a.rtab = c->rtab;
+            a.rflag = c->rflag;
+        }
     }
     return a;
 }
@@ -649,7 +666,10 @@ sfv_status enqueue_step(sfv_ctx *c, cudaStream_t st, bool norms_batch) {
             if (r != SFV_OK) return r;
         }
     }
-    if (c->nranks > 1 && cflmode) NK(nccl().AllReduce(c->sig, c->sig, 2, ncclDouble, ncclMax, c->comm, st));
+    // dt max across ranks: in the bump CTA through peer memory (peer mode), else NCCL
+    const bool dev_dt = c->halo == SFV_HALO_PEER && c->sig_dev;
+    if (c->nranks > 1 && cflmode && !dev_dt)
+        NK(nccl().AllReduce(c->sig, c->sig, 2, ncclDouble, ncclMax, c->comm, st));
     if (norms_batch) return enqueue_norms(c, -1, c->pring, st);
     return SFV_OK;
 }
@@ -876,6 +896,7 @@ sfv_status sfv_set_state(sfv_ctx *c, const double *U) {
         // and the sigma all-reduce below before anyone steps again
         if (c->nranks > 1) NK(nccl().AllReduce(c->sig, c->sig, 1, ncclDouble, ncclMax, c->comm, st));
         for (Block &b : c->blocks) CK(cudaMemsetAsync(b.flags, 0, PEER_SYNC_BYTES, st));
+        CK(cudaMemsetAsync(c->sig_flag, 0, sizeof(unsigned long long) * SIG_RANKS_MAX, st));
         CK(cudaMemsetAsync(c->halo_err, 0, sizeof(unsigned), st));
     }
     CK(cudaMemsetAsync(c->err, 0xff, 8, st));
@@ -908,6 +929,9 @@ sfv_status sfv_set_state(sfv_ctx *c, const double *U) {
         for (Block &b : c->blocks) CK(launch_sigma(b.buf[0], b.met, b.ni, b.nj, b.PJ, c->P, c->sig, st));
     }
     if (c->nranks > 1) NK(nccl().AllReduce(c->sig, c->sig, 2, ncclDouble, ncclMax, c->comm, st));
+    if (c->halo == SFV_HALO_PEER && c->sig_dev)  // every rank's slot 0 = the global sigma_0 (flags = 0)
+        for (int r = 0; r < c->nranks; ++r)
+            CK(cudaMemcpyAsync(c->sig_tab + r, c->sig, sizeof(double), cudaMemcpyDeviceToDevice, st));
     CK(cudaStreamSynchronize(st));
     c->steps_enq = 0;
     c->have_state = true;
@@ -1153,22 +1177,48 @@ sfv_status sfv_peer_connect(sfv_ctx *c, const void *handles) {
     if (c->peer_ready) return fail(c, SFV_ERR_SEQUENCE, "already connected");
     Block &b = c->blocks[0];
     const PeerHandle *H = static_cast<const PeerHandle *>(handles);
+    for (int r = 0; r < c->nranks; ++r)
+        if (H[r].block != r) return fail(c, SFV_ERR_ARG, "peer handle %d names block %d", r, H[r].block);
+    // every other rank's workspace, mapped once (face neighbours: halo
+    // stores; all ranks: the dt table)
+    const bool all = c->nranks <= SIG_RANKS_MAX;
+    std::vector<uint8_t *> ws(c->nranks, nullptr);
+    ws[c->rank] = c->ws;
+    for (int r = 0; r < c->nranks; ++r) {
+        if (r == c->rank) continue;
+        bool face = false;
+        for (int e = 0; e < 4; ++e) face |= b.nbr[e] == r;
+        if (!face && !all) continue;
+        void *p = nullptr;
+        CK(cudaIpcOpenMemHandle(&p, H[r].ipc, cudaIpcMemLazyEnablePeerAccess));
+        c->ipc_open.push_back(p);
+        ws[r] = static_cast<uint8_t *>(p) + H[r].ws_off;
+    }
     for (int e = 0; e < 4; ++e) {
         if (b.nbr[e] < 0) continue;
         const PeerHandle &h = H[b.nbr[e]];
         const bool along_i = e < 2;
-        if (h.block != b.nbr[e] || (along_i ? h.nj != b.nj : h.ni != b.ni) || h.PJ < h.nj + JOFF + 2)
+        if ((along_i ? h.nj != b.nj : h.ni != b.ni) || h.PJ < h.nj + JOFF + 2)
             return fail(c, SFV_ERR_ARG, "peer handle of block %d inconsistent with the partition", b.nbr[e]);
-        void *p = nullptr;
-        CK(cudaIpcOpenMemHandle(&p, h.ipc, cudaIpcMemLazyEnablePeerAccess));
-        c->ipc_open.push_back(p);
-        uint8_t *ws = static_cast<uint8_t *>(p) + h.ws_off;
+        uint8_t *w = ws[b.nbr[e]];
         PeerView &v = b.pv[e];
-        for (int k = 0; k < 4; ++k) v.buf[k] = h.buf_off[k] >= 0 ? reinterpret_cast<double *>(ws + h.buf_off[k]) : nullptr;
-        v.flags = reinterpret_cast<unsigned long long *>(ws + h.flags_off);
+        for (int k = 0; k < 4; ++k) v.buf[k] = h.buf_off[k] >= 0 ? reinterpret_cast<double *>(w + h.buf_off[k]) : nullptr;
+        v.flags = reinterpret_cast<unsigned long long *>(w + h.flags_off);
         v.PJ = h.PJ;
         v.ni = h.ni;
         v.nj = h.nj;
+    }
+    if (all) {
+        std::vector<double *> t(c->nranks);
+        std::vector<unsigned long long *> f(c->nranks);
+        for (int r = 0; r < c->nranks; ++r) {
+            t[r] = reinterpret_cast<double *>(ws[r] + MISC_SIGTAB);
+            f[r] = reinterpret_cast<unsigned long long *>(ws[r] + MISC_SIGFLAG);
+        }
+        CK(cudaMemcpy(c->rtab, t.data(), sizeof(double *) * c->nranks, cudaMemcpyHostToDevice));
+        CK(cudaMemcpy(c->rflag, f.data(), sizeof(unsigned long long *) * c->nranks, cudaMemcpyHostToDevice));
+        const char *ev = getenv("SFV_DEVICE_DT");
+        c->sig_dev = !(ev && ev[0] == '0');
     }
     c->peer_ready = true;
     return SFV_OK;

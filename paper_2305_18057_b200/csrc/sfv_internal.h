@@ -83,11 +83,26 @@ struct StageArgs {
     unsigned *edge_cnt;           // [4 * CNT_STRIDE]
     int edge_writers[4];
     unsigned *halo_err;           // sticky: a peer never signalled (timeout)
+    // device-side CFL max across ranks (peer mode, nranks > 1):
+    // every rank's sigma of step n lands in slot n&1 of each rank's table and
+    // is flagged with n; stage kernels take dt_n = cfl / max_r table[n&1][r]
+    int sig_ranks, rank;          // 0 = off (local sigma: one rank, or NCCL all-reduce)
+    double *sig_tab;              // local [2][SIG_RANKS_MAX]
+    unsigned long long *sig_flag; // local [SIG_RANKS_MAX]: rank r published slot for step >= value
+    double *const *rtab;          // [sig_ranks] every rank's sig_tab (mapped; own included)
+    unsigned long long *const *rflag;  // [sig_ranks] every rank's sig_flag
     Params P;
 };
 constexpr int FLAG_STRIDE = 16;   // u64 per inbound flag (own 128-B line)
 constexpr int CNT_STRIDE = 32;    // u32 per arrival counter
-constexpr size_t PEER_SYNC_BYTES = 1024;  // per block: flags [0, 512), counters [512, 1024)
+constexpr size_t PEER_SYNC_BYTES = 1024;
+constexpr int SIG_RANKS_MAX = 32;
+// workspace misc region (same offsets on every rank)
+constexpr size_t MISC_BYTES = 2048;
+constexpr size_t MISC_SIGTAB = 256;    // double [2][SIG_RANKS_MAX]
+constexpr size_t MISC_SIGFLAG = 768;   // u64 [SIG_RANKS_MAX]
+constexpr size_t MISC_RTAB = 1024;     // double * [SIG_RANKS_MAX]
+constexpr size_t MISC_RFLAG = 1536;    // u64 * [SIG_RANKS_MAX]  // per block: flags [0, 512), counters [512, 1024)
 
 // Reduction of `count` steps of one block's norm partials into the history:
 // steps first .. first+count-1 (first < 0: the `count` steps before *step_ctr).

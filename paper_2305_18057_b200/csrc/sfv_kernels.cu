@@ -316,7 +316,24 @@ __global__ void __launch_bounds__(NT, SFV_MINB) stage_kernel(const __grid_consta
     auto read_step = [&]() {
         // the last CTA of the step's last launch advances the counter
         n = *a.step_ctr;
-        dt = P.dt_fixed > 0.0 ? P.dt_fixed : P.cfl / a.sig[n & 1];
+        double sg = 0.0;
+        bool tab = false;
+        if constexpr (PEER) tab = a.sig_ranks > 0;  // (peer variants only: keeps the default kernel's code as is)
+        if (tab) {
+            // device-side max over ranks: lane r waits for rank r's sigma of
+            // step n, then a warp max (warp-uniform call)
+            const int ln = threadIdx.x & 31;
+            double v = 0.0;
+            if (ln < a.sig_ranks) {
+                wait_flag(a.sig_flag + ln, (unsigned long long)n, a.halo_err);
+                v = *(volatile double *)(a.sig_tab + (n & 1) * SIG_RANKS_MAX + ln);
+            }
+            for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+            sg = v;
+        } else {
+            sg = a.sig[n & 1];
+        }
+        dt = P.dt_fixed > 0.0 ? P.dt_fixed : P.cfl / sg;
         coef = a.coef * dt;
     };
     const int PJ = a.PJ;
@@ -785,10 +802,18 @@ __global__ void __launch_bounds__(NT, SFV_MINB) stage_kernel(const __grid_consta
             __threadfence();
             if (atomicAdd(a.done, 1u) == gridDim.x - 1) {
                 __threadfence();
-                if (P.dt_fixed > 0.0) {
-                    a.dt_hist[n % a.cap] = P.dt_fixed;
-                } else {
-                    a.dt_hist[n % a.cap] = P.cfl / a.sig[n & 1];
+                a.dt_hist[n % a.cap] = dt;  // dt_n as every CTA of the step used it
+                if (!(P.dt_fixed > 0.0)) {
+                    if (PEER && a.sig_ranks > 0) {
+                        // publish this rank's sigma of U^{n+1} (complete: every CTA
+                        // of the launch has arrived) to every rank's table, then flag it
+                        const double mine = *(volatile double *)(a.sig + ((n + 1) & 1));
+                        for (int r = 0; r < a.sig_ranks; ++r)
+                            a.rtab[r][((n + 1) & 1) * SIG_RANKS_MAX + a.rank] = mine;
+                        __threadfence_system();
+                        for (int r = 0; r < a.sig_ranks; ++r)
+                            st_release_sys(a.rflag[r] + a.rank, (unsigned long long)(n + 1));
+                    }
                     a.sig[n & 1] = 0.0;
                 }
                 *a.done = 0u;
