@@ -370,6 +370,16 @@ def main():
         cpu = cpu_baseline_oracle()
 
     li = solver.launch_info()
+    halo_info = None
+    if px > 1:
+        # halo traffic per step of the busiest rank (2 edge rows x 4 components per
+        # connected cut, every stage) and the time it would take at NVLink 5's
+        # 900 GB/s per direction, as a fraction of the measured step: a bandwidth
+        # model (multi-GPU exchange is not timed separately on this pool)
+        cuts = 2 if px > 2 or world == 1 else 1
+        hb = cuts * 2 * 4 * 8 * nj * stages
+        halo_info = {"bytes_per_step_per_rank": hb, "nvlink_gbs": 900.0,
+                     "nvlink_time_fraction_model": hb / 900e9 / (ms_max * 1e-3 / args.steps)}
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": n_gpus, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
@@ -377,6 +387,7 @@ def main():
                 "config": {"workload": desc, "global_cells": cells_total, "cells_per_gpu": cells_rank,
                            "rk_stages": stages, "rk": args.rk, "parallelism": f"slab{px}x1",
                            "halo": halo_note if px > 1 else "none",
+                           **({"halo_traffic": halo_info} if halo_info else {}),
                            **({"simulated_ranks_on_one_gpu": True} if sim else {}),
                            "l2": f"no flush: working set {solver.ws.numel() / 1e6:.0f} MB per GPU vs 126 MB L2",
                            "launch": li,

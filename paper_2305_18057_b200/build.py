@@ -36,13 +36,13 @@ def up_to_date():
     return all(os.path.getmtime(d) <= t for d in DEPS)
 
 
-def build(force=False, verbose=False, out=None, defines=()):
+def build(force=False, verbose=False, out=None, defines=(), extra=()):
     if out is None and not force and up_to_date():
         return LIB
     target = out or LIB
     cmd = ["nvcc", *ARCH, *[f"-D{d}" for d in defines], "-O3", "-lineinfo", "-std=c++17", "-Xptxas", "-v",
            "-Xcompiler", "-fPIC", "-shared", "-I", os.path.join(ROOT, "include"),
-           "-I", CSRC, "-I", nccl_include(), *SOURCES, "-o", target + ".tmp", "-ldl"]
+           "-I", CSRC, "-I", nccl_include(), *extra, *SOURCES, "-o", target + ".tmp", "-ldl"]
     r = subprocess.run(cmd, capture_output=True, text=True)
     with open(os.path.join(HERE, "build.log" if out is None else os.path.basename(target) + ".log"), "w") as f:
         f.write(" ".join(cmd) + "\n" + r.stdout + r.stderr)
@@ -56,9 +56,11 @@ def build(force=False, verbose=False, out=None, defines=()):
 
 
 if __name__ == "__main__":
-    if "--variant" in sys.argv:  # A/B experiment builds: --variant NAME DEF=V ...
+    if "--variant" in sys.argv:  # A/B experiment builds: --variant NAME DEF=V ... [-- NVCC FLAGS]
         k = sys.argv.index("--variant")
-        name, defs = sys.argv[k + 1], sys.argv[k + 2:]
-        print(build(out=os.path.join(HERE, f"libsfv_{name}.so"), defines=defs))
+        rest = sys.argv[k + 2:]
+        extra = rest[rest.index("--") + 1:] if "--" in rest else []
+        defs = rest[:rest.index("--")] if "--" in rest else rest
+        print(build(out=os.path.join(HERE, f"libsfv_{sys.argv[k + 1]}.so"), defines=defs, extra=extra))
     else:
         build(force="--force" in sys.argv, verbose=True)
