@@ -268,14 +268,27 @@ __device__ __forceinline__ void store4(double *buf, int PJ, int i, int j, const 
 // and mbarriers.  j-face states / fluxes move between lanes by __shfl, so the
 // main loop has no CTA-wide barrier; warps drift independently.
 
+#ifndef SFV_DEEP_MASK
+// rings with 2 rows in flight instead of 1 (bit 0: stencil, 1: metrics, 2:
+// pointwise).  Measured on C2 / C3 (profiles/r1_ab_ring_depth.txt): pointwise
+// +0.3% / +1.3%, stencil -0.2% / +0.3%, all three -8% / -1%
+#define SFV_DEEP_MASK 4
+#endif
 template <int MODE>
 struct StageTraits {
     static constexpr int NPW = MODE == M_OWN ? 0 : (MODE == M_RK4F ? 3 : 1);
-    static constexpr int W_SLOT = 4 * WROW;           // stencil ring: 4 rows (v..v+2 + 1 in flight), 1152 B
-    static constexpr int M_SLOT = (NMET * WROW + 15) / 16 * 16;  // metrics ring: 2 rows (v + 1 in flight), 128 B aligned
-    static constexpr int P_SLOT = 4 * NPW * WROW;     // pointwise ring: 2 rows (v + 1 in flight)
+    // the RK4 final stage (3 pointwise inputs) keeps 1 row in flight per ring
+    // (12 CTAs/SM fit in 228 KB only so)
+    static constexpr bool DEEP = MODE != M_RK4F;
+    static constexpr int WS = DEEP && (SFV_DEEP_MASK & 1) ? 5 : 4;  // stencil ring: rows v..v+2 resident + (WS-3) in flight
+    static constexpr int MS = DEEP && (SFV_DEEP_MASK & 2) ? 3 : 2;  // metrics ring: row v + (MS-1) in flight
+    static constexpr int PS = DEEP && (SFV_DEEP_MASK & 4) ? 3 : 2;  // pointwise ring: row v + (PS-1) in flight
+    static constexpr int W_SLOT = 4 * WROW;           // 1152 B
+    static constexpr int M_SLOT = (NMET * WROW + 15) / 16 * 16;  // 128 B aligned
+    static constexpr int P_SLOT = 4 * NPW * WROW;
     static constexpr int X_SLOT = 8 * 32;             // lane exchange: north states [4][32], south fluxes [4][32]
-    static constexpr int WARP_DBL = 4 * W_SLOT + 2 * M_SLOT + 2 * P_SLOT + X_SLOT + 16;  // + 8 mbarriers, 128 B aligned
+    static constexpr int NBAR = WS + MS + PS;
+    static constexpr int WARP_DBL = WS * W_SLOT + MS * M_SLOT + PS * P_SLOT + X_SLOT + 16;  // + <= 16 mbarriers
 };
 
 template <int MODE>
@@ -299,13 +312,13 @@ __global__ void __launch_bounds__(NT, SFV_MINB) stage_kernel(const __grid_consta
     extern __shared__ __align__(128) double smem[];
     const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
     double *wbase = smem + warp * TR::WARP_DBL;
-    double *wring = wbase;                      // [4][4][WROW]
-    double *mring = wring + 4 * TR::W_SLOT;     // [2][7][WROW]
-    double *pring = mring + 2 * TR::M_SLOT;     // [2][4*NPW][WROW]
-    double *xch = pring + 2 * TR::P_SLOT;       // [8][32] lane exchange
-    uint64_t *wbar = reinterpret_cast<uint64_t *>(xch + TR::X_SLOT);   // [4]
-    uint64_t *mbar = wbar + 4;                                           // [2]
-    uint64_t *pbar = mbar + 2;                                           // [2]
+    double *wring = wbase;                      // [WS][4][WROW]
+    double *mring = wring + TR::WS * TR::W_SLOT;  // [MS][7][WROW]
+    double *pring = mring + TR::MS * TR::M_SLOT;  // [PS][4*NPW][WROW]
+    double *xch = pring + TR::PS * TR::P_SLOT;  // [8][32] lane exchange
+    uint64_t *wbar = reinterpret_cast<uint64_t *>(xch + TR::X_SLOT);   // [WS]
+    uint64_t *mbar = wbar + TR::WS;                                      // [MS]
+    uint64_t *pbar = mbar + TR::MS;                                      // [PS]
     double *red = smem + WPC * TR::WARP_DBL;    // [8][WPC]
 
     const Params &P = a.P;
@@ -389,8 +402,8 @@ __global__ void __launch_bounds__(NT, SFV_MINB) stage_kernel(const __grid_consta
         const int m0 = i_start - 1, m_last = i_end - 1;  // metric rows
         constexpr unsigned ROWB = WROW * 8u;
 
-        auto wslot = [&](int r) -> const double * { return wring + ((r - r0) & 3) * TR::W_SLOT; };
-        auto mslot = [&](int r) -> const double * { return mring + ((r - m0) & 1) * TR::M_SLOT; };
+        auto wslot = [&](int r) -> const double * { return wring + ((unsigned)(r - r0) % TR::WS) * TR::W_SLOT; };
+        auto mslot = [&](int r) -> const double * { return mring + ((unsigned)(r - m0) % TR::MS) * TR::M_SLOT; };
         // one 2D TMA box per ring row (36 columns x 4 / 7 rows), issued by the
         // whole warp through elect.sync (operands are warp-uniform: 1 warp/CTA);
         // shared-window addresses are computed once
@@ -398,17 +411,17 @@ __global__ void __launch_bounds__(NT, SFV_MINB) stage_kernel(const __grid_consta
         const unsigned wring_s = smem_u32(wring), mring_s = smem_u32(mring), pring_s = smem_u32(pring);
         const unsigned wbar_s = smem_u32(wbar), mbar_s = smem_u32(mbar), pbar_s = smem_u32(pbar);
         auto issue_w = [&](int r) {
-            const unsigned s = (unsigned)(r - r0) & 3u;
+            const unsigned s = (unsigned)(r - r0) % TR::WS;
             elect_issue_s(wring_s + s * (TR::W_SLOT * 8u), &a.tm_in, tx, (r + 2) * 4, wbar_s + 8u * s, 4u * ROWB);
         };
         auto issue_m = [&](int r) {
-            const unsigned s = (unsigned)(r - m0) & 1u;
+            const unsigned s = (unsigned)(r - m0) % TR::MS;
             elect_issue_s(mring_s + s * (TR::M_SLOT * 8u), &a.tm_met, tx, (r + 1) * NMET, mbar_s + 8u * s,
                           (unsigned)NMET * ROWB);
         };
-        auto issue_p = [&](int r) {  // pointwise rows: ring of 2, slot (r - i_start) & 1
+        auto issue_p = [&](int r) {  // pointwise rows: ring of PS, slot (r - i_start) % PS
             if constexpr (TR::NPW > 0) {
-                const unsigned s = (unsigned)(r - i_start) & 1u;
+                const unsigned s = (unsigned)(r - i_start) % TR::PS;
                 const unsigned dst = pring_s + s * (TR::P_SLOT * 8u), bar = pbar_s + 8u * s;
                 elect_issue_s(dst, &a.tm_pw[0], tx, (r + 2) * 4, bar, 4u * TR::NPW * ROWB);
 #pragma unroll
@@ -417,20 +430,20 @@ __global__ void __launch_bounds__(NT, SFV_MINB) stage_kernel(const __grid_consta
             }
         };
         auto wait_w = [&](int r) {
-            mbar_wait_s(wbar_s + 8u * ((unsigned)(r - r0) & 3u), (unsigned)(((r - r0) >> 2) & 1));
+            mbar_wait_s(wbar_s + 8u * ((unsigned)(r - r0) % TR::WS), ((unsigned)(r - r0) / TR::WS) & 1u);
         };
         auto wait_m = [&](int r) {
-            mbar_wait_s(mbar_s + 8u * ((unsigned)(r - m0) & 1u), (unsigned)(((r - m0) >> 1) & 1));
+            mbar_wait_s(mbar_s + 8u * ((unsigned)(r - m0) % TR::MS), ((unsigned)(r - m0) / TR::MS) & 1u);
         };
 
         if (lane == 0) {
-            for (int s = 0; s < 8; ++s) mbar_init(&wbar[s], 1);
+            for (int s = 0; s < TR::NBAR; ++s) mbar_init(&wbar[s], 1);
             asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         }
         __syncwarp();
         // metrics are read-only: prefetch them before waiting for the previous grid
-        for (int r = m0; r <= m0 + 1 && r <= m_last; ++r) issue_m(r);
+        for (int r = m0; r <= m0 + TR::MS - 1 && r <= m_last; ++r) issue_m(r);
         pdl_wait();
         // trigger only after the wait: at most one dependent grid is pending, so
         // its waiting CTAs cannot hold slots this grid still needs
@@ -444,8 +457,8 @@ __global__ void __launch_bounds__(NT, SFV_MINB) stage_kernel(const __grid_consta
             for (int e = 0; e < 4; ++e)
                 if (touch & (1u << e)) wait_flag(a.in_flag + e * FLAG_STRIDE, need, a.halo_err);
         }
-        for (int r = r0; r <= r0 + 3 && r <= r_last; ++r) issue_w(r);
-        issue_p(i_start);
+        for (int r = r0; r <= r0 + TR::WS - 1 && r <= r_last; ++r) issue_w(r);
+        for (int r = i_start; r <= i_start + TR::PS - 2 && r < i_end; ++r) issue_p(r);
 
         // ---- peeled prologue: rows i_start-2, i_start-1 (i direction only) ---
         double Wc[CPL][4], fp[CPL][4], QLp[CPL][4], GW[CPL][4];
@@ -470,7 +483,7 @@ __global__ void __launch_bounds__(NT, SFV_MINB) stage_kernel(const __grid_consta
                 }
         }
         __syncwarp();  // rows r0, r0+1 consumed
-        for (int r = r0 + 4; r <= r0 + 5 && r <= r_last; ++r) issue_w(r);
+        for (int r = r0 + TR::WS; r <= r0 + TR::WS + 1 && r <= r_last; ++r) issue_w(r);
         wait_w(r0 + 3);
         wait_m(m0);
         {
@@ -539,11 +552,10 @@ __global__ void __launch_bounds__(NT, SFV_MINB) stage_kernel(const __grid_consta
                 }
             }
             __syncwarp();  // stencil row v-1, metric row v-1, pointwise slot consumed
-            // steady state: exactly one row per ring (rows up to r0+5 / m0+1 were
-            // issued in the prologue)
-            if (v + 3 >= r0 + 6 && v + 3 <= r_last) issue_w(v + 3);
-            if (v + 1 <= m_last) issue_m(v + 1);
-            if (v + 1 < i_end) issue_p(v + 1);
+            // steady state: row v-1's slots are free -> rows v+WS-1, v+MS-1, v+PS-1
+            if (v + TR::WS - 1 >= r0 + TR::WS + 2 && v + TR::WS - 1 <= r_last) issue_w(v + TR::WS - 1);
+            if (v + TR::MS - 1 <= m_last && v + TR::MS - 1 >= m0 + TR::MS) issue_m(v + TR::MS - 1);
+            if (v + TR::PS - 1 < i_end) issue_p(v + TR::PS - 1);
             wait_m(v);
             const double *mv = mslot(v);
 #pragma unroll
@@ -569,9 +581,9 @@ __global__ void __launch_bounds__(NT, SFV_MINB) stage_kernel(const __grid_consta
             __syncwarp();
 #pragma unroll
             for (int c = 0; c < 4; ++c) GN[CPL - 1][c] = xch[(4 + c) * 32 + (lane < 31 ? lane + 1 : 31)];
-            const double *prow = pring + ((v - i_start) & 1) * TR::P_SLOT;
+            const double *prow = pring + ((unsigned)(v - i_start) % TR::PS) * TR::P_SLOT;
             if constexpr (TR::NPW > 0)
-                mbar_wait_s(pbar_s + 8u * ((unsigned)(v - i_start) & 1u), (unsigned)(((v - i_start) >> 1) & 1));
+                mbar_wait_s(pbar_s + 8u * ((unsigned)(v - i_start) % TR::PS), ((unsigned)(v - i_start) / TR::PS) & 1u);
             bool bad = false;
 #pragma unroll
             for (int k = 0; k < CPL; ++k) {
