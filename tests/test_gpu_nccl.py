@@ -32,7 +32,7 @@ def _free_port():
     return p
 
 
-def _worker(rank, world, port, px, py, ni, nj, steps, overlap, halo, out_q):
+def _worker(rank, world, port, px, py, ni, nj, steps, overlap, halo, rk, wx, out_q):
     os.environ.update({"MASTER_ADDR": "127.0.0.1", "MASTER_PORT": str(port),
                        "NCCL_HOSTID": f"sfv-sim-host-{rank}", "NCCL_SOCKET_IFNAME": "lo",
                        "NCCL_IB_DISABLE": "1", "NCCL_NVLS_ENABLE": "0", "SFV_OVERLAP": str(overlap)})
@@ -45,10 +45,10 @@ def _worker(rank, world, port, px, py, ni, nj, steps, overlap, halo, out_q):
         from paper_2305_18057_b200 import inputs as I
         from paper_2305_18057_b200 import sfv
         X, Y = I.ramp_nodes(ni, nj, 30.0)
-        cfg = I.default_config(ni, nj)
+        cfg = I.default_config(ni, nj, rk=rk)
         obj = [sfv.nccl_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(obj, src=0)
-        s = sfv.Solver(cfg, X, Y, px=px, py=py, rank=rank, nranks=world, nccl_id=obj[0], device=0)
+        s = sfv.Solver(cfg, X, Y, px=px, py=py, wx=wx, rank=rank, nranks=world, nccl_id=obj[0], device=0)
         if halo == "peer":
             s.enable_peer_halo()  # CUDA-IPC mapping of the neighbours' workspaces
         s.set_state(I.perturbed_state(ni, nj, 7))
@@ -65,12 +65,12 @@ def _worker(rank, world, port, px, py, ni, nj, steps, overlap, halo, out_q):
         dist.destroy_process_group()
 
 
-def _run(world, px, py, ni, nj, steps, overlap, halo="copy"):
+def _run(world, px, py, ni, nj, steps, overlap, halo="copy", rk=0, wx=None):
     import torch.multiprocessing as mp
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    ps = [ctx.Process(target=_worker, args=(r, world, port, px, py, ni, nj, steps, overlap, halo, q))
+    ps = [ctx.Process(target=_worker, args=(r, world, port, px, py, ni, nj, steps, overlap, halo, rk, wx, q))
           for r in range(world)]
     for p in ps:
         p.start()
@@ -86,23 +86,25 @@ def _run(world, px, py, ni, nj, steps, overlap, halo="copy"):
     return res
 
 
-@pytest.mark.parametrize("world,px,py,overlap,halo", [(2, 2, 1, 1, "copy"), (2, 2, 1, 0, "copy"), (2, 1, 2, 1, "copy"),
-                                                      (4, 2, 2, 1, "copy"), (2, 2, 1, 1, "peer"), (2, 1, 2, 1, "peer"),
-                                                      (4, 2, 2, 1, "peer")])
-def test_nccl_ranks_match_loopback_and_oracle(oracle_mod, world, px, py, overlap, halo):
-    """halo="peer": the stage kernels store the edge layers into the
-    neighbour rank's workspace through its CUDA-IPC mapping (DESIGN.md §5.2);
-    NCCL only for dt (per step), norms and get_state (per query)."""
+@pytest.mark.parametrize("world,px,py,overlap,halo,rk,wx", [
+    (2, 2, 1, 1, "copy", 0, None), (2, 2, 1, 0, "copy", 0, None), (2, 1, 2, 1, "copy", 0, None),
+    (4, 2, 2, 1, "copy", 0, None), (2, 2, 1, 1, "peer", 0, None), (2, 1, 2, 1, "peer", 0, None),
+    (4, 2, 2, 1, "peer", 0, None), (3, 3, 1, 1, "peer", 2, [1, 2, 3]), (2, 2, 1, 1, "peer", 1, None)])
+def test_nccl_ranks_match_loopback_and_oracle(oracle_mod, world, px, py, overlap, halo, rk, wx):
+    """halo="peer": the stage kernels store the edge layers into the neighbour
+    rank's workspace through its CUDA-IPC mapping and the CFL max travels
+    through every rank's sigma table; NCCL only for the
+    norms and state gathers.  rk: 0 RK4, 1 Heun, 2 Jameson; wx: slab weights."""
     from paper_2305_18057_b200 import inputs as I
     from paper_2305_18057_b200 import sfv
     from parity_util import dt_error, norm_error, state_error
     ni, nj, steps = 160, 64, 50
-    res = _run(world, px, py, ni, nj, steps, overlap, halo)
+    res = _run(world, px, py, ni, nj, steps, overlap, halo, rk, wx)
     U = res[0][2]
     X, Y = I.ramp_nodes(ni, nj, 30.0)
-    cfg = I.default_config(ni, nj)
+    cfg = I.default_config(ni, nj, rk=rk)
     U0 = I.perturbed_state(ni, nj, 7)
-    g = sfv.Solver(cfg, X, Y, px=px, py=py)
+    g = sfv.Solver(cfg, X, Y, px=px, py=py, wx=wx)
     g.set_state(U0); g.step(steps); g.sync()
     np.testing.assert_array_equal(U, g.get_state())
     for rank, _, _, nrm, dts in res:  # every rank holds the global histories
