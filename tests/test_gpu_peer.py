@@ -131,3 +131,18 @@ def test_peer_ghost_frames_are_neighbour_edges(sfv_mod, px, py, rk):
             mine, theirs = {0: (B[0:2, :, 2:-2], N[-4:-2, :, 2:-2]), 1: (B[-2:, :, 2:-2], N[2:4, :, 2:-2]),
                             2: (B[2:-2, :, 0:2], N[2:-2, :, -4:-2]), 3: (B[2:-2, :, -2:], N[2:-2, :, 2:4])}[e]
             np.testing.assert_array_equal(mine, theirs, err_msg=f"block {b} edge {'WESN'[e]}")
+
+
+@pytest.mark.parametrize("ni,nj,px,py", [(37, 29, 5, 3), (64, 62, 2, 2), (12, 40, 3, 1), (90, 31, 1, 1),
+                                         (48, 93, 2, 3)])
+def test_peer_small_and_ragged_blocks(sfv_mod, ni, nj, px, py):
+    """Blocks of a single segment (ni_b < 8), a last strip of one column
+    (nj_b = 31: two strips touch the N edge), 1-column-wide tail strips and
+    odd sizes: peer mode stays bitwise equal to the single block."""
+    X, Y = I.ramp_nodes(ni, nj, 30.0)
+    cfg = I.default_config(ni, nj)
+    U0 = I.perturbed_state(ni, nj, 13)
+    g1 = _run(sfv_mod, cfg, X, Y, U0, 25, False)
+    gp = _run(sfv_mod, cfg, X, Y, U0, 25, True, px=px, py=py)
+    np.testing.assert_array_equal(gp.get_state(), g1.get_state())
+    np.testing.assert_array_equal(gp.dt(), g1.dt())
