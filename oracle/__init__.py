@@ -49,7 +49,8 @@ class orc_config(C.Structure):
                 ("cfl", C.c_double), ("dt_fixed", C.c_double),
                 ("bc", C.c_int32 * 4), ("inflow_U", (C.c_double * 4) * 4),
                 ("max_history", C.c_int64), ("residual_kind", C.c_int32),
-                ("linear_rate", C.c_double)]
+                ("linear_rate", C.c_double), ("viscous", C.c_int32), ("mu", C.c_double),
+                ("prandtl", C.c_double), ("gas_R", C.c_double)]
 
 
 _lib = None
@@ -82,6 +83,10 @@ def lib():
         L.orc_get_dt.argtypes = [C.c_void_p, C.c_int64, C.c_int64, _D]
         L.orc_residual.argtypes = [C.c_void_p, _D, _D]
         L.orc_ghost_frame.argtypes = [C.c_void_p, _D, _D]
+        L.orc_gradients.argtypes = [C.c_void_p, _D, _D]
+        L.orc_viscous_flux.argtypes = [_D, C.c_double, C.c_double, C.c_double, C.c_double, C.c_double,
+                                       C.c_double, _D]
+        L.orc_viscous_flux.restype = None
         L.orc_steps_done.argtypes = [C.c_void_p]
         L.orc_steps_done.restype = C.c_int64
         L.orc_error_info.argtypes = [C.c_void_p, _I64]
@@ -143,6 +148,13 @@ def roe_flux(QL, QR, nx, ny, gamma=1.4, harten_eps=0.1):
     return F
 
 
+def viscous_flux(grad, u, v, nx, ny, mu, k):
+    """F_v . n (Eq. 2 viscous flux) from face gradients (u_x, u_y, v_x, v_y, T_x, T_y)."""
+    g = _f64(grad, (6,)); F = np.empty(4)
+    lib().orc_viscous_flux(_dp(g), u, v, nx, ny, mu, k, _dp(F))
+    return F
+
+
 def split(n, parts, weights=None):
     starts = np.zeros(parts + 1, dtype=np.int32)
     w = None if weights is None else np.ascontiguousarray(weights, dtype=np.int32)
@@ -177,6 +189,8 @@ def make_config(d, residual_kind=RES_EULER, linear_rate=0.0):
             c.inflow_U[e][k] = float(d["inflow_U"][e][k])
     c.max_history = d["max_history"]
     c.residual_kind = residual_kind; c.linear_rate = linear_rate
+    c.viscous = int(d.get("viscous", 0)); c.mu = float(d.get("mu", 0.0))
+    c.prandtl = float(d.get("prandtl", 0.72)); c.gas_R = float(d.get("gas_R", 287.0))
     return c
 
 
@@ -248,6 +262,12 @@ class Oracle:
         U = _f64(U, (self.nj, self.ni, 4)); R = np.empty_like(U)
         self._check(lib().orc_residual(self._h, _dp(U), _dp(R)))
         return R
+
+    def gradients(self, U):
+        """Green-Gauss cell gradients (u_x, u_y, v_x, v_y, T_x, T_y), [nj, ni, 6]."""
+        U = _f64(U, (self.nj, self.ni, 4)); G = np.empty((self.nj, self.ni, 6))
+        self._check(lib().orc_gradients(self._h, _dp(U), _dp(G)))
+        return G
 
     def ghost_frame(self, U):
         U = _f64(U, (self.nj, self.ni, 4))

@@ -10,7 +10,11 @@
  *   - Eq. 7: MUSCL extrapolation with limiters Psi;
  *   - PAPER.md:120, 138: ghost-cell boundary enforcement every RK substep,
  *     connected boundaries filled by exchange between partitions;
- *   - PAPER.md:174: 1D (and, for config C5, 2D) decomposition.
+ *   - PAPER.md:174: 1D (and, for config C5, 2D) decomposition;
+ *   - Navier-Stokes mode (cfg.viscous): the viscous flux of Eq. 2
+ *      with Stokes' hypothesis, R_h = sum (F - F_v) ds
+ *     (Eq. 5), Green-Gauss gradients and a no-slip adiabatic wall (SPEC.md:
+ *     201-227; readings N-R1..N-R5 in DESIGN.md).
  * Numerical choices the paper does not make come from SPEC.md: Roe flux with
  * Harten's entropy fix, van Albada limiter (SPEC.md:177,
  * :255), eps=1, kappa=-1, Heun RK2 / classical RK4
@@ -227,6 +231,7 @@ typedef struct {
     double *W;                /* stage input with a 2-cell ghost frame */
     double *R[4];             /* residual of each stage, interior */
     double *GI, *GJ;          /* face fluxes x area */
+    double *grad;             /* NS: interior cell gradients, (j*ni+i)*6 */
 } orc_block;
 
 struct orc_ctx {
@@ -288,7 +293,7 @@ static void free_blocks(orc_ctx *c)
         orc_block *bk = &c->b[n];
         free(bk->iface); free(bk->jface); free(bk->vol); free(bk->Un); free(bk->W);
         for (int s = 0; s < 4; ++s) free(bk->R[s]);
-        free(bk->GI); free(bk->GJ);
+        free(bk->GI); free(bk->GJ); free(bk->grad);
     }
     free(c->b); c->b = NULL;
     free(c->xs); free(c->ys); c->xs = c->ys = NULL;
@@ -303,7 +308,8 @@ int orc_create(const orc_config *cfg, const double *X, const double *Y, orc_ctx 
         || cfg->rk < 0 || cfg->rk > 2 || cfg->limiter < 0 || cfg->limiter > 2)
         return ORC_ERR_ARG;
     for (int e = 0; e < 4; ++e)
-        if (cfg->bc[e] < 0 || cfg->bc[e] > 2) return ORC_ERR_ARG;
+        if (cfg->bc[e] < 0 || cfg->bc[e] > 3 || (cfg->bc[e] == 3 && !cfg->viscous)) return ORC_ERR_ARG;
+    if (cfg->viscous && !(cfg->mu >= 0.0 && cfg->prandtl > 0.0 && cfg->gas_R > 0.0)) return ORC_ERR_ARG;
     orc_ctx *c = (orc_ctx *)calloc(1, sizeof(orc_ctx));
     c->cfg = *cfg;
     size_t nn = (size_t)(cfg->ni + 1) * (size_t)(cfg->nj + 1);
@@ -351,6 +357,7 @@ int orc_partition(orc_ctx *c, int32_t px, int32_t py, const int32_t *wx, const i
             for (int s = 0; s < 4; ++s) bk->R[s] = (double *)malloc(sizeof(double) * 4 * (size_t)ncell);
             bk->GI = (double *)malloc(sizeof(double) * 4 * (size_t)((bk->ni + 1) * (int64_t)bk->nj));
             bk->GJ = (double *)malloc(sizeof(double) * 4 * (size_t)(bk->ni * (int64_t)(bk->nj + 1)));
+            bk->grad = (double *)calloc(6 * (size_t)(bk->ni * (int64_t)bk->nj), sizeof(double));
             /* block-local nodes -> metrics; same arithmetic on the same values
              * as the single-block computation, hence bitwise equal */
             int64_t bw = bk->ni + 1, bh = bk->nj + 1;
@@ -394,6 +401,16 @@ static void mirror(const double *w, double nx, double ny, double *g)
     g[3] = w[3];
 }
 
+/* no-slip adiabatic wall (reading N-R4): ghost layer m = interior
+ * layer m with the velocity negated (rho, p and T copied) */
+static void noslip(const double *w, double *g)
+{
+    g[0] = w[0];
+    g[1] = -w[1];
+    g[2] = -w[2];
+    g[3] = w[3];
+}
+
 /* Ghost fill of the stage input W (reading A-R11):
  * physical edges by boundary condition, connected edges by bit-copies of the
  * neighbour's interior layers (step 10; "boundary data
@@ -415,6 +432,8 @@ static void fill_ghosts(orc_ctx *c)
                     memcpy(g, cf->inflow_U[0], 4 * sizeof(double));
                 } else if (cf->bc[0] == ORC_BC_OUTFLOW) {
                     memcpy(g, W + FR(bk, 0, j), 4 * sizeof(double));
+                } else if (cf->bc[0] == ORC_BC_NOSLIP_WALL) {
+                    noslip(W + FR(bk, m, j), g);
                 } else {
                     const double *f = bk->iface + ((int64_t)j * (bk->ni + 1) + 0) * 3;
                     mirror(W + FR(bk, m, j), f[0], f[1], g);
@@ -430,6 +449,8 @@ static void fill_ghosts(orc_ctx *c)
                     memcpy(g, cf->inflow_U[1], 4 * sizeof(double));
                 } else if (cf->bc[1] == ORC_BC_OUTFLOW) {
                     memcpy(g, W + FR(bk, bk->ni - 1, j), 4 * sizeof(double));
+                } else if (cf->bc[1] == ORC_BC_NOSLIP_WALL) {
+                    noslip(W + FR(bk, bk->ni - 1 - m, j), g);
                 } else {
                     const double *f = bk->iface + ((int64_t)j * (bk->ni + 1) + bk->ni) * 3;
                     mirror(W + FR(bk, bk->ni - 1 - m, j), f[0], f[1], g);
@@ -445,6 +466,8 @@ static void fill_ghosts(orc_ctx *c)
                     memcpy(g, cf->inflow_U[2], 4 * sizeof(double));
                 } else if (cf->bc[2] == ORC_BC_OUTFLOW) {
                     memcpy(g, W + FR(bk, i, 0), 4 * sizeof(double));
+                } else if (cf->bc[2] == ORC_BC_NOSLIP_WALL) {
+                    noslip(W + FR(bk, i, m), g);
                 } else {
                     const double *f = bk->jface + ((int64_t)0 * bk->ni + i) * 3;
                     mirror(W + FR(bk, i, m), f[0], f[1], g);
@@ -460,6 +483,8 @@ static void fill_ghosts(orc_ctx *c)
                     memcpy(g, cf->inflow_U[3], 4 * sizeof(double));
                 } else if (cf->bc[3] == ORC_BC_OUTFLOW) {
                     memcpy(g, W + FR(bk, i, bk->nj - 1), 4 * sizeof(double));
+                } else if (cf->bc[3] == ORC_BC_NOSLIP_WALL) {
+                    noslip(W + FR(bk, i, bk->nj - 1 - m), g);
                 } else {
                     const double *f = bk->jface + ((int64_t)bk->nj * bk->ni + i) * 3;
                     mirror(W + FR(bk, i, bk->nj - 1 - m), f[0], f[1], g);
@@ -467,6 +492,110 @@ static void fill_ghosts(orc_ctx *c)
             }
         }
     }
+}
+
+/* ------------------------------------------------------------------------
+ * Navier-Stokes pieces (Eq. 2).
+ * ---------------------------------------------------------------------- */
+/* viscous normal flux: Stokes' hypothesis lambda = -2 mu / 3,
+ * tau_xx = 2 mu u_x + lambda (u_x + v_y), tau_yy = 2 mu v_y + lambda (u_x + v_y),
+ * tau_xy = mu (u_y + v_x), Theta_i = u tau_xi + v tau_yi + k T_i;
+ * F_v . n = (0, tau_xx nx + tau_xy ny, tau_xy nx + tau_yy ny, Theta_x nx + Theta_y ny) */
+void orc_viscous_flux(const double g[6], double u, double v, double nx, double ny, double mu, double k,
+                      double Fv[4])
+{
+    double lambda = -2.0 * mu / 3.0;
+    double div = g[0] + g[3];
+    double txx = 2.0 * mu * g[0] + lambda * div;
+    double tyy = 2.0 * mu * g[3] + lambda * div;
+    double txy = mu * (g[1] + g[2]);
+    double thx = u * txx + v * txy + k * g[4];
+    double thy = u * txy + v * tyy + k * g[5];
+    Fv[0] = 0.0;
+    Fv[1] = txx * nx + txy * ny;
+    Fv[2] = txy * nx + tyy * ny;
+    Fv[3] = thx * nx + thy * ny;
+}
+
+/* (u, v, T) of a conserved state, T = p / (rho R) */
+static void uvT(const double *w, double gamma, double R, double out[3])
+{
+    double prim[4];
+    orc_primitive(w, gamma, prim);
+    out[0] = prim[1];
+    out[1] = prim[2];
+    out[2] = prim[3] / (prim[0] * R);
+}
+
+/* Green-Gauss gradient of (u, v, T) in every interior cell of a block from
+ * the ghost-filled W (reading N-R2): grad phi = (1/V) sum_f phi_f n_f A_f
+ * over the 4 faces with outward normals, phi_f the arithmetic mean of the
+ * two cells sharing the face.  Needs only face-neighbour ghosts. */
+static void gradients_block(orc_ctx *c, orc_block *bk)
+{
+    const orc_config *cf = &c->cfg;
+    for (int32_t j = 0; j < bk->nj; ++j)
+        for (int32_t i = 0; i < bk->ni; ++i) {
+            double pc[3], pw[3], pe[3], ps[3], pn[3];
+            uvT(bk->W + FR(bk, i, j), cf->gamma, cf->gas_R, pc);
+            uvT(bk->W + FR(bk, i - 1, j), cf->gamma, cf->gas_R, pw);
+            uvT(bk->W + FR(bk, i + 1, j), cf->gamma, cf->gas_R, pe);
+            uvT(bk->W + FR(bk, i, j - 1), cf->gamma, cf->gas_R, ps);
+            uvT(bk->W + FR(bk, i, j + 1), cf->gamma, cf->gas_R, pn);
+            const double *fW = bk->iface + ((int64_t)j * (bk->ni + 1) + i) * 3;
+            const double *fE = bk->iface + ((int64_t)j * (bk->ni + 1) + i + 1) * 3;
+            const double *fS = bk->jface + ((int64_t)j * bk->ni + i) * 3;
+            const double *fN = bk->jface + ((int64_t)(j + 1) * bk->ni + i) * 3;
+            double V = bk->vol[(int64_t)j * bk->ni + i];
+            for (int q = 0; q < 3; ++q) {
+                double phE = 0.5 * (pc[q] + pe[q]), phW = 0.5 * (pw[q] + pc[q]);
+                double phN = 0.5 * (pc[q] + pn[q]), phS = 0.5 * (ps[q] + pc[q]);
+                double gx = phE * fE[0] * fE[2] - phW * fW[0] * fW[2] + phN * fN[0] * fN[2] - phS * fS[0] * fS[2];
+                double gy = phE * fE[1] * fE[2] - phW * fW[1] * fW[2] + phN * fN[1] * fN[2] - phS * fS[1] * fS[2];
+                bk->grad[IN(bk, i, j) / 4 * 6 + 2 * q] = gx / V;
+                bk->grad[IN(bk, i, j) / 4 * 6 + 2 * q + 1] = gy / V;
+            }
+        }
+}
+
+/* gradient of cell (i, j) of a block, i in [-1, ni], j in [-1, nj] (not a
+ * corner): interior cells their own; a connected edge's ghost the
+ * neighbour's cell; a physical edge's ghost the adjacent interior cell's
+ * (reading N-R1) */
+static const double *cell_grad(orc_ctx *c, orc_block *bk, int32_t i, int32_t j)
+{
+    if (i < 0 || i >= bk->ni) {
+        int e = i < 0 ? 0 : 1;
+        if (bk->nbr[e] >= 0) {
+            orc_block *nb = &c->b[bk->nbr[e]];
+            return nb->grad + IN(nb, i < 0 ? nb->ni - 1 : 0, j) / 4 * 6;
+        }
+        return bk->grad + IN(bk, i < 0 ? 0 : bk->ni - 1, j) / 4 * 6;
+    }
+    if (j < 0 || j >= bk->nj) {
+        int e = j < 0 ? 2 : 3;
+        if (bk->nbr[e] >= 0) {
+            orc_block *nb = &c->b[bk->nbr[e]];
+            return nb->grad + IN(nb, i, j < 0 ? nb->nj - 1 : 0) / 4 * 6;
+        }
+        return bk->grad + IN(bk, i, j < 0 ? 0 : bk->nj - 1) / 4 * 6;
+    }
+    return bk->grad + IN(bk, i, j) / 4 * 6;
+}
+
+/* F_v . n of the face between cells L and R (reading N-R3): gradients and
+ * (u, v) are arithmetic means of the two cells */
+static void face_viscous(orc_ctx *c, orc_block *bk, int32_t iL, int32_t jL, int32_t iR, int32_t jR,
+                         double nx, double ny, double Fv[4])
+{
+    const orc_config *cf = &c->cfg;
+    const double *gL = cell_grad(c, bk, iL, jL), *gR = cell_grad(c, bk, iR, jR);
+    double g[6], pL[3], pR[3];
+    for (int q = 0; q < 6; ++q) g[q] = 0.5 * (gL[q] + gR[q]);
+    uvT(bk->W + FR(bk, iL, jL), cf->gamma, cf->gas_R, pL);
+    uvT(bk->W + FR(bk, iR, jR), cf->gamma, cf->gas_R, pR);
+    double k = cf->mu * (cf->gamma * cf->gas_R / (cf->gamma - 1.0)) / cf->prandtl;
+    orc_viscous_flux(g, 0.5 * (pL[0] + pR[0]), 0.5 * (pL[1] + pR[1]), nx, ny, cf->mu, k, Fv);
 }
 
 /* Residual R = sum_f G_f (Eq. 5 with S = 0):
@@ -503,6 +632,11 @@ static int residual_block(orc_ctx *c, orc_block *bk, double *R, int64_t *bad)
                 status = ORC_ERR_STATE;
                 for (int k = 0; k < 4; ++k) F[k] = NAN;
             }
+            if (cf->viscous) {
+                double Fv[4];
+                face_viscous(c, bk, i - 1, j, i, j, f[0], f[1], Fv);
+                for (int k = 0; k < 4; ++k) F[k] = F[k] - Fv[k];
+            }
             for (int k = 0; k < 4; ++k) bk->GI[((int64_t)j * (bk->ni + 1) + i) * 4 + k] = F[k] * f[2];
         }
     for (int32_t j = 0; j <= bk->nj; ++j)
@@ -520,6 +654,11 @@ static int residual_block(orc_ctx *c, orc_block *bk, double *R, int64_t *bad)
                 if (*bad < 0 || key < *bad) *bad = key;
                 status = ORC_ERR_STATE;
                 for (int k = 0; k < 4; ++k) F[k] = NAN;
+            }
+            if (cf->viscous) {
+                double Fv[4];
+                face_viscous(c, bk, i, j - 1, i, j, f[0], f[1], Fv);
+                for (int k = 0; k < 4; ++k) F[k] = F[k] - Fv[k];
             }
             for (int k = 0; k < 4; ++k) bk->GJ[((int64_t)j * bk->ni + i) * 4 + k] = F[k] * f[2];
         }
@@ -674,6 +813,8 @@ int orc_step(orc_ctx *c, int32_t nsteps)
             fill_ghosts(c);
             int64_t bad = -1;
             int st = ORC_OK;
+            if (cf->viscous)  /* every block's gradients first: ghost gradients are the neighbours' */
+                for (int32_t n = 0; n < c->nblocks; ++n) gradients_block(c, &c->b[n]);
             for (int32_t n = 0; n < c->nblocks; ++n)
                 if (residual_block(c, &c->b[n], c->b[n].R[k - 1], &bad) != ORC_OK) st = ORC_ERR_STATE;
             if (st != ORC_OK) {
@@ -782,6 +923,8 @@ int orc_residual(orc_ctx *c, const double *U, double *R)
     fill_ghosts(c);
     int64_t bad = -1;
     int st = ORC_OK;
+    if (c->cfg.viscous)
+        for (int32_t n = 0; n < c->nblocks; ++n) gradients_block(c, &c->b[n]);
     for (int32_t n = 0; n < c->nblocks; ++n) {
         orc_block *bk = &c->b[n];
         if (residual_block(c, bk, bk->R[0], &bad) != ORC_OK) st = ORC_ERR_STATE;
@@ -805,6 +948,27 @@ int orc_ghost_frame(orc_ctx *c, const double *U, double *frame)
             memcpy(bk->W + FR(bk, i, j), U + ((int64_t)j * c->cfg.ni + i) * 4, 4 * sizeof(double));
     fill_ghosts(c);
     memcpy(frame, bk->W, sizeof(double) * 4 * (size_t)((bk->ni + 4) * (int64_t)(bk->nj + 4)));
+    return ORC_OK;
+}
+
+int orc_gradients(orc_ctx *c, const double *U, double *grad)
+{
+    for (int32_t n = 0; n < c->nblocks; ++n) {
+        orc_block *bk = &c->b[n];
+        for (int32_t j = 0; j < bk->nj; ++j)
+            for (int32_t i = 0; i < bk->ni; ++i)
+                memcpy(bk->W + FR(bk, i, j), U + ((int64_t)(bk->j0 + j) * c->cfg.ni + (bk->i0 + i)) * 4,
+                       4 * sizeof(double));
+    }
+    fill_ghosts(c);
+    for (int32_t n = 0; n < c->nblocks; ++n) {
+        orc_block *bk = &c->b[n];
+        gradients_block(c, bk);
+        for (int32_t j = 0; j < bk->nj; ++j)
+            for (int32_t i = 0; i < bk->ni; ++i)
+                memcpy(grad + ((int64_t)(bk->j0 + j) * c->cfg.ni + (bk->i0 + i)) * 6, bk->grad + IN(bk, i, j) / 4 * 6,
+                       6 * sizeof(double));
+    }
     return ORC_OK;
 }
 

@@ -29,7 +29,7 @@ extern "C" {
 
 enum { ORC_OK = 0, ORC_ERR_ARG = 1, ORC_ERR_GEOMETRY = 2, ORC_ERR_STATE = 3,
        ORC_ERR_SEQUENCE = 4 };
-enum { ORC_BC_INFLOW = 0, ORC_BC_OUTFLOW = 1, ORC_BC_SLIP_WALL = 2 };
+enum { ORC_BC_INFLOW = 0, ORC_BC_OUTFLOW = 1, ORC_BC_SLIP_WALL = 2, ORC_BC_NOSLIP_WALL = 3 };
 enum { ORC_LIM_VAN_ALBADA = 0, ORC_LIM_VAN_ALBADA2 = 1, ORC_LIM_NONE = 2 };
 enum { ORC_RK4_CLASSIC = 0, ORC_RK2_HEUN = 1, ORC_RK4_JAMESON = 2 };
 enum { ORC_RES_EULER = 0, ORC_RES_LINEAR = 1 };
@@ -48,6 +48,9 @@ typedef struct {
     int64_t max_history;
     int32_t residual_kind;      /* test hook: ORC_RES_LINEAR => R = rate*V*U */
     double linear_rate;
+    /* Navier-Stokes (Eq. 2 viscous flux; readings N-R*): */
+    int32_t viscous;            /* 0 = Euler, 1 = Navier-Stokes */
+    double mu, prandtl, gas_R;  /* constant viscosity, Prandtl number, gas constant */
 } orc_config;
 
 typedef struct orc_ctx orc_ctx;
@@ -62,6 +65,10 @@ void orc_muscl(const double w[4], double eps, double kappa, int32_t kind,
 int orc_roe_flux(const double QL[4], const double QR[4], double nx, double ny,
                  double gamma, double harten_eps, double F[4]);
 int orc_split(int32_t n, int32_t parts, const int32_t *weights, int32_t *starts);
+/* viscous normal flux F_v . n (Eq. 2) from the face gradients
+ * g = (u_x, u_y, v_x, v_y, T_x, T_y) and face values u, v (reading N-R3) */
+void orc_viscous_flux(const double g[6], double u, double v, double nx, double ny, double mu, double k,
+                      double Fv[4]);
 int orc_stable_dt(int32_t ni, int32_t nj, const double *X, const double *Y, const double *U, double gamma,
                   double cfl, double *dt);
 
@@ -76,6 +83,9 @@ int orc_get_residual_norms(const orc_ctx *c, int64_t first, int64_t count, doubl
 int orc_get_dt(const orc_ctx *c, int64_t first, int64_t count, double *out);
 int orc_residual(orc_ctx *c, const double *U, double *R);
 int orc_ghost_frame(orc_ctx *c, const double *U, double *frame);
+/* Green-Gauss cell gradients (u_x, u_y, v_x, v_y, T_x, T_y) of U after the
+ * ghost fill, ni*nj*6 doubles, index (j*ni+i)*6+q (reading N-R2) */
+int orc_gradients(orc_ctx *c, const double *U, double *grad);
 int64_t orc_steps_done(const orc_ctx *c);
 void orc_error_info(const orc_ctx *c, int64_t out4[4]);
 const char *orc_last_error(const orc_ctx *c);

@@ -36,7 +36,7 @@ TABLE1_T = 217.0
 # Boundary kinds, limiter kinds and RK tableaus (numeric codes shared by the
 # two independent C headers include/sfv.h and oracle/oracle.h by convention;
 # each header defines its own constants).
-BC_INFLOW, BC_OUTFLOW, BC_SLIP_WALL = 0, 1, 2
+BC_INFLOW, BC_OUTFLOW, BC_SLIP_WALL, BC_NOSLIP_WALL = 0, 1, 2, 3
 LIM_VAN_ALBADA, LIM_VAN_ALBADA2, LIM_NONE = 0, 1, 2
 RK4_CLASSIC, RK2_HEUN, RK4_JAMESON = 0, 1, 2
 RK_STAGES = {RK4_CLASSIC: 4, RK2_HEUN: 2, RK4_JAMESON: 4}
@@ -178,7 +178,8 @@ def uniform_state(ni, nj, U0=None):
 def default_config(ni, nj, rk=RK4_CLASSIC, cfl=None, bc=None,
                    inflow=None, dt_fixed=0.0, harten_eps=0.1,
                    limiter=LIM_VAN_ALBADA2, lim_delta=1e-12, eps=1.0,
-                   kappa=-1.0, gamma=GAMMA, max_history=4096):
+                   kappa=-1.0, gamma=GAMMA, max_history=4096, viscous=0, mu=0.0, prandtl=0.72,
+                   gas_R=None):
     """The scheme settings of SURVEY.md §8(d) "common settings", except the
     limiter: van Albada in its bounded form psi = max(0, (2ab+d)/(a^2+b^2+d))
     (reading A-R3, revised).  It satisfies SPEC.md:166 (0 <= Psi
@@ -204,4 +205,6 @@ def default_config(ni, nj, rk=RK4_CLASSIC, cfl=None, bc=None,
                 limiter=int(limiter), lim_delta=float(lim_delta),
                 harten_eps=float(harten_eps), rk=int(rk), cfl=float(cfl),
                 dt_fixed=float(dt_fixed), bc=tuple(int(b) for b in bc),
-                inflow_U=inflow, max_history=int(max_history))
+                inflow_U=inflow, max_history=int(max_history),
+                viscous=int(viscous), mu=float(mu), prandtl=float(prandtl),
+                gas_R=float(R_GAS if gas_R is None else gas_R))
