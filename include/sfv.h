@@ -62,7 +62,8 @@ typedef enum {
     SFV_ERR_HALO = 9         /* device-initiated halo exchange: a neighbour never signalled */
 } sfv_status;
 
-typedef enum { SFV_BC_INFLOW = 0, SFV_BC_OUTFLOW = 1, SFV_BC_SLIP_WALL = 2 } sfv_bc;
+typedef enum { SFV_BC_INFLOW = 0, SFV_BC_OUTFLOW = 1, SFV_BC_SLIP_WALL = 2,
+               SFV_BC_NOSLIP_WALL = 3 /* adiabatic; viscous only (reading N-R4) */ } sfv_bc;
 typedef enum { SFV_LIM_VAN_ALBADA = 0, SFV_LIM_VAN_ALBADA2 = 1, SFV_LIM_NONE = 2 } sfv_limiter;
 typedef enum { SFV_RK4_CLASSIC = 0, SFV_RK2_HEUN = 1, SFV_RK4_JAMESON = 2 } sfv_rk;
 /* How the ghost layers of connected edges are refreshed after each stage
@@ -92,11 +93,19 @@ typedef struct {
     int32_t bc[4];               /* physical boundary per edge W, E, S, N (sfv_bc)      reading A-R11/12 */
     double inflow_U[4][4];       /* conserved inflow state per edge, used if INFLOW      reading A-R27 */
     int64_t max_history;         /* capacity (steps) of the dt / norm history, >= 1 */
+    /* Navier-Stokes (Eq. 2 viscous flux; readings N-R1..N-R6):
+     * R_h = sum_f (F - F_v) ds with Green-Gauss gradients of (u, v, T).
+     * Single-rank only (any px x py loopback blocks, SFV_HALO_COPY). */
+    int32_t viscous;             /* 0 = Euler, 1 = Navier-Stokes */
+    double mu;                   /* constant dynamic viscosity, >= 0            reading N-R5 */
+    double prandtl;              /* Prandtl number, > 0 (0.72)                   reading N-R5 */
+    double gas_R;                /* gas constant, > 0 (287): T = p / (rho R)     reading N-R5 */
 } sfv_config;
 
 /* Validate cfg and copy the node arrays.  Host only (no device work).
  * ARG: ni<2 || nj<2, gamma<=1, |kappa|>1, eps not in {0,1}, cfl<=0 without
- *      dt_fixed, unknown enum, max_history<1.
+ *      dt_fixed, unknown enum, max_history<1, a no-slip wall without viscous,
+ *      viscous with mu<0, prandtl<=0 or gas_R<=0.
  * GEOMETRY: some cell volume <= 0 (sfv_error_info gives its i, j). */
 sfv_status sfv_create(const sfv_config *cfg, const double *x_nodes, const double *y_nodes,
                       sfv_ctx **out);
@@ -218,6 +227,10 @@ sfv_status sfv_peer_connect(sfv_ctx *ctx, const void *handles);
  * tableau) of local block `block`, ghost frame included, to the host:
  * out[((i+2)*4 + c)*(nj_b+4) + (j+2)] for i in [-2, ni_b+2), c in 0..3,
  * j in [-2, nj_b+2) (block-local indices; corner ghosts are NaN).
+ * Navier-Stokes mode also: k = -1 the last stage's viscous residual
+ * sum_f F_v . n A (same layout, interior meaningful), k = -2 the gradient
+ * frame (u_x, u_y, v_x, v_y, T_x, T_y): out[((i+1)*6 + q)*(nj_b+2) + j+1],
+ * i in [-1, ni_b], j in [-1, nj_b].
  * Synchronising.  ARG: block not local or k out of range. */
 sfv_status sfv_debug_block_buffer(sfv_ctx *ctx, int32_t block, int32_t k, double *out);
 

@@ -99,6 +99,8 @@ struct Block {
     unsigned long long *flags = nullptr;  // inbound halo flags [4 * FLAG_STRIDE] (peer mode)
     unsigned *ecnt = nullptr;             // writer arrival counters [4 * CNT_STRIDE]
     PeerView pv[4];                       // neighbour per edge (peer mode)
+    double *grad = nullptr, *rv = nullptr;  // Navier-Stokes: gradients (1-layer ghost frame), viscous residual
+    int PG = 0;
     CUtensorMap tm_buf[4], tm_met;  // 2D TMA descriptors (made at sfv_bind)
     size_t buf_elems() const { return (size_t)(ni + 4) * 4 * PJ + PADD; }
     size_t met_elems() const { return (size_t)(ni + 1) * NMET * PJ + PADD; }
@@ -254,6 +256,9 @@ void build_params(sfv_ctx *c) {
     P.cfl = f.cfl;
     P.dt_fixed = f.dt_fixed;
     P.limiter = f.limiter;
+    P.mu = f.viscous ? f.mu : 0.0;
+    P.rgas = f.gas_R > 0.0 ? f.gas_R : 287.0;
+    P.kcond = f.viscous ? f.mu * (f.gamma * P.rgas / (f.gamma - 1.0)) / f.prandtl : 0.0;
 }
 
 // Launch geometry: strips of <= NT-4 columns (even starts), segments along i
@@ -293,7 +298,7 @@ void plan_launches(sfv_ctx *c, Block &b) {
     const bool overlap = !(ov && ov[0] == '0');
     // peer mode: one launch per stage; the edge tasks store into the
     // neighbours' ghost frames themselves
-    b.split = overlap && (cw || ce) && b.ni >= 8 && c->halo != SFV_HALO_PEER;
+    b.split = overlap && (cw || ce) && b.ni >= 8 && c->halo != SFV_HALO_PEER && !c->cfg.viscous;
     int n = 0;
     int lo = 0, hi = b.ni;
     if (b.split) {
@@ -387,6 +392,9 @@ size_t layout(sfv_ctx *c, bool assign) {
         const int max_cta = (((b.nj + WOUT - 1) / WOUT) * (NSEG_MAX + 2) + WPC - 1) / WPC + 2;
         size_t op = take(sizeof(double) * 8 * (size_t)max_cta * c->pring);
         size_t of = take(PEER_SYNC_BYTES);
+        const int PG = b.nj + 2;
+        size_t og = take(c->cfg.viscous ? sizeof(double) * (size_t)(b.ni + 2) * 6 * PG : 0);
+        size_t orv = take(c->cfg.viscous ? sizeof(double) * b.buf_elems() : 0);
         size_t ox[4];
         for (int k = 0; k < 4; ++k) ox[k] = take(c->nranks > 1 ? sizeof(double) * 8 * (size_t)b.ni : 0);
         if (assign) {
@@ -401,6 +409,9 @@ size_t layout(sfv_ctx *c, bool assign) {
             b.xr[1] = reinterpret_cast<double *>(c->ws + ox[3]);
             b.flags = reinterpret_cast<unsigned long long *>(c->ws + of);
             b.ecnt = reinterpret_cast<unsigned *>(c->ws + of + PEER_SYNC_BYTES / 2);
+            b.PG = PG;
+            b.grad = c->cfg.viscous ? reinterpret_cast<double *>(c->ws + og) : nullptr;
+            b.rv = c->cfg.viscous ? reinterpret_cast<double *>(c->ws + orv) : nullptr;
         }
     }
     return off;
@@ -579,7 +590,52 @@ StageArgs make_args(sfv_ctx *c, Block &b, int k) {
             a.rflag = c->rflag;
         }
     }
+    a.rv = c->cfg.viscous ? b.rv : nullptr;
     return a;
+}
+
+// Navier-Stokes: gradients of every block's stage input, physical-edge ghost
+// gradients, loopback exchange of the connected ones (1 layer: rows for
+// i-cuts, columns for j-cuts), then every block's viscous residual
+// (readings N-R1..N-R3)
+sfv_status enqueue_viscous(sfv_ctx *c, int in, cudaStream_t st) {
+    auto args = [&](Block &b) {
+        ViscArgs v{};
+        v.in = b.buf[in];
+        v.met = b.met;
+        v.grad = b.grad;
+        v.rv = b.rv;
+        v.ni = b.ni;
+        v.nj = b.nj;
+        v.PJ = b.PJ;
+        v.PG = b.PG;
+        for (int e = 0; e < 4; ++e) v.bc[e] = b.edge[e];
+        v.P = c->P;
+        return v;
+    };
+    for (Block &b : c->blocks) {
+        const ViscArgs v = args(b);
+        CK(launch_grad(v, st));
+        CK(launch_grad_ghosts(v, st));
+    }
+    for (Block &b : c->blocks) {
+        const size_t rowd = (size_t)6 * b.PG;  // one i-row of the gradient frame
+        if (b.nbr[1] >= 0) {  // E neighbour e: b row ni-1 -> e row -1; e row 0 -> b row ni
+            Block &e = *local_block(c, b.nbr[1]);
+            CK(cudaMemcpyAsync(e.grad, b.grad + (size_t)b.ni * rowd, rowd * 8, cudaMemcpyDeviceToDevice, st));
+            CK(cudaMemcpyAsync(b.grad + (size_t)(b.ni + 1) * rowd, e.grad + rowd, rowd * 8, cudaMemcpyDeviceToDevice,
+                               st));
+        }
+        if (b.nbr[3] >= 0) {  // N neighbour n: b column nj-1 -> n column -1; n column 0 -> b column nj
+            Block &n = *local_block(c, b.nbr[3]);
+            CK(cudaMemcpy2DAsync(n.grad + (size_t)6 * n.PG + 0, (size_t)n.PG * 8, b.grad + (size_t)6 * b.PG + b.nj,
+                                 (size_t)b.PG * 8, 8, (size_t)b.ni * 6, cudaMemcpyDeviceToDevice, st));
+            CK(cudaMemcpy2DAsync(b.grad + (size_t)6 * b.PG + b.nj + 1, (size_t)b.PG * 8, n.grad + (size_t)6 * n.PG + 1,
+                                 (size_t)n.PG * 8, 8, (size_t)n.ni * 6, cudaMemcpyDeviceToDevice, st));
+        }
+    }
+    for (Block &b : c->blocks) CK(launch_visc(args(b), st));
+    return SFV_OK;
 }
 
 // Tasks of a launch (nseg segments over all rows) that touch edge e: the same
@@ -622,6 +678,10 @@ sfv_status enqueue_step(sfv_ctx *c, cudaStream_t st, bool norms_batch) {
     for (Block &b : c->blocks) any_split |= b.split;
     for (int k = 1; k <= s; ++k) {
         const StageSpec sp = stage_spec(c->cfg.rk, k);
+        if (c->cfg.viscous) {
+            sfv_status r = enqueue_viscous(c, sp.in, st);
+            if (r != SFV_OK) return r;
+        }
         auto launch_part = [&](Block &b, int q) -> sfv_status {
             StageArgs a = make_args(c, b, k);
             // the step's last launch in stream order advances the step counter
@@ -631,7 +691,7 @@ sfv_status enqueue_step(sfv_ctx *c, cudaStream_t st, bool norms_batch) {
             a.nseg = b.lseg[q];
             a.part_base = b.lbase[q];
             for (int e = 0; e < 4; ++e) a.edge_writers[e] = a.peer_out[e] ? edge_writers(b, a.nseg, e) : 0;
-            CK(launch_stage(a, sp.mode, k == 1, k == s && cflmode, c->halo == SFV_HALO_PEER, st));
+            CK(launch_stage(a, sp.mode, k == 1, k == s && cflmode, c->halo == SFV_HALO_PEER, c->cfg.viscous != 0, st));
             return SFV_OK;
         };
         if (any_split) {
@@ -719,7 +779,9 @@ sfv_status sfv_create(const sfv_config *cfg, const double *x, const double *y, s
         !(f.harten_eps >= 0.0))
         return SFV_ERR_ARG;
     for (int e = 0; e < 4; ++e)
-        if (f.bc[e] < 0 || f.bc[e] > 2) return SFV_ERR_ARG;
+        if (f.bc[e] < 0 || f.bc[e] > 3 || (f.bc[e] == SFV_BC_NOSLIP_WALL && !f.viscous)) return SFV_ERR_ARG;
+    if (f.viscous != 0 && f.viscous != 1) return SFV_ERR_ARG;
+    if (f.viscous && !(f.mu >= 0.0 && f.prandtl > 0.0 && f.gas_R > 0.0)) return SFV_ERR_ARG;
     if ((long long)f.ni * f.nj >= (1ll << 31)) return SFV_ERR_UNSUPPORTED;
     sfv_ctx *c = new sfv_ctx();
     c->cfg = f;
@@ -768,6 +830,8 @@ sfv_status sfv_partition(sfv_ctx *c, int32_t px, int32_t py, const int32_t *wx, 
     if (px < 1 || py < 1 || nranks < 1 || rank < 0 || rank >= nranks)
         return fail(c, SFV_ERR_ARG, "bad px/py/rank/nranks");
     if (nranks > 1 && px * py != nranks) return fail(c, SFV_ERR_ARG, "px*py (%d) != nranks (%d)", px * py, nranks);
+    if (nranks > 1 && c->cfg.viscous)
+        return fail(c, SFV_ERR_UNSUPPORTED, "Navier-Stokes mode is single-rank (loopback blocks) in this build");
     std::vector<int> xs(px + 1), ys(py + 1);
     if (split_impl(c->cfg.ni, px, wx, xs.data()) != SFV_OK || split_impl(c->cfg.nj, py, wy, ys.data()) != SFV_OK)
         return fail(c, SFV_ERR_ARG, "partition: block width < 2 or weight <= 0");
@@ -1228,6 +1292,8 @@ sfv_status sfv_set_halo_mode(sfv_ctx *c, int32_t mode) {
     if (!c) return SFV_ERR_ARG;
     if (!c->bound) return fail(c, SFV_ERR_SEQUENCE, "sfv_set_halo_mode before sfv_bind");
     if (mode != SFV_HALO_COPY && mode != SFV_HALO_PEER) return fail(c, SFV_ERR_ARG, "unknown halo mode %d", mode);
+    if (mode == SFV_HALO_PEER && c->cfg.viscous)
+        return fail(c, SFV_ERR_UNSUPPORTED, "Navier-Stokes mode uses SFV_HALO_COPY");
     if (mode == SFV_HALO_PEER && c->nranks > 1 && !c->peer_ready)
         return fail(c, SFV_ERR_SEQUENCE, "SFV_HALO_PEER across ranks needs sfv_peer_connect first");
     CK(cudaStreamSynchronize(c->st));
@@ -1260,10 +1326,16 @@ sfv_status sfv_debug_block_buffer(sfv_ctx *c, int32_t block, int32_t k, double *
     if (!c || !out) return SFV_ERR_ARG;
     if (!c->bound) return fail(c, SFV_ERR_SEQUENCE, "not bound");
     Block *b = local_block(c, block);
-    if (!b || k < 0 || k >= nbuf_of(c->cfg.rk)) return fail(c, SFV_ERR_ARG, "no local block %d / buffer %d", block, k);
+    if (!b || k < -2 || k >= nbuf_of(c->cfg.rk) || (k < 0 && !c->cfg.viscous))
+        return fail(c, SFV_ERR_ARG, "no local block %d / buffer %d", block, k);
     CK(cudaStreamSynchronize(c->st));
+    if (k == -2) {  // Navier-Stokes gradient frame [(ni+2)*6][nj+2]
+        CK(cudaMemcpy(out, b->grad, sizeof(double) * (size_t)(b->ni + 2) * 6 * b->PG, cudaMemcpyDeviceToHost));
+        return SFV_OK;
+    }
+    const double *src = k == -1 ? b->rv : b->buf[k];
     // rows i = -2 .. ni+1, components, columns j = -2 .. nj+1
-    CK(cudaMemcpy2D(out, sizeof(double) * (b->nj + 4), b->buf[k] + (JOFF - 2), sizeof(double) * b->PJ,
+    CK(cudaMemcpy2D(out, sizeof(double) * (b->nj + 4), src + (JOFF - 2), sizeof(double) * b->PJ,
                     sizeof(double) * (b->nj + 4), (size_t)(b->ni + 4) * 4, cudaMemcpyDeviceToHost));
     return SFV_OK;
 }

@@ -32,7 +32,7 @@ constexpr int WROW = 32 * CPL + 4;  // staged doubles per row: columns j0-2 .. j
 
 
 enum Mode { M_OWN = 0, M_UN = 1, M_RK4F = 2, M_HEUNF = 3 };
-enum Edge { E_INFLOW = 0, E_OUTFLOW = 1, E_SLIP = 2, E_CONNECTED = 3 };
+enum Edge { E_INFLOW = 0, E_OUTFLOW = 1, E_SLIP = 2, E_NOSLIP = 3, E_CONNECTED = 4 };
 
 struct Params {
     double gamma, gm1;
@@ -42,6 +42,8 @@ struct Params {
     double heps, hinv;      // Harten eps and 0.5/eps
     double cfl, dt_fixed;
     int limiter;
+    // Navier-Stokes (readings N-R1..N-R6)
+    double mu, kcond, rgas;  // viscosity, conductivity mu c_p / Pr, gas constant
 };
 
 struct StageArgs {
@@ -91,6 +93,7 @@ struct StageArgs {
     unsigned long long *sig_flag; // local [SIG_RANKS_MAX]: rank r published slot for step >= value
     double *const *rtab;          // [sig_ranks] every rank's sig_tab (mapped; own included)
     unsigned long long *const *rflag;  // [sig_ranks] every rank's sig_flag
+    const double *rv;             // NS: viscous residual sum_f F_v . n A, state layout (NULL = Euler)
     Params P;
 };
 constexpr int FLAG_STRIDE = 16;   // u64 per inbound flag (own 128-B line)
@@ -123,7 +126,23 @@ struct MetricsArgs {
 };
 
 // launchers (sfv_kernels.cu); all asynchronous on `st`
-cudaError_t launch_stage(const StageArgs &a, int mode, bool norms, bool dtmax, bool peer, cudaStream_t st);
+cudaError_t launch_stage(const StageArgs &a, int mode, bool norms, bool dtmax, bool peer, bool visc,
+                         cudaStream_t st);
+// Navier-Stokes per stage: Green-Gauss gradients of (u, v, T)
+// of a block's stage input into grad ([(i+1)*6+q]*PG + j+1, i in [-1, ni],
+// j in [-1, nj]), physical-edge ghost gradients, then the viscous residual
+struct ViscArgs {
+    const double *in;        // stage input (state layout, ghosts filled)
+    const double *met;
+    double *grad;
+    double *rv;              // out: sum over the 4 faces of F_v . n A (state layout)
+    int ni, nj, PJ, PG;
+    int bc[4];               // Edge per W, E, S, N (E_CONNECTED: exchanged ghosts)
+    Params P;
+};
+cudaError_t launch_grad(const ViscArgs &v, cudaStream_t st);
+cudaError_t launch_grad_ghosts(const ViscArgs &v, cudaStream_t st);
+cudaError_t launch_visc(const ViscArgs &v, cudaStream_t st);
 cudaError_t launch_norms(const NormsArgs &f, cudaStream_t st);
 cudaError_t stage_occupancy(int mode, bool norms, bool dtmax, bool fast, bool peer, int *ctas_per_sm);
 bool fast_path(const Params &P);

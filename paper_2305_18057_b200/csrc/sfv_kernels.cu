@@ -255,6 +255,14 @@ __device__ __forceinline__ void mirror(const double u[4], double nx, double ny, 
     g[3] = u[3];
 }
 
+// no-slip adiabatic wall ghost (reading N-R4): momentum negated, rho and E copied
+__device__ __forceinline__ void noslip(const double u[4], double g[4]) {
+    g[0] = u[0];
+    g[1] = -u[1];
+    g[2] = -u[2];
+    g[3] = u[3];
+}
+
 __device__ __forceinline__ void store4(double *buf, int PJ, int i, int j, const double u[4]) {
     double *p = buf + (size_t)((i + 2) * 4) * PJ + (j + JOFF);
 #pragma unroll
@@ -306,7 +314,7 @@ constexpr int SFV_MINB = SFV_MIN_WARPS / WPC;
 constexpr int kRowUnroll = SFV_UNROLL;
 
 
-template <int MODE, bool NORMS, bool DTMAX, bool FAST, bool PEER>
+template <int MODE, bool NORMS, bool DTMAX, bool FAST, bool PEER, bool VISC>
 __global__ void __launch_bounds__(NT, SFV_MINB) stage_kernel(const __grid_constant__ StageArgs a) {
     using TR = StageTraits<MODE>;
     extern __shared__ __align__(128) double smem[];
@@ -368,7 +376,9 @@ __global__ void __launch_bounds__(NT, SFV_MINB) stage_kernel(const __grid_consta
             is_out[k] = col >= j0 && col < j1;
             jflux[k] = col >= j0 && col <= j1;
         }
-        auto writes_ghost = [&](int e) { return a.bc[e] == E_SLIP || a.bc[e] == E_OUTFLOW; };
+        auto writes_ghost = [&](int e) {
+            return a.bc[e] == E_SLIP || a.bc[e] == E_OUTFLOW || (VISC && a.bc[e] == E_NOSLIP);
+        };
         // edges whose ghost frame this task reads (and, for peer edges, whose
         // neighbour ghost frame it writes): segments at i = 0 / ni, strips
         // whose staged columns reach j = -1 / nj
@@ -594,6 +604,11 @@ __global__ void __launch_bounds__(NT, SFV_MINB) stage_kernel(const __grid_consta
                 double R[4], U[4];
 #pragma unroll
                 for (int c = 0; c < 4; ++c) R[c] = ((GE[k][c] - GW[k][c]) + GN[k][c]) - GS[k][c];
+                if constexpr (VISC) {  // R = sum (F - F_v) ds (Eq. 5): the viscous sum of this cell
+                    const double *rvp = a.rv + (size_t)((v + 2) * 4) * PJ + (jc + k + JOFF);
+#pragma unroll
+                    for (int c = 0; c < 4; ++c) R[c] -= __ldg(rvp + (size_t)c * PJ);
+                }
 #pragma unroll
                 for (int c = 0; c < 4; ++c) {
                     const double rv = R[c] * iV;
@@ -632,6 +647,9 @@ __global__ void __launch_bounds__(NT, SFV_MINB) stage_kernel(const __grid_consta
                     } else if (a.bc[2] == E_OUTFLOW && jk == 0) {
                         store4(a.out, PJ, v, -1, U);
                         store4(a.out, PJ, v, -2, U);
+                    } else if (VISC && a.bc[2] == E_NOSLIP && jk <= 1) {
+                        const double g[4] = {U[0], -U[1], -U[2], U[3]};
+                        store4(a.out, PJ, v, -1 - jk, g);
                     }
                     if (a.bc[3] == E_SLIP && jk >= a.nj - 2) {
                         double g[4];
@@ -641,6 +659,9 @@ __global__ void __launch_bounds__(NT, SFV_MINB) stage_kernel(const __grid_consta
                     } else if (a.bc[3] == E_OUTFLOW && jk == a.nj - 1) {
                         store4(a.out, PJ, v, a.nj, U);
                         store4(a.out, PJ, v, a.nj + 1, U);
+                    } else if (VISC && a.bc[3] == E_NOSLIP && jk >= a.nj - 2) {
+                        const double g[4] = {U[0], -U[1], -U[2], U[3]};
+                        store4(a.out, PJ, v, a.nj + (a.nj - 1 - jk), g);
                     }
                     if (a.bc[0] == E_SLIP && v <= 1) {  // segments start at 0 or >= 4 (choose_launch)
                         double g[4];
@@ -649,6 +670,9 @@ __global__ void __launch_bounds__(NT, SFV_MINB) stage_kernel(const __grid_consta
                     } else if (a.bc[0] == E_OUTFLOW && v == 0) {
                         store4(a.out, PJ, -1, jk, U);
                         store4(a.out, PJ, -2, jk, U);
+                    } else if (VISC && a.bc[0] == E_NOSLIP && v <= 1) {
+                        const double g[4] = {U[0], -U[1], -U[2], U[3]};
+                        store4(a.out, PJ, -1 - v, jk, g);
                     }
                     if (a.bc[1] == E_SLIP && v >= a.ni - 2) {
                         double g[4];
@@ -659,6 +683,9 @@ __global__ void __launch_bounds__(NT, SFV_MINB) stage_kernel(const __grid_consta
                     } else if (a.bc[1] == E_OUTFLOW && v == a.ni - 1) {
                         store4(a.out, PJ, a.ni, jk, U);
                         store4(a.out, PJ, a.ni + 1, jk, U);
+                    } else if (VISC && a.bc[1] == E_NOSLIP && v >= a.ni - 2) {
+                        const double g[4] = {U[0], -U[1], -U[2], U[3]};
+                        store4(a.out, PJ, a.ni + (a.ni - 1 - v), jk, g);
                     }
                 }
                 if constexpr (PEER) {
@@ -878,9 +905,9 @@ cudaError_t launch_norms(const NormsArgs &f, cudaStream_t st) {
     return cudaGetLastError();
 }
 
-template <int MODE, bool NORMS, bool DTMAX, bool FAST, bool PEER>
+template <int MODE, bool NORMS, bool DTMAX, bool FAST, bool PEER, bool VISC>
 static cudaError_t launch_t(const StageArgs &a, cudaStream_t st) {
-    auto k = stage_kernel<MODE, NORMS, DTMAX, FAST, PEER>;
+    auto k = stage_kernel<MODE, NORMS, DTMAX, FAST, PEER, VISC>;
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3((a.nstrips * a.nseg + WPC - 1) / WPC);
     cfg.blockDim = dim3(NT);
@@ -894,52 +921,63 @@ static cudaError_t launch_t(const StageArgs &a, cudaStream_t st) {
     return cudaLaunchKernelEx(&cfg, k, a);
 }
 
-template <int MODE, bool NORMS, bool DTMAX, bool FAST, bool PEER>
+template <int MODE, bool NORMS, bool DTMAX, bool FAST, bool PEER, bool VISC>
 static cudaError_t occ_t(int *n) {
-    auto k = stage_kernel<MODE, NORMS, DTMAX, FAST, PEER>;
+    auto k = stage_kernel<MODE, NORMS, DTMAX, FAST, PEER, VISC>;
     const size_t sm = stage_smem<MODE>();
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     if (e != cudaSuccess) return e;
     return cudaOccupancyMaxActiveBlocksPerMultiprocessor(n, k, NT, sm);
 }
 
-#define SFV_DISPATCH_F(FN, F, Q, ...)                                                  \
+#define SFV_DISPATCH_F(FN, F, Q, V, ...)                                               \
     switch (mode * 4 + (norms ? 2 : 0) + (dtmax ? 1 : 0)) {                              \
-        case M_OWN * 4 + 2: return FN<M_OWN, true, false, F, Q>(__VA_ARGS__);            \
-        case M_OWN * 4 + 0: return FN<M_OWN, false, false, F, Q>(__VA_ARGS__);           \
-        case M_UN * 4 + 0: return FN<M_UN, false, false, F, Q>(__VA_ARGS__);             \
-        case M_UN * 4 + 1: return FN<M_UN, false, true, F, Q>(__VA_ARGS__);              \
-        case M_RK4F * 4 + 1: return FN<M_RK4F, false, true, F, Q>(__VA_ARGS__);          \
-        case M_RK4F * 4 + 0: return FN<M_RK4F, false, false, F, Q>(__VA_ARGS__);         \
-        case M_HEUNF * 4 + 1: return FN<M_HEUNF, false, true, F, Q>(__VA_ARGS__);        \
-        case M_HEUNF * 4 + 0: return FN<M_HEUNF, false, false, F, Q>(__VA_ARGS__);       \
+        case M_OWN * 4 + 2: return FN<M_OWN, true, false, F, Q, V>(__VA_ARGS__);         \
+        case M_OWN * 4 + 0: return FN<M_OWN, false, false, F, Q, V>(__VA_ARGS__);        \
+        case M_UN * 4 + 0: return FN<M_UN, false, false, F, Q, V>(__VA_ARGS__);          \
+        case M_UN * 4 + 1: return FN<M_UN, false, true, F, Q, V>(__VA_ARGS__);           \
+        case M_RK4F * 4 + 1: return FN<M_RK4F, false, true, F, Q, V>(__VA_ARGS__);       \
+        case M_RK4F * 4 + 0: return FN<M_RK4F, false, false, F, Q, V>(__VA_ARGS__);      \
+        case M_HEUNF * 4 + 1: return FN<M_HEUNF, false, true, F, Q, V>(__VA_ARGS__);     \
+        case M_HEUNF * 4 + 0: return FN<M_HEUNF, false, false, F, Q, V>(__VA_ARGS__);    \
         default: return cudaErrorInvalidValue;                                           \
     }
+// (peer halos and Navier-Stokes are not combined: NS runs in copy mode)
 #define SFV_DISPATCH(FN, ...)                                                             \
+    if (peer && visc) return cudaErrorNotSupported;                                       \
     if (fast) {                                                                           \
-        if (peer) { SFV_DISPATCH_F(FN, true, true, __VA_ARGS__) }                         \
-        else { SFV_DISPATCH_F(FN, true, false, __VA_ARGS__) }                             \
+        if (peer) { SFV_DISPATCH_F(FN, true, true, false, __VA_ARGS__) }                  \
+        else if (visc) { SFV_DISPATCH_F(FN, true, false, true, __VA_ARGS__) }             \
+        else { SFV_DISPATCH_F(FN, true, false, false, __VA_ARGS__) }                      \
     } else {                                                                              \
-        if (peer) { SFV_DISPATCH_F(FN, false, true, __VA_ARGS__) }                        \
-        else { SFV_DISPATCH_F(FN, false, false, __VA_ARGS__) }                            \
+        if (peer) { SFV_DISPATCH_F(FN, false, true, false, __VA_ARGS__) }                 \
+        else if (visc) { SFV_DISPATCH_F(FN, false, false, true, __VA_ARGS__) }            \
+        else { SFV_DISPATCH_F(FN, false, false, false, __VA_ARGS__) }                     \
     }
 
 // fast = bounded van Albada with kappa = -1 (the default scheme, reading A-R3/A-R7)
 bool fast_path(const Params &P) { return P.limiter == 1 && P.c2 == 0.0; }
-cudaError_t launch_stage(const StageArgs &a, int mode, bool norms, bool dtmax, bool peer, cudaStream_t st) {
+cudaError_t launch_stage(const StageArgs &a, int mode, bool norms, bool dtmax, bool peer, bool visc,
+                         cudaStream_t st) {
     const bool fast = fast_path(a.P);
     SFV_DISPATCH(launch_t, a, st)
 }
 cudaError_t stage_occupancy(int mode, bool norms, bool dtmax, bool fast, bool peer, int *n) {
+    const bool visc = false;
+    SFV_DISPATCH(occ_t, n)
+}
+static cudaError_t stage_occupancy_v(int mode, bool norms, bool dtmax, bool fast, int *n) {
+    const bool peer = false, visc = true;
     SFV_DISPATCH(occ_t, n)
 }
 cudaError_t prepare_stage_kernels() {
     const int variants[8][3] = {{M_OWN, 1, 0}, {M_OWN, 0, 0}, {M_UN, 0, 0}, {M_UN, 0, 1},
                                 {M_RK4F, 0, 1}, {M_RK4F, 0, 0}, {M_HEUNF, 0, 1}, {M_HEUNF, 0, 0}};
     for (auto &v : variants)
-        for (int f = 0; f < 4; ++f) {
+        for (int f = 0; f < 6; ++f) {
             int n = 0;
-            cudaError_t e = stage_occupancy(v[0], v[1] != 0, v[2] != 0, (f & 1) != 0, (f & 2) != 0, &n);
+            cudaError_t e = f < 4 ? stage_occupancy(v[0], v[1] != 0, v[2] != 0, (f & 1) != 0, (f & 2) != 0, &n)
+                                  : stage_occupancy_v(v[0], v[1] != 0, v[2] != 0, (f & 1) != 0, &n);
             if (e != cudaSuccess) return e;
         }
     return cudaSuccess;
@@ -995,6 +1033,118 @@ cudaError_t launch_metrics(const MetricsArgs &a, cudaStream_t st) {
     return cudaGetLastError();
 }
 
+// ------------------------------------------------------------ Navier-Stokes
+// Per stage: Green-Gauss gradients of (u, v, T) (reading N-R2), ghost
+// gradients of physical edges (N-R1; connected edges are exchanged by the
+// host), then the viscous residual sum_f F_v . n A per cell (Eq. 2 viscous
+// flux, N-R3/N-R5), which the stage kernel subtracts from the inviscid one.
+// Straightforward one-thread-per-cell kernels: correctness first.
+__device__ __forceinline__ void uvT(const double *buf, int PJ, int i, int j, const Params &P, double o[3]) {
+    const double *q = buf + (size_t)((i + 2) * 4) * PJ + (j + JOFF);
+    const double r = q[0], ir = 1.0 / r;
+    const double u = q[PJ] * ir, v = q[2 * (size_t)PJ] * ir;
+    const double p = P.gm1 * (q[3 * (size_t)PJ] - 0.5 * (q[PJ] * u + q[2 * (size_t)PJ] * v));
+    o[0] = u;
+    o[1] = v;
+    o[2] = p * ir / P.rgas;
+}
+__device__ __forceinline__ double metf(const double *met, int PJ, int row, int f, int j) {
+    return met[(size_t)(row * NMET + f) * PJ + j + JOFF];
+}
+__device__ __forceinline__ double *gradp(double *grad, int PG, int i, int j, int q) {
+    return grad + (size_t)((i + 1) * 6 + q) * PG + (j + 1);
+}
+
+__global__ void grad_kernel(const ViscArgs a) {
+    const int j = blockIdx.x * blockDim.x + threadIdx.x, i = blockIdx.y;
+    if (j >= a.nj) return;
+    double c[3], w[3], e[3], s[3], n[3];
+    uvT(a.in, a.PJ, i, j, a.P, c);
+    uvT(a.in, a.PJ, i - 1, j, a.P, w);
+    uvT(a.in, a.PJ, i + 1, j, a.P, e);
+    uvT(a.in, a.PJ, i, j - 1, a.P, s);
+    uvT(a.in, a.PJ, i, j + 1, a.P, n);
+    // faces: the mean of the two cells times A
+    const double wx = metf(a.met, a.PJ, i, 0, j), wy = metf(a.met, a.PJ, i, 1, j), wA = metf(a.met, a.PJ, i, 2, j);
+    const double ex = metf(a.met, a.PJ, i + 1, 0, j), ey = metf(a.met, a.PJ, i + 1, 1, j),
+                 eA = metf(a.met, a.PJ, i + 1, 2, j);
+    const double sx = metf(a.met, a.PJ, i + 1, 3, j), sy = metf(a.met, a.PJ, i + 1, 4, j),
+                 sA = metf(a.met, a.PJ, i + 1, 5, j);
+    const double nx = metf(a.met, a.PJ, i + 1, 3, j + 1), ny = metf(a.met, a.PJ, i + 1, 4, j + 1),
+                 nA = metf(a.met, a.PJ, i + 1, 5, j + 1);
+    const double iV = metf(a.met, a.PJ, i + 1, 6, j);
+#pragma unroll
+    for (int q = 0; q < 3; ++q) {
+        const double fE = 0.5 * (c[q] + e[q]) * eA, fW = 0.5 * (w[q] + c[q]) * wA;
+        const double fN = 0.5 * (c[q] + n[q]) * nA, fS = 0.5 * (s[q] + c[q]) * sA;
+        *gradp(a.grad, a.PG, i, j, 2 * q) = (((fE * ex - fW * wx) + fN * nx) - fS * sx) * iV;
+        *gradp(a.grad, a.PG, i, j, 2 * q + 1) = (((fE * ey - fW * wy) + fN * ny) - fS * sy) * iV;
+    }
+}
+
+__global__ void grad_ghost_kernel(const ViscArgs a) {
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    for (int q = 0; q < 6; ++q) {
+        if (k < a.nj) {
+            if (a.bc[0] != E_CONNECTED) *gradp(a.grad, a.PG, -1, k, q) = *gradp(a.grad, a.PG, 0, k, q);
+            if (a.bc[1] != E_CONNECTED) *gradp(a.grad, a.PG, a.ni, k, q) = *gradp(a.grad, a.PG, a.ni - 1, k, q);
+        }
+        if (k < a.ni) {
+            if (a.bc[2] != E_CONNECTED) *gradp(a.grad, a.PG, k, -1, q) = *gradp(a.grad, a.PG, k, 0, q);
+            if (a.bc[3] != E_CONNECTED) *gradp(a.grad, a.PG, k, a.nj, q) = *gradp(a.grad, a.PG, k, a.nj - 1, q);
+        }
+    }
+}
+
+// F_v . n A of the face between cells L and R (the lower-index cell is L)
+__device__ __forceinline__ void face_visc(const ViscArgs &a, int iL, int jL, int iR, int jR, double nx, double ny,
+                                          double A, double F[4]) {
+    double pl[3], pr[3], g[6];
+    uvT(a.in, a.PJ, iL, jL, a.P, pl);
+    uvT(a.in, a.PJ, iR, jR, a.P, pr);
+#pragma unroll
+    for (int q = 0; q < 6; ++q) g[q] = 0.5 * (*gradp(a.grad, a.PG, iL, jL, q) + *gradp(a.grad, a.PG, iR, jR, q));
+    const double u = 0.5 * (pl[0] + pr[0]), v = 0.5 * (pl[1] + pr[1]);
+    const double mu = a.P.mu, lam = -2.0 * mu / 3.0, div = g[0] + g[3];
+    const double txx = 2.0 * mu * g[0] + lam * div, tyy = 2.0 * mu * g[3] + lam * div, txy = mu * (g[1] + g[2]);
+    const double thx = u * txx + v * txy + a.P.kcond * g[4], thy = u * txy + v * tyy + a.P.kcond * g[5];
+    F[0] = 0.0;
+    F[1] = (txx * nx + txy * ny) * A;
+    F[2] = (txy * nx + tyy * ny) * A;
+    F[3] = (thx * nx + thy * ny) * A;
+}
+
+__global__ void visc_kernel(const ViscArgs a) {
+    const int j = blockIdx.x * blockDim.x + threadIdx.x, i = blockIdx.y;
+    if (j >= a.nj) return;
+    double FW[4], FE[4], FS[4], FN[4];
+    face_visc(a, i - 1, j, i, j, metf(a.met, a.PJ, i, 0, j), metf(a.met, a.PJ, i, 1, j), metf(a.met, a.PJ, i, 2, j),
+              FW);
+    face_visc(a, i, j, i + 1, j, metf(a.met, a.PJ, i + 1, 0, j), metf(a.met, a.PJ, i + 1, 1, j),
+              metf(a.met, a.PJ, i + 1, 2, j), FE);
+    face_visc(a, i, j - 1, i, j, metf(a.met, a.PJ, i + 1, 3, j), metf(a.met, a.PJ, i + 1, 4, j),
+              metf(a.met, a.PJ, i + 1, 5, j), FS);
+    face_visc(a, i, j, i, j + 1, metf(a.met, a.PJ, i + 1, 3, j + 1), metf(a.met, a.PJ, i + 1, 4, j + 1),
+              metf(a.met, a.PJ, i + 1, 5, j + 1), FN);
+    double *o = a.rv + (size_t)((i + 2) * 4) * a.PJ + (j + JOFF);
+#pragma unroll
+    for (int c = 0; c < 4; ++c) o[(size_t)c * a.PJ] = ((FE[c] - FW[c]) + FN[c]) - FS[c];
+}
+
+cudaError_t launch_grad(const ViscArgs &v, cudaStream_t st) {
+    grad_kernel<<<dim3((v.nj + 127) / 128, v.ni), 128, 0, st>>>(v);
+    return cudaGetLastError();
+}
+cudaError_t launch_grad_ghosts(const ViscArgs &v, cudaStream_t st) {
+    const int n = v.ni > v.nj ? v.ni : v.nj;
+    grad_ghost_kernel<<<(n + 127) / 128, 128, 0, st>>>(v);
+    return cudaGetLastError();
+}
+cudaError_t launch_visc(const ViscArgs &v, cudaStream_t st) {
+    visc_kernel<<<dim3((v.nj + 127) / 128, v.ni), 128, 0, st>>>(v);
+    return cudaGetLastError();
+}
+
 // --------------------------------------------------------- init / transpose
 __global__ void fill_kernel(double *p, long long n, double v) {
     for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < n; k += (long long)gridDim.x * blockDim.x)
@@ -1042,18 +1192,22 @@ __global__ void bc_fill_kernel(double *buf, const double *met, int ni, int nj, i
         if (bc.x == E_INFLOW) { double q[4] = {in0.x, in0.y, in0.z, in0.w}; st(-1 - m, j, q); }
         else if (bc.x == E_OUTFLOW) { ld(0, j, u); st(-1 - m, j, u); }
         else if (bc.x == E_SLIP) { ld(m, j, u); mirror(u, metv(0, 0, j), metv(0, 1, j), g); st(-1 - m, j, g); }
+        else if (bc.x == E_NOSLIP) { ld(m, j, u); noslip(u, g); st(-1 - m, j, g); }
         if (bc.y == E_INFLOW) { double q[4] = {in1.x, in1.y, in1.z, in1.w}; st(ni + m, j, q); }
         else if (bc.y == E_OUTFLOW) { ld(ni - 1, j, u); st(ni + m, j, u); }
         else if (bc.y == E_SLIP) { ld(ni - 1 - m, j, u); mirror(u, metv(ni, 0, j), metv(ni, 1, j), g); st(ni + m, j, g); }
+        else if (bc.y == E_NOSLIP) { ld(ni - 1 - m, j, u); noslip(u, g); st(ni + m, j, g); }
     }
     if (k < ni) {  // S and N edges, row k
         const int i = k;
         if (bc.z == E_INFLOW) { double q[4] = {in2.x, in2.y, in2.z, in2.w}; st(i, -1 - m, q); }
         else if (bc.z == E_OUTFLOW) { ld(i, 0, u); st(i, -1 - m, u); }
         else if (bc.z == E_SLIP) { ld(i, m, u); mirror(u, metv(i + 1, 3, 0), metv(i + 1, 4, 0), g); st(i, -1 - m, g); }
+        else if (bc.z == E_NOSLIP) { ld(i, m, u); noslip(u, g); st(i, -1 - m, g); }
         if (bc.w == E_INFLOW) { double q[4] = {in3.x, in3.y, in3.z, in3.w}; st(i, nj + m, q); }
         else if (bc.w == E_OUTFLOW) { ld(i, nj - 1, u); st(i, nj + m, u); }
         else if (bc.w == E_SLIP) { ld(i, nj - 1 - m, u); mirror(u, metv(i + 1, 3, nj), metv(i + 1, 4, nj), g); st(i, nj + m, g); }
+        else if (bc.w == E_NOSLIP) { ld(i, nj - 1 - m, u); noslip(u, g); st(i, nj + m, g); }
     }
 }
 cudaError_t launch_bc_fill(double *buf, const double *met, int ni, int nj, int PJ, const int bc[4],

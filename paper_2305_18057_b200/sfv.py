@@ -45,7 +45,8 @@ class sfv_config(C.Structure):
                 ("harten_eps", C.c_double), ("rk", C.c_int32),
                 ("cfl", C.c_double), ("dt_fixed", C.c_double),
                 ("bc", C.c_int32 * 4), ("inflow_U", (C.c_double * 4) * 4),
-                ("max_history", C.c_int64)]
+                ("max_history", C.c_int64), ("viscous", C.c_int32), ("mu", C.c_double),
+                ("prandtl", C.c_double), ("gas_R", C.c_double)]
 
 
 _lib = None
@@ -107,6 +108,8 @@ def make_config(d):
         for k in range(4):
             c.inflow_U[e][k] = float(d["inflow_U"][e][k])
     c.max_history = d["max_history"]
+    c.viscous = int(d.get("viscous", 0)); c.mu = float(d.get("mu", 0.0))
+    c.prandtl = float(d.get("prandtl", 0.72)); c.gas_R = float(d.get("gas_R", 287.0))
     return c
 
 
@@ -287,7 +290,7 @@ class Solver:
         frame, as an array [ni_b+4, 4, nj_b+4] (index i+2, c, j+2)."""
         m = self.partition_map(block)
         nib, njb = int(m[1] - m[0]), int(m[3] - m[2])
-        out = np.empty((nib + 4, 4, njb + 4))
+        out = np.empty((nib + 2, 6, njb + 2)) if k == -2 else np.empty((nib + 4, 4, njb + 4))
         self._check(lib().sfv_debug_block_buffer(self._h, block, k, _dp(out)))
         return out
 

@@ -117,3 +117,15 @@ def test_halo_mode_calls_need_bind():
     assert L.sfv_peer_handle(s._h, C.cast(buf, C.c_void_p)) == sfv.ERR_SEQUENCE
     assert L.sfv_peer_connect(s._h, C.cast(buf, C.c_void_p)) == sfv.ERR_SEQUENCE
     assert L.sfv_peer_handle(None, C.cast(buf, C.c_void_p)) == sfv.ERR_ARG
+
+
+def test_noslip_and_viscous_validation():
+    X, Y = I.ramp_nodes(8, 4, 30.0)
+    with pytest.raises(sfv.SfvError) as ei:  # no-slip wall needs the viscous mode
+        sfv.Solver(I.default_config(8, 4, bc=(0, 1, 3, 2)), X, Y, bind=False)
+    assert ei.value.code == sfv.ERR_ARG
+    with pytest.raises(sfv.SfvError) as ei:
+        sfv.Solver(I.default_config(8, 4, viscous=1, mu=-1.0), X, Y, bind=False)
+    assert ei.value.code == sfv.ERR_ARG
+    s = sfv.Solver(I.default_config(8, 4, viscous=1, mu=0.1, bc=(0, 1, 3, 3)), X, Y, bind=False)
+    s.close()

@@ -1,0 +1,99 @@
+"""Navier-Stokes mode on the GPU vs the oracle (Eq. 2
+viscous flux; readings N-R1..N-R6).  Same gates as the
+Euler path: per conserved variable e_k <= 1e-12 after 1 step; residual-norm
+histories 1e-10; dt 1e-13; loopback decompositions bitwise equal to one
+block (ghost gradients at cuts are the neighbour's own, N-R1)."""
+import numpy as np
+import pytest
+
+from paper_2305_18057_b200 import inputs as I
+from parity_util import dt_error, norm_error, state_error
+
+pytestmark = pytest.mark.gpu
+
+NOSLIP_S = (I.BC_INFLOW, I.BC_OUTFLOW, I.BC_NOSLIP_WALL, I.BC_SLIP_WALL)
+
+
+@pytest.fixture(scope="module")
+def sfv_mod():
+    import torch
+    assert torch.cuda.is_available(), "GPU tests need a CUDA device"
+    from paper_2305_18057_b200 import sfv
+    sfv.lib()
+    return sfv
+
+
+def _pair(sfv_mod, oracle_mod, cfg, X, Y, U0, steps, **kw):
+    g = sfv_mod.Solver(cfg, X, Y, **kw)
+    g.set_state(U0); g.step(steps); g.sync()
+    o = oracle_mod.Oracle(cfg, X, Y)
+    o.set_state(U0); o.step(steps)
+    return g, o
+
+
+@pytest.mark.parametrize("steps,tol", [(1, 1e-12), (100, 1e-10)])
+@pytest.mark.parametrize("mu", [0.02, 0.2])
+def test_ns_parity(sfv_mod, oracle_mod, steps, tol, mu):
+    ni, nj = 64, 32
+    X, Y = I.ramp_nodes(ni, nj, 5.0)  # (the impulsive Mach-4 start over a steeper no-slip ramp is not stable)
+    cfg = I.default_config(ni, nj, viscous=1, mu=mu, bc=NOSLIP_S)
+    U0 = I.perturbed_state(ni, nj, 21)
+    g, o = _pair(sfv_mod, oracle_mod, cfg, X, Y, U0, steps)
+    e = state_error(g.get_state(), o.get_state())
+    assert np.all(e <= tol), e
+    assert norm_error(g.residual_norms(), o.residual_norms()) <= 1e-10
+    assert dt_error(g.dt(), o.dt()) <= 1e-13
+
+
+@pytest.mark.parametrize("rk", [I.RK2_HEUN, I.RK4_JAMESON])
+def test_ns_tableaus(sfv_mod, oracle_mod, rk):
+    ni, nj = 48, 40
+    X, Y = I.ramp_nodes(ni, nj, 5.0)
+    cfg = I.default_config(ni, nj, rk=rk, viscous=1, mu=0.3,
+                           bc=(I.BC_INFLOW, I.BC_OUTFLOW, I.BC_NOSLIP_WALL, I.BC_NOSLIP_WALL))
+    U0 = I.perturbed_state(ni, nj, 5)
+    g, o = _pair(sfv_mod, oracle_mod, cfg, X, Y, U0, 10)
+    assert np.all(state_error(g.get_state(), o.get_state()) <= 1e-11)
+
+
+@pytest.mark.parametrize("px,py", [(2, 1), (1, 3), (2, 2), (3, 2)])
+def test_ns_loopback_bitwise(sfv_mod, oracle_mod, px, py):
+    ni, nj = 90, 70
+    X, Y = I.ramp_nodes(ni, nj, 5.0)
+    cfg = I.default_config(ni, nj, viscous=1, mu=0.2, bc=NOSLIP_S)
+    U0 = I.perturbed_state(ni, nj, 8)
+    g1 = sfv_mod.Solver(cfg, X, Y); g1.set_state(U0); g1.step(20); g1.sync()
+    gp = sfv_mod.Solver(cfg, X, Y, px=px, py=py); gp.set_state(U0); gp.step(20); gp.sync()
+    np.testing.assert_array_equal(gp.get_state(), g1.get_state())
+    np.testing.assert_array_equal(gp.dt(), g1.dt())
+    o = oracle_mod.Oracle(cfg, X, Y); o.set_state(U0); o.step(20)
+    assert np.all(state_error(gp.get_state(), o.get_state()) <= 1e-11)
+
+
+def test_ns_peer_mode_unsupported(sfv_mod):
+    ni, nj = 32, 16
+    X, Y = I.ramp_nodes(ni, nj, 15.0)
+    g = sfv_mod.Solver(I.default_config(ni, nj, viscous=1, mu=0.1), X, Y, px=2)
+    with pytest.raises(sfv_mod.SfvError) as ex:
+        g.set_halo_mode(sfv_mod.HALO_PEER)
+    assert ex.value.code == sfv_mod.ERR_UNSUPPORTED
+
+
+def test_ns_operator_matches_oracle(sfv_mod, oracle_mod):
+    """The GPU's Green-Gauss gradients and viscous residual sum_f F_v . n A of
+    a stage input (Heun stage 2 input W2, read back through
+    sfv_debug_block_buffer) equal the oracle's on the same state:
+    gradients to 1e-13, R_v to 1e-11 of its maximum."""
+    ni, nj = 64, 32
+    X, Y = I.ramp_nodes(ni, nj, 15.0)
+    cfg = I.default_config(ni, nj, viscous=1, mu=0.05, rk=I.RK2_HEUN, dt_fixed=1e-6, bc=NOSLIP_S)
+    g = sfv_mod.Solver(cfg, X, Y)
+    g.set_state(I.perturbed_state(ni, nj, 21)); g.step(1); g.sync()
+    W2 = np.transpose(g.block_buffer(0, 1)[2:-2, :, 2:-2], (2, 0, 1)).copy()
+    rv = np.transpose(g.block_buffer(0, -1)[2:-2, :, 2:-2], (2, 0, 1))
+    G = np.transpose(g.block_buffer(0, -2)[1:-1, :, 1:-1], (2, 0, 1))
+    o = oracle_mod.Oracle(cfg, X, Y)
+    Rv = -(o.residual(W2) - oracle_mod.Oracle(dict(cfg, mu=0.0), X, Y).residual(W2))
+    Go = o.gradients(W2)
+    assert np.max(np.abs(G - Go)) <= 1e-13 * np.max(np.abs(Go))
+    assert np.max(np.abs(rv - Rv)) <= 1e-11 * np.max(np.abs(Rv))
