@@ -136,7 +136,13 @@ def measured_peak():
         return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
 
 
-def cpu_baseline_oracle(budget_s=15.0, steps_cap=None):
+# --ns: constant viscosity (Re ~ 2e5 on the unit-length inlet).  The walls stay slip walls: the
+# impulsive Mach-4 start against a no-slip 30-degree ramp is not stable under the inviscid CFL
+# (it fails within a few steps on the C2 grid); the no-slip wall is exercised by tests/test_gpu_ns.py.
+NS_MU = 1.0e-3
+
+
+def cpu_baseline_oracle(budget_s=15.0, steps_cap=None, ns=False):
     """The oracle, as it stands, single-threaded on a bounded sample: the
     bottom rows of the C2 grid (ramp included) for a few RK4 steps."""
     import oracle
@@ -144,7 +150,7 @@ def cpu_baseline_oracle(budget_s=15.0, steps_cap=None):
     ni = 1440
     rows = 16
     X, Y = I.ramp_nodes(ni, rows, 30.0)
-    cfg = I.default_config(ni, rows)
+    cfg = I.default_config(ni, rows, **(dict(viscous=1, mu=NS_MU) if ns else {}))
     o = oracle.Oracle(cfg, X, Y)
     o.set_state(I.uniform_state(ni, rows))
     o.step(1)  # warm
@@ -156,8 +162,8 @@ def cpu_baseline_oracle(budget_s=15.0, steps_cap=None):
     dt = time.perf_counter() - t0
     v = ni * rows * 4 * n / dt / 1e6
     return {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle",
-            "sample": f"C2 grid bottom {rows} rows ({ni}x{rows} cells incl. ramp), {n} RK4 steps, "
-                      f"{dt:.1f} s single-threaded -O2 -ffp-contract=off"}
+            "sample": f"C2 grid bottom {rows} rows ({ni}x{rows} cells incl. ramp), {n} RK4 steps"
+                      f"{' (Navier-Stokes)' if ns else ''}, {dt:.1f} s single-threaded -O2 -ffp-contract=off"}
 
 
 def run_reference(args, rank, world):
@@ -207,6 +213,8 @@ def main():
     ap.add_argument("--blocks", type=int, default=1,
                     help="N = 1 only: decompose the grid into this many slabs on the one GPU (loopback "
                          "partition-overhead experiment; not the headline configuration)")
+    ap.add_argument("--ns", action="store_true",
+                    help="Navier-Stokes mode (SURVEY §8(f) f4): viscous flux with mu = 1e-3")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     args = ap.parse_args()
@@ -250,7 +258,10 @@ def main():
         desc += f"; {px} loopback slabs on one GPU"
     X, Y = I.ramp_nodes(ni, nj, theta)
     rk = {"rk4": I.RK4_CLASSIC, "heun": I.RK2_HEUN, "jst4": I.RK4_JAMESON}[args.rk]
-    cfg = I.default_config(ni, nj, rk=rk, max_history=max(args.steps + args.warmup + 16, 64))
+    cfg = I.default_config(ni, nj, rk=rk, max_history=max(args.steps + args.warmup + 16, 64),
+                           **(dict(viscous=1, mu=NS_MU) if args.ns else {}))
+    if args.ns:
+        desc = "Navier-Stokes terms (mu = 1e-3, Green-Gauss gradients; slip walls) on " + desc
     U0 = I.uniform_state(ni, nj)
     nccl_id = None
     if world > 1:
@@ -262,6 +273,8 @@ def main():
                         device=local_rank, stream=stream)
     nblk = px if world == 1 else 1
     halo_note = args.halo
+    if args.ns:
+        args.halo = "copy"  # NS runs with copy-mode halos (single rank)
     if args.halo == "peer" and px > 1:
         if world == 1:
             solver.enable_peer_halo()
@@ -316,7 +329,8 @@ def main():
     if args.halo == "peer":
         edges = 0
     nbatch = (args.warmup + args.steps) // 32 - args.warmup // 32
-    launches = int(round(nblk * (stages * (1 + edges) * args.steps + nbatch)))
+    # (Navier-Stokes: + gradient and viscous-residual kernels per stage)
+    launches = int(round(nblk * (stages * (1 + edges + (2 if args.ns else 0)) * args.steps + nbatch)))
     stage_launches = stages * args.steps * nblk
 
     # ---- roofline of the dominant kernel (the fused stage kernel) ----
@@ -331,7 +345,8 @@ def main():
     hbm = {"bound": "hbm", "achieved": hbm_achieved, "peak": peak, "unit": "GB/s", "frac": hbm_achieved / peak,
            "traffic": (traffic_pc * cells_launch) if traffic_pc else None,
            "alg_bytes_per_cell_stage": ALG_BYTES_PER_CELL_STAGE, "peak_source": peak_src}
-    roof = dict(hbm, kernel="sfv::stage_kernel (4 launches per step, averaged)")
+    roof = dict(hbm, kernel=("sfv::stage_kernel + NS gradient/viscous kernels (per stage, averaged)" if args.ns
+                                  else "sfv::stage_kernel (4 launches per step, averaged)"))
     if prof and prof.get("fp64_inst_per_cell_stage"):
         # FP64 pipe is the nearer roof: report it as the bound, HBM alongside
         fp64_rate = prof["fp64_inst_per_cell_stage"] * cells_launch / avg_launch_s
@@ -339,7 +354,8 @@ def main():
                 "unit": "T FP64-inst/s", "frac": fp64_rate / FP64_PEAK_INST_S,
                 "traffic": hbm["traffic"], "fp64_inst_per_cell_stage": prof["fp64_inst_per_cell_stage"],
                 "peak_source": "measured DFMA issue rate (profiles/r1_fp64_microbench.txt)",
-                "profile": prof.get("source"), "kernel": "sfv::stage_kernel (4 launches per step, averaged)",
+                "profile": prof.get("source"), "kernel": ("sfv::stage_kernel + NS gradient/viscous kernels (per stage, averaged)" if args.ns
+                           else "sfv::stage_kernel (4 launches per step, averaged)"),
                 "hbm": hbm}
     # ---- end to end through the public API with host buffers ----
     e2e = None
@@ -367,7 +383,7 @@ def main():
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        cpu = cpu_baseline_oracle()
+        cpu = cpu_baseline_oracle(ns=args.ns)
 
     li = solver.launch_info()
     halo_info = None

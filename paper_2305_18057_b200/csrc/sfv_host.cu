@@ -258,6 +258,7 @@ void build_params(sfv_ctx *c) {
     P.limiter = f.limiter;
     P.mu = f.viscous ? f.mu : 0.0;
     P.rgas = f.gas_R > 0.0 ? f.gas_R : 287.0;
+    P.rgas_inv = 1.0 / P.rgas;
     P.kcond = f.viscous ? f.mu * (f.gamma * P.rgas / (f.gamma - 1.0)) / f.prandtl : 0.0;
 }
 
@@ -613,11 +614,7 @@ sfv_status enqueue_viscous(sfv_ctx *c, int in, cudaStream_t st) {
         v.P = c->P;
         return v;
     };
-    for (Block &b : c->blocks) {
-        const ViscArgs v = args(b);
-        CK(launch_grad(v, st));
-        CK(launch_grad_ghosts(v, st));
-    }
+    for (Block &b : c->blocks) CK(launch_grad(args(b), st));  // (writes the physical ghost gradients too)
     for (Block &b : c->blocks) {
         const size_t rowd = (size_t)6 * b.PG;  // one i-row of the gradient frame
         if (b.nbr[1] >= 0) {  // E neighbour e: b row ni-1 -> e row -1; e row 0 -> b row ni

@@ -43,7 +43,7 @@ struct Params {
     double cfl, dt_fixed;
     int limiter;
     // Navier-Stokes (readings N-R1..N-R6)
-    double mu, kcond, rgas;  // viscosity, conductivity mu c_p / Pr, gas constant
+    double mu, kcond, rgas, rgas_inv;  // viscosity, conductivity mu c_p / Pr, gas constant
 };
 
 struct StageArgs {
@@ -141,7 +141,6 @@ struct ViscArgs {
     Params P;
 };
 cudaError_t launch_grad(const ViscArgs &v, cudaStream_t st);
-cudaError_t launch_grad_ghosts(const ViscArgs &v, cudaStream_t st);
 cudaError_t launch_visc(const ViscArgs &v, cudaStream_t st);
 cudaError_t launch_norms(const NormsArgs &f, cudaStream_t st);
 cudaError_t stage_occupancy(int mode, bool norms, bool dtmax, bool fast, bool peer, int *ctas_per_sm);

@@ -1034,19 +1034,19 @@ cudaError_t launch_metrics(const MetricsArgs &a, cudaStream_t st) {
 }
 
 // ------------------------------------------------------------ Navier-Stokes
-// Per stage: Green-Gauss gradients of (u, v, T) (reading N-R2), ghost
-// gradients of physical edges (N-R1; connected edges are exchanged by the
-// host), then the viscous residual sum_f F_v . n A per cell (Eq. 2 viscous
+// Per stage: Green-Gauss gradients of (u, v, T) (reading N-R2) with the
+// ghost gradients of physical edges (N-R1; connected edges are exchanged by
+// the host), then the viscous residual sum_f F_v . n A per cell (Eq. 2 viscous
 // flux, N-R3/N-R5), which the stage kernel subtracts from the inviscid one.
 // Straightforward one-thread-per-cell kernels: correctness first.
 __device__ __forceinline__ void uvT(const double *buf, int PJ, int i, int j, const Params &P, double o[3]) {
     const double *q = buf + (size_t)((i + 2) * 4) * PJ + (j + JOFF);
-    const double r = q[0], ir = 1.0 / r;
+    const double ir = frcp(q[0]);
     const double u = q[PJ] * ir, v = q[2 * (size_t)PJ] * ir;
     const double p = P.gm1 * (q[3 * (size_t)PJ] - 0.5 * (q[PJ] * u + q[2 * (size_t)PJ] * v));
     o[0] = u;
     o[1] = v;
-    o[2] = p * ir / P.rgas;
+    o[2] = p * ir * P.rgas_inv;
 }
 __device__ __forceinline__ double metf(const double *met, int PJ, int row, int f, int j) {
     return met[(size_t)(row * NMET + f) * PJ + j + JOFF];
@@ -1073,35 +1073,29 @@ __global__ void grad_kernel(const ViscArgs a) {
     const double nx = metf(a.met, a.PJ, i + 1, 3, j + 1), ny = metf(a.met, a.PJ, i + 1, 4, j + 1),
                  nA = metf(a.met, a.PJ, i + 1, 5, j + 1);
     const double iV = metf(a.met, a.PJ, i + 1, 6, j);
+    // physical-edge ghost cells take this cell's gradient (reading N-R1)
+    const bool gw = i == 0 && a.bc[0] != E_CONNECTED, ge = i == a.ni - 1 && a.bc[1] != E_CONNECTED;
+    const bool gs = j == 0 && a.bc[2] != E_CONNECTED, gn = j == a.nj - 1 && a.bc[3] != E_CONNECTED;
 #pragma unroll
     for (int q = 0; q < 3; ++q) {
         const double fE = 0.5 * (c[q] + e[q]) * eA, fW = 0.5 * (w[q] + c[q]) * wA;
         const double fN = 0.5 * (c[q] + n[q]) * nA, fS = 0.5 * (s[q] + c[q]) * sA;
-        *gradp(a.grad, a.PG, i, j, 2 * q) = (((fE * ex - fW * wx) + fN * nx) - fS * sx) * iV;
-        *gradp(a.grad, a.PG, i, j, 2 * q + 1) = (((fE * ey - fW * wy) + fN * ny) - fS * sy) * iV;
+        const double gx = (((fE * ex - fW * wx) + fN * nx) - fS * sx) * iV;
+        const double gy = (((fE * ey - fW * wy) + fN * ny) - fS * sy) * iV;
+        *gradp(a.grad, a.PG, i, j, 2 * q) = gx;
+        *gradp(a.grad, a.PG, i, j, 2 * q + 1) = gy;
+        if (gw) { *gradp(a.grad, a.PG, -1, j, 2 * q) = gx; *gradp(a.grad, a.PG, -1, j, 2 * q + 1) = gy; }
+        if (ge) { *gradp(a.grad, a.PG, a.ni, j, 2 * q) = gx; *gradp(a.grad, a.PG, a.ni, j, 2 * q + 1) = gy; }
+        if (gs) { *gradp(a.grad, a.PG, i, -1, 2 * q) = gx; *gradp(a.grad, a.PG, i, -1, 2 * q + 1) = gy; }
+        if (gn) { *gradp(a.grad, a.PG, i, a.nj, 2 * q) = gx; *gradp(a.grad, a.PG, i, a.nj, 2 * q + 1) = gy; }
     }
 }
 
-__global__ void grad_ghost_kernel(const ViscArgs a) {
-    const int k = blockIdx.x * blockDim.x + threadIdx.x;
-    for (int q = 0; q < 6; ++q) {
-        if (k < a.nj) {
-            if (a.bc[0] != E_CONNECTED) *gradp(a.grad, a.PG, -1, k, q) = *gradp(a.grad, a.PG, 0, k, q);
-            if (a.bc[1] != E_CONNECTED) *gradp(a.grad, a.PG, a.ni, k, q) = *gradp(a.grad, a.PG, a.ni - 1, k, q);
-        }
-        if (k < a.ni) {
-            if (a.bc[2] != E_CONNECTED) *gradp(a.grad, a.PG, k, -1, q) = *gradp(a.grad, a.PG, k, 0, q);
-            if (a.bc[3] != E_CONNECTED) *gradp(a.grad, a.PG, k, a.nj, q) = *gradp(a.grad, a.PG, k, a.nj - 1, q);
-        }
-    }
-}
-
-// F_v . n A of the face between cells L and R (the lower-index cell is L)
-__device__ __forceinline__ void face_visc(const ViscArgs &a, int iL, int jL, int iR, int jR, double nx, double ny,
-                                          double A, double F[4]) {
-    double pl[3], pr[3], g[6];
-    uvT(a.in, a.PJ, iL, jL, a.P, pl);
-    uvT(a.in, a.PJ, iR, jR, a.P, pr);
+// F_v . n A of the face between cells L and R (the lower-index cell is L):
+// mean gradients and (u, v) of the two cells (reading N-R3)
+__device__ __forceinline__ void face_visc(const ViscArgs &a, int iL, int jL, int iR, int jR, const double pl[3],
+                                          const double pr[3], double nx, double ny, double A, double F[4]) {
+    double g[6];
 #pragma unroll
     for (int q = 0; q < 6; ++q) g[q] = 0.5 * (*gradp(a.grad, a.PG, iL, jL, q) + *gradp(a.grad, a.PG, iR, jR, q));
     const double u = 0.5 * (pl[0] + pr[0]), v = 0.5 * (pl[1] + pr[1]);
@@ -1117,27 +1111,28 @@ __device__ __forceinline__ void face_visc(const ViscArgs &a, int iL, int jL, int
 __global__ void visc_kernel(const ViscArgs a) {
     const int j = blockIdx.x * blockDim.x + threadIdx.x, i = blockIdx.y;
     if (j >= a.nj) return;
+    double c[3], w[3], e[3], s[3], n[3];
+    uvT(a.in, a.PJ, i, j, a.P, c);
+    uvT(a.in, a.PJ, i - 1, j, a.P, w);
+    uvT(a.in, a.PJ, i + 1, j, a.P, e);
+    uvT(a.in, a.PJ, i, j - 1, a.P, s);
+    uvT(a.in, a.PJ, i, j + 1, a.P, n);
     double FW[4], FE[4], FS[4], FN[4];
-    face_visc(a, i - 1, j, i, j, metf(a.met, a.PJ, i, 0, j), metf(a.met, a.PJ, i, 1, j), metf(a.met, a.PJ, i, 2, j),
-              FW);
-    face_visc(a, i, j, i + 1, j, metf(a.met, a.PJ, i + 1, 0, j), metf(a.met, a.PJ, i + 1, 1, j),
+    face_visc(a, i - 1, j, i, j, w, c, metf(a.met, a.PJ, i, 0, j), metf(a.met, a.PJ, i, 1, j),
+              metf(a.met, a.PJ, i, 2, j), FW);
+    face_visc(a, i, j, i + 1, j, c, e, metf(a.met, a.PJ, i + 1, 0, j), metf(a.met, a.PJ, i + 1, 1, j),
               metf(a.met, a.PJ, i + 1, 2, j), FE);
-    face_visc(a, i, j - 1, i, j, metf(a.met, a.PJ, i + 1, 3, j), metf(a.met, a.PJ, i + 1, 4, j),
+    face_visc(a, i, j - 1, i, j, s, c, metf(a.met, a.PJ, i + 1, 3, j), metf(a.met, a.PJ, i + 1, 4, j),
               metf(a.met, a.PJ, i + 1, 5, j), FS);
-    face_visc(a, i, j, i, j + 1, metf(a.met, a.PJ, i + 1, 3, j + 1), metf(a.met, a.PJ, i + 1, 4, j + 1),
+    face_visc(a, i, j, i, j + 1, c, n, metf(a.met, a.PJ, i + 1, 3, j + 1), metf(a.met, a.PJ, i + 1, 4, j + 1),
               metf(a.met, a.PJ, i + 1, 5, j + 1), FN);
     double *o = a.rv + (size_t)((i + 2) * 4) * a.PJ + (j + JOFF);
 #pragma unroll
-    for (int c = 0; c < 4; ++c) o[(size_t)c * a.PJ] = ((FE[c] - FW[c]) + FN[c]) - FS[c];
+    for (int c2 = 0; c2 < 4; ++c2) o[(size_t)c2 * a.PJ] = ((FE[c2] - FW[c2]) + FN[c2]) - FS[c2];
 }
 
 cudaError_t launch_grad(const ViscArgs &v, cudaStream_t st) {
     grad_kernel<<<dim3((v.nj + 127) / 128, v.ni), 128, 0, st>>>(v);
-    return cudaGetLastError();
-}
-cudaError_t launch_grad_ghosts(const ViscArgs &v, cudaStream_t st) {
-    const int n = v.ni > v.nj ? v.ni : v.nj;
-    grad_ghost_kernel<<<(n + 127) / 128, 128, 0, st>>>(v);
     return cudaGetLastError();
 }
 cudaError_t launch_visc(const ViscArgs &v, cudaStream_t st) {
