@@ -614,7 +614,15 @@ sfv_status enqueue_viscous(sfv_ctx *c, int in, cudaStream_t st) {
         v.P = c->P;
         return v;
     };
-    for (Block &b : c->blocks) CK(launch_grad(args(b), st));  // (writes the physical ghost gradients too)
+    const char *fv = getenv("SFV_NS_FUSED");
+    const bool fuse_ok = !(fv && fv[0] == '0');
+    bool all_fused = true;
+    for (Block &b : c->blocks) {
+        const bool iso = b.nbr[0] < 0 && b.nbr[1] < 0 && b.nbr[2] < 0 && b.nbr[3] < 0;
+        if (iso && fuse_ok) CK(launch_gradvisc(args(b), st));  // gradients never leave shared memory
+        else { CK(launch_grad(args(b), st)); all_fused = false; }  // (writes the physical ghost gradients too)
+    }
+    if (all_fused) return SFV_OK;
     for (Block &b : c->blocks) {
         const size_t rowd = (size_t)6 * b.PG;  // one i-row of the gradient frame
         if (b.nbr[1] >= 0) {  // E neighbour e: b row ni-1 -> e row -1; e row 0 -> b row ni
@@ -631,7 +639,10 @@ sfv_status enqueue_viscous(sfv_ctx *c, int in, cudaStream_t st) {
                                  (size_t)n.PG * 8, 8, (size_t)n.ni * 6, cudaMemcpyDeviceToDevice, st));
         }
     }
-    for (Block &b : c->blocks) CK(launch_visc(args(b), st));
+    for (Block &b : c->blocks) {
+        const bool iso = b.nbr[0] < 0 && b.nbr[1] < 0 && b.nbr[2] < 0 && b.nbr[3] < 0;
+        if (!(iso && fuse_ok)) CK(launch_visc(args(b), st));
+    }
     return SFV_OK;
 }
 

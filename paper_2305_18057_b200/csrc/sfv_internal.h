@@ -142,6 +142,7 @@ struct ViscArgs {
 };
 cudaError_t launch_grad(const ViscArgs &v, cudaStream_t st);
 cudaError_t launch_visc(const ViscArgs &v, cudaStream_t st);
+cudaError_t launch_gradvisc(const ViscArgs &v, cudaStream_t st);  // blocks without connected edges
 cudaError_t launch_norms(const NormsArgs &f, cudaStream_t st);
 cudaError_t stage_occupancy(int mode, bool norms, bool dtmax, bool fast, bool peer, int *ctas_per_sm);
 bool fast_path(const Params &P);

@@ -1039,14 +1039,26 @@ cudaError_t launch_metrics(const MetricsArgs &a, cudaStream_t st) {
 // the host), then the viscous residual sum_f F_v . n A per cell (Eq. 2 viscous
 // flux, N-R3/N-R5), which the stage kernel subtracts from the inviscid one.
 // Straightforward one-thread-per-cell kernels: correctness first.
-__device__ __forceinline__ void uvT(const double *buf, int PJ, int i, int j, const Params &P, double o[3]) {
-    const double *q = buf + (size_t)((i + 2) * 4) * PJ + (j + JOFF);
-    const double ir = frcp(q[0]);
-    const double u = q[PJ] * ir, v = q[2 * (size_t)PJ] * ir;
-    const double p = P.gm1 * (q[3 * (size_t)PJ] - 0.5 * (q[PJ] * u + q[2 * (size_t)PJ] * v));
+// The arithmetic of one cell's (u, v, T), one cell's gradient and one face's
+// viscous flux is shared by the two-kernel path and the fused tile kernel and
+// written with round-to-nearest intrinsics (no FMA contraction left to the
+// compiler), so both paths give bitwise the same numbers wherever they are
+// inlined (the loopback decomposition tests compare a fused single block with
+// exchanged-gradient blocks bitwise).
+#define DM __dmul_rn
+#define DA __dadd_rn
+#define DS __dsub_rn
+__device__ __forceinline__ void uvT_core(double r, double mx, double my, double E, const Params &P, double o[3]) {
+    const double ir = frcp(r);
+    const double u = DM(mx, ir), v = DM(my, ir);
+    const double p = DM(P.gm1, DS(E, DM(0.5, DA(DM(mx, u), DM(my, v)))));
     o[0] = u;
     o[1] = v;
-    o[2] = p * ir * P.rgas_inv;
+    o[2] = DM(DM(p, ir), P.rgas_inv);
+}
+__device__ __forceinline__ void uvT(const double *buf, int PJ, int i, int j, const Params &P, double o[3]) {
+    const double *q = buf + (size_t)((i + 2) * 4) * PJ + (j + JOFF);
+    uvT_core(q[0], q[PJ], q[2 * (size_t)PJ], q[3 * (size_t)PJ], P, o);
 }
 __device__ __forceinline__ double metf(const double *met, int PJ, int row, int f, int j) {
     return met[(size_t)(row * NMET + f) * PJ + j + JOFF];
@@ -1055,57 +1067,84 @@ __device__ __forceinline__ double *gradp(double *grad, int PG, int i, int j, int
     return grad + (size_t)((i + 1) * 6 + q) * PG + (j + 1);
 }
 
+// Green-Gauss gradient (reading N-R2) of cell (i, j) from the (u, v, T) of
+// the cell and its 4 face neighbours; faces: the mean of the two cells times A
+__device__ __forceinline__ void gg_cell(const double *met, int PJ, int i, int j, const double c[3], const double w[3],
+                                     const double e[3], const double s[3], const double n[3], double g[6]) {
+    const double wx = metf(met, PJ, i, 0, j), wy = metf(met, PJ, i, 1, j), wA = metf(met, PJ, i, 2, j);
+    const double ex = metf(met, PJ, i + 1, 0, j), ey = metf(met, PJ, i + 1, 1, j), eA = metf(met, PJ, i + 1, 2, j);
+    const double sx = metf(met, PJ, i + 1, 3, j), sy = metf(met, PJ, i + 1, 4, j), sA = metf(met, PJ, i + 1, 5, j);
+    const double nx = metf(met, PJ, i + 1, 3, j + 1), ny = metf(met, PJ, i + 1, 4, j + 1),
+                 nA = metf(met, PJ, i + 1, 5, j + 1);
+    const double iV = metf(met, PJ, i + 1, 6, j);
+#pragma unroll
+    for (int q = 0; q < 3; ++q) {
+        const double fE = DM(DM(0.5, DA(c[q], e[q])), eA), fW = DM(DM(0.5, DA(w[q], c[q])), wA);
+        const double fN = DM(DM(0.5, DA(c[q], n[q])), nA), fS = DM(DM(0.5, DA(s[q], c[q])), sA);
+        g[2 * q] = DM(DS(DA(DS(DM(fE, ex), DM(fW, wx)), DM(fN, nx)), DM(fS, sx)), iV);
+        g[2 * q + 1] = DM(DS(DA(DS(DM(fE, ey), DM(fW, wy)), DM(fN, ny)), DM(fS, sy)), iV);
+    }
+}
+
 __global__ void grad_kernel(const ViscArgs a) {
     const int j = blockIdx.x * blockDim.x + threadIdx.x, i = blockIdx.y;
     if (j >= a.nj) return;
-    double c[3], w[3], e[3], s[3], n[3];
+    double c[3], w[3], e[3], s[3], n[3], g[6];
     uvT(a.in, a.PJ, i, j, a.P, c);
     uvT(a.in, a.PJ, i - 1, j, a.P, w);
     uvT(a.in, a.PJ, i + 1, j, a.P, e);
     uvT(a.in, a.PJ, i, j - 1, a.P, s);
     uvT(a.in, a.PJ, i, j + 1, a.P, n);
-    // faces: the mean of the two cells times A
-    const double wx = metf(a.met, a.PJ, i, 0, j), wy = metf(a.met, a.PJ, i, 1, j), wA = metf(a.met, a.PJ, i, 2, j);
-    const double ex = metf(a.met, a.PJ, i + 1, 0, j), ey = metf(a.met, a.PJ, i + 1, 1, j),
-                 eA = metf(a.met, a.PJ, i + 1, 2, j);
-    const double sx = metf(a.met, a.PJ, i + 1, 3, j), sy = metf(a.met, a.PJ, i + 1, 4, j),
-                 sA = metf(a.met, a.PJ, i + 1, 5, j);
-    const double nx = metf(a.met, a.PJ, i + 1, 3, j + 1), ny = metf(a.met, a.PJ, i + 1, 4, j + 1),
-                 nA = metf(a.met, a.PJ, i + 1, 5, j + 1);
-    const double iV = metf(a.met, a.PJ, i + 1, 6, j);
+    gg_cell(a.met, a.PJ, i, j, c, w, e, s, n, g);
     // physical-edge ghost cells take this cell's gradient (reading N-R1)
     const bool gw = i == 0 && a.bc[0] != E_CONNECTED, ge = i == a.ni - 1 && a.bc[1] != E_CONNECTED;
     const bool gs = j == 0 && a.bc[2] != E_CONNECTED, gn = j == a.nj - 1 && a.bc[3] != E_CONNECTED;
 #pragma unroll
-    for (int q = 0; q < 3; ++q) {
-        const double fE = 0.5 * (c[q] + e[q]) * eA, fW = 0.5 * (w[q] + c[q]) * wA;
-        const double fN = 0.5 * (c[q] + n[q]) * nA, fS = 0.5 * (s[q] + c[q]) * sA;
-        const double gx = (((fE * ex - fW * wx) + fN * nx) - fS * sx) * iV;
-        const double gy = (((fE * ey - fW * wy) + fN * ny) - fS * sy) * iV;
-        *gradp(a.grad, a.PG, i, j, 2 * q) = gx;
-        *gradp(a.grad, a.PG, i, j, 2 * q + 1) = gy;
-        if (gw) { *gradp(a.grad, a.PG, -1, j, 2 * q) = gx; *gradp(a.grad, a.PG, -1, j, 2 * q + 1) = gy; }
-        if (ge) { *gradp(a.grad, a.PG, a.ni, j, 2 * q) = gx; *gradp(a.grad, a.PG, a.ni, j, 2 * q + 1) = gy; }
-        if (gs) { *gradp(a.grad, a.PG, i, -1, 2 * q) = gx; *gradp(a.grad, a.PG, i, -1, 2 * q + 1) = gy; }
-        if (gn) { *gradp(a.grad, a.PG, i, a.nj, 2 * q) = gx; *gradp(a.grad, a.PG, i, a.nj, 2 * q + 1) = gy; }
+    for (int q = 0; q < 6; ++q) {
+        *gradp(a.grad, a.PG, i, j, q) = g[q];
+        if (gw) *gradp(a.grad, a.PG, -1, j, q) = g[q];
+        if (ge) *gradp(a.grad, a.PG, a.ni, j, q) = g[q];
+        if (gs) *gradp(a.grad, a.PG, i, -1, q) = g[q];
+        if (gn) *gradp(a.grad, a.PG, i, a.nj, q) = g[q];
     }
 }
 
 // F_v . n A of the face between cells L and R (the lower-index cell is L):
 // mean gradients and (u, v) of the two cells (reading N-R3)
-__device__ __forceinline__ void face_visc(const ViscArgs &a, int iL, int jL, int iR, int jR, const double pl[3],
-                                          const double pr[3], double nx, double ny, double A, double F[4]) {
+__device__ __forceinline__ void face_visc_core(const double gl[6], const double gr[6], const double pl[3],
+                                               const double pr[3], double nx, double ny, double A, const Params &P,
+                                               double F[4]) {
     double g[6];
 #pragma unroll
-    for (int q = 0; q < 6; ++q) g[q] = 0.5 * (*gradp(a.grad, a.PG, iL, jL, q) + *gradp(a.grad, a.PG, iR, jR, q));
-    const double u = 0.5 * (pl[0] + pr[0]), v = 0.5 * (pl[1] + pr[1]);
-    const double mu = a.P.mu, lam = -2.0 * mu / 3.0, div = g[0] + g[3];
-    const double txx = 2.0 * mu * g[0] + lam * div, tyy = 2.0 * mu * g[3] + lam * div, txy = mu * (g[1] + g[2]);
-    const double thx = u * txx + v * txy + a.P.kcond * g[4], thy = u * txy + v * tyy + a.P.kcond * g[5];
+    for (int q = 0; q < 6; ++q) g[q] = DM(0.5, DA(gl[q], gr[q]));
+    const double u = DM(0.5, DA(pl[0], pr[0])), v = DM(0.5, DA(pl[1], pr[1]));
+    const double mu = P.mu, lam = -2.0 * mu / 3.0, div = DA(g[0], g[3]);
+    const double txx = DA(DM(DM(2.0, mu), g[0]), DM(lam, div)), tyy = DA(DM(DM(2.0, mu), g[3]), DM(lam, div));
+    const double txy = DM(mu, DA(g[1], g[2]));
+    const double thx = DA(DA(DM(u, txx), DM(v, txy)), DM(P.kcond, g[4]));
+    const double thy = DA(DA(DM(u, txy), DM(v, tyy)), DM(P.kcond, g[5]));
     F[0] = 0.0;
-    F[1] = (txx * nx + txy * ny) * A;
-    F[2] = (txy * nx + tyy * ny) * A;
-    F[3] = (thx * nx + thy * ny) * A;
+    F[1] = DM(DA(DM(txx, nx), DM(txy, ny)), A);
+    F[2] = DM(DA(DM(txy, nx), DM(tyy, ny)), A);
+    F[3] = DM(DA(DM(thx, nx), DM(thy, ny)), A);
+}
+__device__ __forceinline__ void face_visc(const ViscArgs &a, int iL, int jL, int iR, int jR, const double pl[3],
+                                          const double pr[3], double nx, double ny, double A, double F[4]) {
+    double gl[6], gr[6];
+#pragma unroll
+    for (int q = 0; q < 6; ++q) {
+        gl[q] = *gradp(a.grad, a.PG, iL, jL, q);
+        gr[q] = *gradp(a.grad, a.PG, iR, jR, q);
+    }
+    face_visc_core(gl, gr, pl, pr, nx, ny, A, a.P, F);
+}
+
+// sum over the 4 faces, written to rv (state layout)
+__device__ __forceinline__ void store_rv(const ViscArgs &a, int i, int j, const double FW[4], const double FE[4],
+                                         const double FS[4], const double FN[4]) {
+    double *o = a.rv + (size_t)((i + 2) * 4) * a.PJ + (j + JOFF);
+#pragma unroll
+    for (int c = 0; c < 4; ++c) o[(size_t)c * a.PJ] = DS(DA(DS(FE[c], FW[c]), FN[c]), FS[c]);
 }
 
 __global__ void visc_kernel(const ViscArgs a) {
@@ -1126,9 +1165,72 @@ __global__ void visc_kernel(const ViscArgs a) {
               metf(a.met, a.PJ, i + 1, 5, j), FS);
     face_visc(a, i, j, i, j + 1, c, n, metf(a.met, a.PJ, i + 1, 3, j + 1), metf(a.met, a.PJ, i + 1, 4, j + 1),
               metf(a.met, a.PJ, i + 1, 5, j + 1), FN);
-    double *o = a.rv + (size_t)((i + 2) * 4) * a.PJ + (j + JOFF);
-#pragma unroll
-    for (int c2 = 0; c2 < 4; ++c2) o[(size_t)c2 * a.PJ] = ((FE[c2] - FW[c2]) + FN[c2]) - FS[c2];
+    store_rv(a, i, j, FW, FE, FS, FN);
+}
+
+// Fused gradient + viscous residual for a block without connected edges
+// (every ghost gradient is a copy of the adjacent interior cell's, N-R1): a
+// CTA takes a VT_I x VT_J tile, stages the (u, v, T) of the tile + 2 rings
+// and the gradients of the tile + 1 ring in shared memory, so gradients are
+// computed once and never go through global memory.
+constexpr int VT_J = 32, VT_I = 8;
+constexpr int VP_J = VT_J + 4, VP_I = VT_I + 4;  // (u, v, T) region
+constexpr int VG_J = VT_J + 2, VG_I = VT_I + 2;  // gradient region
+
+__global__ void __launch_bounds__(VT_J * VT_I) gradvisc_kernel(const ViscArgs a) {
+    __shared__ double pr[VP_I][VP_J][3];
+    __shared__ double gs[VG_I][VG_J][6];
+    const int i0 = blockIdx.y * VT_I, j0 = blockIdx.x * VT_J;
+    const int tid = threadIdx.y * VT_J + threadIdx.x;
+    // (u, v, T) of cells i0-2 .. i0+VT_I+1, j0-2 .. j0+VT_J+1 inside the ghost frame
+    for (int k = tid; k < VP_I * VP_J; k += VT_J * VT_I) {
+        const int ti = k / VP_J, tj = k % VP_J, i = i0 - 2 + ti, j = j0 - 2 + tj;
+        const bool iin = i >= 0 && i < a.ni, jin = j >= 0 && j < a.nj;
+        if (i >= -2 && i < a.ni + 2 && j >= -2 && j < a.nj + 2 && (iin || jin))  // (no corners)
+            uvT(a.in, a.PJ, i, j, a.P, pr[ti][tj]);
+    }
+    __syncthreads();
+    // gradients of interior cells i0-1 .. i0+VT_I, j0-1 .. j0+VT_J
+    for (int k = tid; k < VG_I * VG_J; k += VT_J * VT_I) {
+        const int ti = k / VG_J, tj = k % VG_J, i = i0 - 1 + ti, j = j0 - 1 + tj;
+        if (i >= 0 && i < a.ni && j >= 0 && j < a.nj)
+            gg_cell(a.met, a.PJ, i, j, pr[ti + 1][tj + 1], pr[ti][tj + 1], pr[ti + 2][tj + 1], pr[ti + 1][tj],
+                    pr[ti + 1][tj + 2], gs[ti][tj]);
+    }
+    __syncthreads();
+    // physical ghost ring inside the gradient region: the adjacent interior cell's
+    for (int k = tid; k < VG_I * VG_J; k += VT_J * VT_I) {
+        const int ti = k / VG_J, tj = k % VG_J, i = i0 - 1 + ti, j = j0 - 1 + tj;
+        const bool iin = i >= 0 && i < a.ni, jin = j >= 0 && j < a.nj;
+        if (iin == jin) continue;  // interior (done) or corner (never used)
+        if (!iin && (i == -1 || i == a.ni) && jin) {
+            const int si = i < 0 ? ti + 1 : ti - 1;
+            for (int q = 0; q < 6; ++q) gs[ti][tj][q] = gs[si][tj][q];
+        } else if (!jin && (j == -1 || j == a.nj) && iin) {
+            const int sj = j < 0 ? tj + 1 : tj - 1;
+            for (int q = 0; q < 6; ++q) gs[ti][tj][q] = gs[ti][sj][q];
+        }
+    }
+    __syncthreads();
+    const int i = i0 + threadIdx.y, j = j0 + threadIdx.x;
+    if (i >= a.ni || j >= a.nj) return;
+    const int ti = threadIdx.y + 1, tj = threadIdx.x + 1;  // gradient-region index
+    const double *c = pr[ti + 1][tj + 1];
+    double FW[4], FE[4], FS[4], FN[4];
+    face_visc_core(gs[ti - 1][tj], gs[ti][tj], pr[ti][tj + 1], c, metf(a.met, a.PJ, i, 0, j),
+                   metf(a.met, a.PJ, i, 1, j), metf(a.met, a.PJ, i, 2, j), a.P, FW);
+    face_visc_core(gs[ti][tj], gs[ti + 1][tj], c, pr[ti + 2][tj + 1], metf(a.met, a.PJ, i + 1, 0, j),
+                   metf(a.met, a.PJ, i + 1, 1, j), metf(a.met, a.PJ, i + 1, 2, j), a.P, FE);
+    face_visc_core(gs[ti][tj - 1], gs[ti][tj], pr[ti + 1][tj], c, metf(a.met, a.PJ, i + 1, 3, j),
+                   metf(a.met, a.PJ, i + 1, 4, j), metf(a.met, a.PJ, i + 1, 5, j), a.P, FS);
+    face_visc_core(gs[ti][tj], gs[ti][tj + 1], c, pr[ti + 1][tj + 2], metf(a.met, a.PJ, i + 1, 3, j + 1),
+                   metf(a.met, a.PJ, i + 1, 4, j + 1), metf(a.met, a.PJ, i + 1, 5, j + 1), a.P, FN);
+    store_rv(a, i, j, FW, FE, FS, FN);
+}
+
+cudaError_t launch_gradvisc(const ViscArgs &v, cudaStream_t st) {
+    gradvisc_kernel<<<dim3((v.nj + VT_J - 1) / VT_J, (v.ni + VT_I - 1) / VT_I), dim3(VT_J, VT_I), 0, st>>>(v);
+    return cudaGetLastError();
 }
 
 cudaError_t launch_grad(const ViscArgs &v, cudaStream_t st) {

@@ -84,11 +84,16 @@ def test_ns_operator_matches_oracle(sfv_mod, oracle_mod):
     a stage input (Heun stage 2 input W2, read back through
     sfv_debug_block_buffer) equal the oracle's on the same state:
     gradients to 1e-13, R_v to 1e-11 of its maximum."""
+    import os
     ni, nj = 64, 32
     X, Y = I.ramp_nodes(ni, nj, 15.0)
     cfg = I.default_config(ni, nj, viscous=1, mu=0.05, rk=I.RK2_HEUN, dt_fixed=1e-6, bc=NOSLIP_S)
     g = sfv_mod.Solver(cfg, X, Y)
-    g.set_state(I.perturbed_state(ni, nj, 21)); g.step(1); g.sync()
+    os.environ["SFV_NS_FUSED"] = "0"  # two-kernel path: the gradients go through global memory (readable)
+    try:
+        g.set_state(I.perturbed_state(ni, nj, 21)); g.step(1); g.sync()
+    finally:
+        del os.environ["SFV_NS_FUSED"]
     W2 = np.transpose(g.block_buffer(0, 1)[2:-2, :, 2:-2], (2, 0, 1)).copy()
     rv = np.transpose(g.block_buffer(0, -1)[2:-2, :, 2:-2], (2, 0, 1))
     G = np.transpose(g.block_buffer(0, -2)[1:-1, :, 1:-1], (2, 0, 1))
@@ -97,3 +102,22 @@ def test_ns_operator_matches_oracle(sfv_mod, oracle_mod):
     Go = o.gradients(W2)
     assert np.max(np.abs(G - Go)) <= 1e-13 * np.max(np.abs(Go))
     assert np.max(np.abs(rv - Rv)) <= 1e-11 * np.max(np.abs(Rv))
+
+
+def test_ns_fused_equals_two_kernel_path(sfv_mod):
+    """The fused tile kernel (blocks without connected edges) and the
+    gradient + viscous kernel pair give bitwise the same evolution."""
+    import os
+    ni, nj = 70, 45
+    X, Y = I.ramp_nodes(ni, nj, 5.0)
+    cfg = I.default_config(ni, nj, viscous=1, mu=0.1, bc=NOSLIP_S)
+    U0 = I.perturbed_state(ni, nj, 17)
+    out = []
+    for fused in ("1", "0"):
+        os.environ["SFV_NS_FUSED"] = fused
+        try:
+            g = sfv_mod.Solver(cfg, X, Y); g.set_state(U0); g.step(15); g.sync()
+        finally:
+            del os.environ["SFV_NS_FUSED"]
+        out.append(g.get_state())
+    np.testing.assert_array_equal(out[0], out[1])
