@@ -95,7 +95,7 @@ typedef struct {
     int64_t max_history;         /* capacity (steps) of the dt / norm history, >= 1 */
     /* Navier-Stokes (Eq. 2 viscous flux; readings N-R1..N-R6):
      * R_h = sum_f (F - F_v) ds with Green-Gauss gradients of (u, v, T).
-     * Single-rank only (any px x py loopback blocks, SFV_HALO_COPY). */
+     * Halo mode SFV_HALO_COPY (loopback blocks or NCCL ranks). */
     int32_t viscous;             /* 0 = Euler, 1 = Navier-Stokes */
     double mu;                   /* constant dynamic viscosity, >= 0            reading N-R5 */
     double prandtl;              /* Prandtl number, > 0 (0.72)                   reading N-R5 */

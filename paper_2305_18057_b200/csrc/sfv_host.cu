@@ -623,6 +623,38 @@ sfv_status enqueue_viscous(sfv_ctx *c, int in, cudaStream_t st) {
         else { CK(launch_grad(args(b), st)); all_fused = false; }  // (writes the physical ghost gradients too)
     }
     if (all_fused) return SFV_OK;
+    if (c->nranks > 1) {
+        // NCCL: this rank's block; rows (i-cuts) straight from / into the frame,
+        // columns (j-cuts) through the pack buffers
+        Block &b = c->blocks[0];
+        Nccl &N = nccl();
+        const size_t rowd = (size_t)6 * b.PG;
+        for (int sd = 0; sd < 2; ++sd)
+            if (b.nbr[2 + sd] >= 0)
+                CK(cudaMemcpy2DAsync(b.xs[sd], 8, b.grad + (size_t)6 * b.PG + (sd == 0 ? 1 : b.nj), (size_t)b.PG * 8,
+                                     8, (size_t)b.ni * 6, cudaMemcpyDeviceToDevice, st));
+        NK(N.GroupStart());
+        if (b.nbr[0] >= 0) {
+            NK(N.Send(b.grad + rowd, rowd, ncclDouble, b.nbr[0], c->comm, st));
+            NK(N.Recv(b.grad, rowd, ncclDouble, b.nbr[0], c->comm, st));
+        }
+        if (b.nbr[1] >= 0) {
+            NK(N.Send(b.grad + (size_t)b.ni * rowd, rowd, ncclDouble, b.nbr[1], c->comm, st));
+            NK(N.Recv(b.grad + (size_t)(b.ni + 1) * rowd, rowd, ncclDouble, b.nbr[1], c->comm, st));
+        }
+        for (int sd = 0; sd < 2; ++sd)
+            if (b.nbr[2 + sd] >= 0) {
+                NK(N.Send(b.xs[sd], (size_t)6 * b.ni, ncclDouble, b.nbr[2 + sd], c->comm, st));
+                NK(N.Recv(b.xr[sd], (size_t)6 * b.ni, ncclDouble, b.nbr[2 + sd], c->comm, st));
+            }
+        NK(N.GroupEnd());
+        for (int sd = 0; sd < 2; ++sd)
+            if (b.nbr[2 + sd] >= 0)
+                CK(cudaMemcpy2DAsync(b.grad + (size_t)6 * b.PG + (sd == 0 ? 0 : b.nj + 1), (size_t)b.PG * 8, b.xr[sd],
+                                     8, 8, (size_t)b.ni * 6, cudaMemcpyDeviceToDevice, st));
+        CK(launch_visc(args(b), st));
+        return SFV_OK;
+    }
     for (Block &b : c->blocks) {
         const size_t rowd = (size_t)6 * b.PG;  // one i-row of the gradient frame
         if (b.nbr[1] >= 0) {  // E neighbour e: b row ni-1 -> e row -1; e row 0 -> b row ni
@@ -838,8 +870,6 @@ sfv_status sfv_partition(sfv_ctx *c, int32_t px, int32_t py, const int32_t *wx, 
     if (px < 1 || py < 1 || nranks < 1 || rank < 0 || rank >= nranks)
         return fail(c, SFV_ERR_ARG, "bad px/py/rank/nranks");
     if (nranks > 1 && px * py != nranks) return fail(c, SFV_ERR_ARG, "px*py (%d) != nranks (%d)", px * py, nranks);
-    if (nranks > 1 && c->cfg.viscous)
-        return fail(c, SFV_ERR_UNSUPPORTED, "Navier-Stokes mode is single-rank (loopback blocks) in this build");
     std::vector<int> xs(px + 1), ys(py + 1);
     if (split_impl(c->cfg.ni, px, wx, xs.data()) != SFV_OK || split_impl(c->cfg.nj, py, wy, ys.data()) != SFV_OK)
         return fail(c, SFV_ERR_ARG, "partition: block width < 2 or weight <= 0");

@@ -32,7 +32,7 @@ def _free_port():
     return p
 
 
-def _worker(rank, world, port, px, py, ni, nj, steps, overlap, halo, rk, wx, out_q):
+def _worker(rank, world, port, px, py, ni, nj, steps, overlap, halo, rk, wx, visc, out_q):
     os.environ.update({"MASTER_ADDR": "127.0.0.1", "MASTER_PORT": str(port),
                        "NCCL_HOSTID": f"sfv-sim-host-{rank}", "NCCL_SOCKET_IFNAME": "lo",
                        "NCCL_IB_DISABLE": "1", "NCCL_NVLS_ENABLE": "0", "SFV_OVERLAP": str(overlap)})
@@ -44,8 +44,8 @@ def _worker(rank, world, port, px, py, ni, nj, steps, overlap, halo, rk, wx, out
     try:
         from paper_2305_18057_b200 import inputs as I
         from paper_2305_18057_b200 import sfv
-        X, Y = I.ramp_nodes(ni, nj, 30.0)
-        cfg = I.default_config(ni, nj, rk=rk)
+        X, Y = I.ramp_nodes(ni, nj, 5.0 if visc else 30.0)
+        cfg = I.default_config(ni, nj, rk=rk, **visc)
         obj = [sfv.nccl_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(obj, src=0)
         s = sfv.Solver(cfg, X, Y, px=px, py=py, wx=wx, rank=rank, nranks=world, nccl_id=obj[0], device=0)
@@ -65,12 +65,12 @@ def _worker(rank, world, port, px, py, ni, nj, steps, overlap, halo, rk, wx, out
         dist.destroy_process_group()
 
 
-def _run(world, px, py, ni, nj, steps, overlap, halo="copy", rk=0, wx=None):
+def _run(world, px, py, ni, nj, steps, overlap, halo="copy", rk=0, wx=None, visc=None):
     import torch.multiprocessing as mp
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    ps = [ctx.Process(target=_worker, args=(r, world, port, px, py, ni, nj, steps, overlap, halo, rk, wx, q))
+    ps = [ctx.Process(target=_worker, args=(r, world, port, px, py, ni, nj, steps, overlap, halo, rk, wx, visc or {}, q))
           for r in range(world)]
     for p in ps:
         p.start()
@@ -117,3 +117,26 @@ def test_nccl_ranks_match_loopback_and_oracle(oracle_mod, world, px, py, overlap
     assert np.all(state_error(U, o.get_state()) <= 1e-11)
     assert norm_error(res[0][3], o.residual_norms()) <= 1e-10
     assert dt_error(res[0][4], o.dt()) <= 1e-13
+
+
+@pytest.mark.parametrize("world,px,py", [(2, 2, 1), (2, 1, 2), (4, 2, 2)])
+def test_nccl_navier_stokes_ranks(oracle_mod, world, px, py):
+    """Navier-Stokes across NCCL ranks: ghost gradients travel by send/recv
+    (rows from the frame, columns packed); bitwise equal to loopback blocks
+    and within the parity gates of the oracle."""
+    from paper_2305_18057_b200 import inputs as I
+    from paper_2305_18057_b200 import sfv
+    from parity_util import state_error
+    ni, nj, steps = 96, 48, 30
+    visc = dict(viscous=1, mu=0.1, bc=(I.BC_INFLOW, I.BC_OUTFLOW, I.BC_NOSLIP_WALL, I.BC_SLIP_WALL))
+    res = _run(world, px, py, ni, nj, steps, 1, "copy", 0, None, visc)
+    U = res[0][2]
+    X, Y = I.ramp_nodes(ni, nj, 5.0)
+    cfg = I.default_config(ni, nj, **visc)
+    U0 = I.perturbed_state(ni, nj, 7)
+    g = sfv.Solver(cfg, X, Y, px=px, py=py)
+    g.set_state(U0); g.step(steps); g.sync()
+    np.testing.assert_array_equal(U, g.get_state())
+    o = oracle_mod.Oracle(cfg, X, Y)
+    o.set_state(U0); o.step(steps)
+    assert np.all(state_error(U, o.get_state()) <= 1e-11)
