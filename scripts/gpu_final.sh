@@ -9,6 +9,7 @@ timeout 600 python bench.py > gpurun_out/bench_${TAG}_c2.json 2> gpurun_out/benc
 timeout 400 python bench.py --workload C3 --steps 100 --warmup 5 --no-cpu-baseline > gpurun_out/bench_${TAG}_c3.json 2> gpurun_out/bench_${TAG}_c3.err
 timeout 400 python bench.py --workload C4 --steps 200 --warmup 5 --no-cpu-baseline > gpurun_out/bench_${TAG}_c4.json 2> gpurun_out/bench_${TAG}_c4.err
 timeout 400 python bench.py --impl reference --steps 20 --warmup 3 > gpurun_out/bench_${TAG}_ref.json 2> gpurun_out/bench_${TAG}_ref.err
+timeout 400 python bench.py --ns --steps 2000 --warmup 20 > gpurun_out/bench_${TAG}_ns.json 2> gpurun_out/bench_${TAG}_ns.err
 SFV_SIM_HOSTS=1 timeout 300 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29541 bench.py --gpus 2 --steps 100 --warmup 5 --no-e2e > gpurun_out/bench_${TAG}_sim2.json 2> gpurun_out/bench_${TAG}_sim2.err
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_$TAG.csv python bench.py --steps 40 --warmup 5 --no-cpu-baseline --no-e2e > gpurun_out/ncu_launch_$TAG.log 2>&1
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:stage_kernel -s 40 -c 4 -o gpurun_out/prof_$TAG python bench.py --steps 20 --warmup 10 --no-cpu-baseline --no-e2e > gpurun_out/ncu_$TAG.log 2>&1

@@ -5,16 +5,17 @@ cat > /tmp/san.py <<'PY'
 import sys, numpy as np
 sys.path.insert(0, '.')
 from paper_2305_18057_b200 import inputs as I, sfv
-for (ni, nj, px, py, rk, peer) in [(64, 32, 1, 1, 0, 0), (40, 36, 2, 2, 0, 0), (96, 48, 1, 1, 1, 0), (96, 48, 3, 1, 2, 0),
-                                   (40, 36, 2, 2, 0, 1), (96, 48, 3, 1, 2, 1), (64, 70, 1, 3, 1, 1)]:
-    X, Y = I.ramp_nodes(ni, nj, 30.0)
-    cfg = I.default_config(ni, nj, rk=rk)
+for (ni, nj, px, py, rk, peer, ns) in [(64, 32, 1, 1, 0, 0, 0), (40, 36, 2, 2, 0, 0, 0), (96, 48, 1, 1, 1, 0, 0),
+                                       (96, 48, 3, 1, 2, 0, 0), (40, 36, 2, 2, 0, 1, 0), (96, 48, 3, 1, 2, 1, 0),
+                                       (64, 70, 1, 3, 1, 1, 0), (70, 45, 1, 1, 0, 0, 1), (64, 40, 2, 2, 0, 0, 1)]:
+    X, Y = I.ramp_nodes(ni, nj, 5.0 if ns else 30.0)
+    cfg = I.default_config(ni, nj, rk=rk, **(dict(viscous=1, mu=0.1, bc=(0, 1, 3, 2)) if ns else {}))
     g = sfv.Solver(cfg, X, Y, px=px, py=py)
     if peer:
         g.enable_peer_halo()
     g.set_state(I.perturbed_state(ni, nj, 1)); g.step(3); g.sync()
     assert np.all(np.isfinite(g.get_state()))
-    print("ok", ni, nj, px, py, rk, "peer" if peer else "copy", g.residual_norms()[-1][:2])
+    print("ok", ni, nj, px, py, rk, "peer" if peer else "copy", "ns" if ns else "euler", g.residual_norms()[-1][:2])
 PY
 for tool in memcheck racecheck synccheck; do
   timeout 900 compute-sanitizer --tool $tool --error-exitcode 9 python /tmp/san.py > gpurun_out/san_${TAG}_$tool.log 2>&1; echo rc=$? >> gpurun_out/san_${TAG}_$tool.log
