@@ -356,7 +356,9 @@ def main():
                 "peak_source": "measured DFMA issue rate (profiles/r1_fp64_microbench.txt)",
                 "profile": prof.get("source"), "kernel": ("sfv::stage_kernel + NS gradient/viscous kernels (per stage, averaged)" if args.ns
                            else "sfv::stage_kernel (4 launches per step, averaged)"),
-                "hbm": hbm}
+                "hbm": hbm,
+                **({"note": "NS: the FP64 count per cell-stage is the Euler stage kernel's (ncu); the gradient / "
+                            "viscous-flux kernels add work not counted here (profiles/r1_ns_*)"} if args.ns else {})}
     # ---- end to end through the public API with host buffers ----
     e2e = None
     if not args.no_e2e:
