@@ -527,6 +527,17 @@ __global__ void __launch_bounds__(NT, SFV_MINB) stage_kernel(const __grid_consta
         double *outp = a.out + (size_t)((i_start + 2) * 4) * PJ + (jc + JOFF);
 #pragma unroll kRowUnroll
         for (int v = i_start; v < i_end; ++v) {
+            // NS: this row's viscous sum, loaded before the fluxes so the load
+            // latency hides behind them
+            double rvv[CPL][4];
+            if constexpr (VISC) {
+#pragma unroll
+                for (int k = 0; k < CPL; ++k) {
+                    const double *rvp = a.rv + (size_t)((v + 2) * 4) * PJ + (jc + k + JOFF);
+#pragma unroll
+                    for (int c = 0; c < 4; ++c) rvv[k][c] = __ldg(rvp + (size_t)c * PJ);
+                }
+            }
             wait_w(v + 2);
             double qD[CPL][4], qU[CPL][4], qS[CPL][4], qN[CPL][4], Wv[CPL][4];
             {
@@ -605,9 +616,8 @@ __global__ void __launch_bounds__(NT, SFV_MINB) stage_kernel(const __grid_consta
 #pragma unroll
                 for (int c = 0; c < 4; ++c) R[c] = ((GE[k][c] - GW[k][c]) + GN[k][c]) - GS[k][c];
                 if constexpr (VISC) {  // R = sum (F - F_v) ds (Eq. 5): the viscous sum of this cell
-                    const double *rvp = a.rv + (size_t)((v + 2) * 4) * PJ + (jc + k + JOFF);
 #pragma unroll
-                    for (int c = 0; c < 4; ++c) R[c] -= __ldg(rvp + (size_t)c * PJ);
+                    for (int c = 0; c < 4; ++c) R[c] -= rvv[k][c];
                 }
 #pragma unroll
                 for (int c = 0; c < 4; ++c) {
