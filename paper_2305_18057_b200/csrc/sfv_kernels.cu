@@ -1080,19 +1080,21 @@ __device__ __forceinline__ double *gradp(double *grad, int PG, int i, int j, int
 // Green-Gauss gradient (reading N-R2) of cell (i, j) from the (u, v, T) of
 // the cell and its 4 face neighbours; faces: the mean of the two cells times A
 __device__ __forceinline__ void gg_cell(const double *met, int PJ, int i, int j, const double c[3], const double w[3],
-                                     const double e[3], const double s[3], const double n[3], double g[6]) {
-    const double wx = metf(met, PJ, i, 0, j), wy = metf(met, PJ, i, 1, j), wA = metf(met, PJ, i, 2, j);
-    const double ex = metf(met, PJ, i + 1, 0, j), ey = metf(met, PJ, i + 1, 1, j), eA = metf(met, PJ, i + 1, 2, j);
-    const double sx = metf(met, PJ, i + 1, 3, j), sy = metf(met, PJ, i + 1, 4, j), sA = metf(met, PJ, i + 1, 5, j);
-    const double nx = metf(met, PJ, i + 1, 3, j + 1), ny = metf(met, PJ, i + 1, 4, j + 1),
-                 nA = metf(met, PJ, i + 1, 5, j + 1);
-    const double iV = metf(met, PJ, i + 1, 6, j);
+                                        const double e[3], const double s[3], const double n[3], double g[6]) {
+    // per face: n A / (2 V), so grad = sum_f (phi_L + phi_R) n A / (2 V) with outward signs
+    const double h = DM(0.5, metf(met, PJ, i + 1, 6, j));
+    const double hW = DM(metf(met, PJ, i, 2, j), h), hE = DM(metf(met, PJ, i + 1, 2, j), h);
+    const double hS = DM(metf(met, PJ, i + 1, 5, j), h), hN = DM(metf(met, PJ, i + 1, 5, j + 1), h);
+    const double kWx = DM(metf(met, PJ, i, 0, j), hW), kWy = DM(metf(met, PJ, i, 1, j), hW);
+    const double kEx = DM(metf(met, PJ, i + 1, 0, j), hE), kEy = DM(metf(met, PJ, i + 1, 1, j), hE);
+    const double kSx = DM(metf(met, PJ, i + 1, 3, j), hS), kSy = DM(metf(met, PJ, i + 1, 4, j), hS);
+    const double kNx = DM(metf(met, PJ, i + 1, 3, j + 1), hN), kNy = DM(metf(met, PJ, i + 1, 4, j + 1), hN);
 #pragma unroll
     for (int q = 0; q < 3; ++q) {
-        const double fE = DM(DM(0.5, DA(c[q], e[q])), eA), fW = DM(DM(0.5, DA(w[q], c[q])), wA);
-        const double fN = DM(DM(0.5, DA(c[q], n[q])), nA), fS = DM(DM(0.5, DA(s[q], c[q])), sA);
-        g[2 * q] = DM(DS(DA(DS(DM(fE, ex), DM(fW, wx)), DM(fN, nx)), DM(fS, sx)), iV);
-        g[2 * q + 1] = DM(DS(DA(DS(DM(fE, ey), DM(fW, wy)), DM(fN, ny)), DM(fS, sy)), iV);
+        const double sE = DA(c[q], e[q]), sW = DA(w[q], c[q]), sN = DA(c[q], n[q]), sS = DA(s[q], c[q]);
+        // explicit fma: the same rounding wherever this is inlined
+        g[2 * q] = fma(-sS, kSx, fma(sN, kNx, fma(-sW, kWx, DM(sE, kEx))));
+        g[2 * q + 1] = fma(-sS, kSy, fma(sN, kNy, fma(-sW, kWy, DM(sE, kEy))));
     }
 }
 
@@ -1124,19 +1126,22 @@ __global__ void grad_kernel(const ViscArgs a) {
 __device__ __forceinline__ void face_visc_core(const double gl[6], const double gr[6], const double pl[3],
                                                const double pr[3], double nx, double ny, double A, const Params &P,
                                                double F[4]) {
+    // mean gradients / velocities with the 1/2 folded into the coefficients
     double g[6];
 #pragma unroll
-    for (int q = 0; q < 6; ++q) g[q] = DM(0.5, DA(gl[q], gr[q]));
+    for (int q = 0; q < 6; ++q) g[q] = DA(gl[q], gr[q]);          // 2 x mean
     const double u = DM(0.5, DA(pl[0], pr[0])), v = DM(0.5, DA(pl[1], pr[1]));
-    const double mu = P.mu, lam = -2.0 * mu / 3.0, div = DA(g[0], g[3]);
-    const double txx = DA(DM(DM(2.0, mu), g[0]), DM(lam, div)), tyy = DA(DM(DM(2.0, mu), g[3]), DM(lam, div));
+    const double mu = DM(0.5, P.mu), lam = DM(-2.0 / 3.0, mu), div = DA(g[0], g[3]);
+    const double txx = fma(DM(2.0, mu), g[0], DM(lam, div)), tyy = fma(DM(2.0, mu), g[3], DM(lam, div));
     const double txy = DM(mu, DA(g[1], g[2]));
-    const double thx = DA(DA(DM(u, txx), DM(v, txy)), DM(P.kcond, g[4]));
-    const double thy = DA(DA(DM(u, txy), DM(v, tyy)), DM(P.kcond, g[5]));
+    const double hk = DM(0.5, P.kcond);
+    const double thx = fma(hk, g[4], fma(v, txy, DM(u, txx)));
+    const double thy = fma(hk, g[5], fma(v, tyy, DM(u, txy)));
+    const double ax = DM(nx, A), ay = DM(ny, A);
     F[0] = 0.0;
-    F[1] = DM(DA(DM(txx, nx), DM(txy, ny)), A);
-    F[2] = DM(DA(DM(txy, nx), DM(tyy, ny)), A);
-    F[3] = DM(DA(DM(thx, nx), DM(thy, ny)), A);
+    F[1] = fma(txy, ay, DM(txx, ax));
+    F[2] = fma(tyy, ay, DM(txy, ax));
+    F[3] = fma(thy, ay, DM(thx, ax));
 }
 __device__ __forceinline__ void face_visc(const ViscArgs &a, int iL, int jL, int iR, int jR, const double pl[3],
                                           const double pr[3], double nx, double ny, double A, double F[4]) {
