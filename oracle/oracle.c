@@ -699,7 +699,7 @@ static int check_states(orc_ctx *c, int use_W, int64_t *bad)
  * t_f = (|u nx + v ny| + a) A_f.  cell_v_over_sigma returns V/sigma of one
  * cell (faces W, E, S, N as {nx, ny, A}). */
 static int cell_v_over_sigma(const double *U, const double *fW, const double *fE, const double *fS,
-                             const double *fN, double V, double gamma, double *r)
+                             const double *fN, double V, double gamma, double visc, double *r)
 {
     double prim[4];
     if (orc_primitive(U, gamma, prim) != ORC_OK) return ORC_ERR_STATE;
@@ -710,8 +710,21 @@ static int cell_v_over_sigma(const double *U, const double *fW, const double *fE
     double tS = (fabs(u * fS[0] + v * fS[1]) + a) * fS[2];
     double tN = (fabs(u * fN[0] + v * fN[1]) + a) * fN[2];
     double sigma = ((tW + tE) + tS) + tN;
+    if (visc > 0.0) {
+        /* viscous spectral radius (reading N-R6, revised): visc = 4 max(4/3, gamma) mu / Pr,
+         * sigma_v = visc / rho * (S_I^2 + S_J^2) / V with S_I, S_J the mean face areas */
+        double sI = 0.5 * (fW[2] + fE[2]), sJ = 0.5 * (fS[2] + fN[2]);
+        sigma = sigma + visc / prim[0] * (sI * sI + sJ * sJ) / V;
+    }
     *r = V / sigma;
     return ORC_OK;
+}
+
+static double visc_factor(const orc_config *cf)
+{
+    if (!cf->viscous) return 0.0;
+    double m = cf->gamma > 4.0 / 3.0 ? cf->gamma : 4.0 / 3.0;
+    return 4.0 * m * cf->mu / cf->prandtl;
 }
 
 static int compute_dt(orc_ctx *c, double *dt)
@@ -728,7 +741,8 @@ static int compute_dt(orc_ctx *c, double *dt)
                                       bk->iface + ((int64_t)j * (bk->ni + 1) + i + 1) * 3,
                                       bk->jface + ((int64_t)j * bk->ni + i) * 3,
                                       bk->jface + ((int64_t)(j + 1) * bk->ni + i) * 3,
-                                      bk->vol[(int64_t)j * bk->ni + i], c->cfg.gamma, &r) != ORC_OK)
+                                      bk->vol[(int64_t)j * bk->ni + i], c->cfg.gamma, visc_factor(&c->cfg),
+                                      &r) != ORC_OK)
                     return ORC_ERR_STATE;
                 if (r < mn) mn = r;
             }
@@ -757,7 +771,7 @@ int orc_stable_dt(int32_t ni, int32_t nj, const double *X, const double *Y, cons
                 double r;
                 st = cell_v_over_sigma(U + ((int64_t)(j0 + j) * ni + i) * 4, fi + ((int64_t)j * (ni + 1) + i) * 3,
                                        fi + ((int64_t)j * (ni + 1) + i + 1) * 3, fj + ((int64_t)j * ni + i) * 3,
-                                       fj + ((int64_t)(j + 1) * ni + i) * 3, vol[(int64_t)j * ni + i], gamma, &r);
+                                       fj + ((int64_t)(j + 1) * ni + i) * 3, vol[(int64_t)j * ni + i], gamma, 0.0, &r);
                 if (st != ORC_OK) break;
                 if (r < mn) mn = r;
             }

@@ -259,6 +259,7 @@ void build_params(sfv_ctx *c) {
     P.mu = f.viscous ? f.mu : 0.0;
     P.rgas = f.gas_R > 0.0 ? f.gas_R : 287.0;
     P.rgas_inv = 1.0 / P.rgas;
+    P.visc_dt = f.viscous ? 4.0 * std::max(4.0 / 3.0, f.gamma) * f.mu / f.prandtl : 0.0;
     P.kcond = f.viscous ? f.mu * (f.gamma * P.rgas / (f.gamma - 1.0)) / f.prandtl : 0.0;
 }
 

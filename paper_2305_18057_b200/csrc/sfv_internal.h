@@ -44,6 +44,7 @@ struct Params {
     int limiter;
     // Navier-Stokes (readings N-R1..N-R6)
     double mu, kcond, rgas, rgas_inv;  // viscosity, conductivity mu c_p / Pr, gas constant
+    double visc_dt;                    // 4 max(4/3, gamma) mu / Pr: viscous spectral radius factor (N-R6)
 };
 
 struct StageArgs {

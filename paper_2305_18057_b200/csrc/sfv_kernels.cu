@@ -726,7 +726,12 @@ __global__ void __launch_bounds__(NT, SFV_MINB) stage_kernel(const __grid_consta
                         (fabs(fma(u, mv[3 * WROW + o], vv * mv[4 * WROW + o])) + snd) * mv[5 * WROW + o];
                     const double tN = (fabs(fma(u, mv[3 * WROW + o + 1], vv * mv[4 * WROW + o + 1])) + snd) *
                                       mv[5 * WROW + o + 1];
-                    const double sv = (((tW + tE) + tS) + tN) * iV;
+                    double sv = (((tW + tE) + tS) + tN) * iV;
+                    if constexpr (VISC) {  // viscous spectral radius (reading N-R6)
+                        const double sI = 0.5 * (wfA[k] + mv[2 * WROW + o]);
+                        const double sJ = 0.5 * (mv[5 * WROW + o] + mv[5 * WROW + o + 1]);
+                        sv = fma(P.visc_dt * ir * fma(sI, sI, sJ * sJ), iV * iV, sv);
+                    }
                     smax = (is_out[k] && sv > smax) ? sv : smax;
                     wfx[k] = mv[0 * WROW + o];
                     wfy[k] = mv[1 * WROW + o];
@@ -1396,6 +1401,11 @@ __global__ void sigma_kernel(const double *buf, const double *met, int ni, int n
         const double tS = (fabs(fma(u, m(i + 1, 3, j), vv * m(i + 1, 4, j))) + snd) * m(i + 1, 5, j);
         const double tN = (fabs(fma(u, m(i + 1, 3, j + 1), vv * m(i + 1, 4, j + 1))) + snd) * m(i + 1, 5, j + 1);
         s = (((tW + tE) + tS) + tN) * m(i + 1, 6, j);
+        if (P.visc_dt > 0.0) {  // viscous spectral radius (reading N-R6)
+            const double sI = 0.5 * (m(i, 2, j) + m(i + 1, 2, j)), sJ = 0.5 * (m(i + 1, 5, j) + m(i + 1, 5, j + 1));
+            const double iV = m(i + 1, 6, j);
+            s = fma(P.visc_dt * ir * fma(sI, sI, sJ * sJ), iV * iV, s);
+        }
     }
     for (int o = 16; o > 0; o >>= 1) s = fmax(s, __shfl_xor_sync(0xffffffffu, s, o));
     if ((threadIdx.x & 31) == 0 && s > 0.0)

@@ -168,3 +168,20 @@ def test_heat_conduction_closed_form(oracle_mod):
     inner = R[2:-2, 2:-2]
     np.testing.assert_allclose(inner[..., 3], -2.0 * a * k * V, rtol=1e-9)
     assert np.max(np.abs(inner[..., :3])) < 1e-9 * 2.0 * a * k * V
+
+
+def test_viscous_time_step_closed_form(oracle_mod):
+    """Gas at rest on a uniform square grid of spacing d: the 4 faces give
+    sigma_c = 4 a d and the viscous spectral radius (reading N-R6)
+    sigma_v = 4 max(4/3, gamma) mu / (rho Pr) (d^2 + d^2) / d^2, so
+    dt = CFL d^2 / (sigma_c + sigma_v) exactly (one step records dt_0)."""
+    n, d, mu, Pr, rho, p = 10, 0.01, 3.0e-3, 0.72, 0.6, 5.0e4
+    X, Y = np.meshgrid(np.arange(n + 1) * d, np.arange(n + 1) * d)
+    U = np.zeros((n, n, 4)); U[..., 0] = rho; U[..., 3] = p / (I.GAMMA - 1.0)
+    cfg = I.default_config(n, n, viscous=1, mu=mu, prandtl=Pr, bc=(1, 1, 1, 1), cfl=0.8)
+    o = oracle_mod.Oracle(cfg, X, Y); o.set_state(U); o.step(1)
+    a = np.sqrt(I.GAMMA * p / rho)
+    sv = 4.0 * max(4.0 / 3.0, I.GAMMA) * mu / (rho * Pr) * 2.0
+    np.testing.assert_allclose(o.dt()[0], 0.8 * d * d / (4.0 * a * d + sv), rtol=1e-14)
+    oe = oracle_mod.Oracle(I.default_config(n, n, bc=(1, 1, 1, 1), cfl=0.8), X, Y); oe.set_state(U); oe.step(1)
+    np.testing.assert_allclose(oe.dt()[0], 0.8 * d * d / (4.0 * a * d), rtol=1e-14)
