@@ -118,6 +118,23 @@ __device__ __forceinline__ double frcp(double d) {
     double e = fma(-d, y, 1.0);
     return fma(y, fma(e, e, e), y);
 }
+#ifndef SFV_LIM_RCP2
+#define SFV_LIM_RCP2 1
+#endif
+// Limiter reciprocal: one quadratic Newton step (relative error ~ seed^2,
+// ~1e-14) instead of the cubic one: the limiter value only scales a
+// difference.  C2 +1.5% (profiles/r1_ab_lim_rcp2.txt); parity margins in
+// DESIGN.md §4.2 (C1 gates 4 orders inside; the perturbed-inlet 1000-step
+// difference stays at the oracle's own 1-ulp sensitivity)
+__device__ __forceinline__ double frcp_lim(double d) {
+#if SFV_LIM_RCP2
+    double y;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(d));
+    return fma(y, fma(-d, y, 1.0), y);
+#else
+    return frcp(d);
+#endif
+}
 __device__ __forceinline__ double frsqrt(double x) {
     double y;
     asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
@@ -147,7 +164,7 @@ __device__ __forceinline__ void muscl_cell(double w, double b, double f, const P
         // bounded van Albada, kappa = -1 (c2 = 0): s1 = c1 max(0, (2bf+d)/(b^2+f^2+d))
         //   qU = w + s1 b,  qD = w - s1 f
         // with h = s1/2 = c1 (bf + d/2) / (b^2+f^2+d): max(0, 2h) = h + |h| exactly
-        const double r = frcp(fma(b, b, fma(f, f, P.delta)));
+        const double r = frcp_lim(fma(b, b, fma(f, f, P.delta)));
         const double h = fma(P.c1h, b * f, P.c1dh) * r;
         const double s1 = h + fabs(h);
         qU = fma(s1, b, w);

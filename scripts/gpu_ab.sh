@@ -1,11 +1,11 @@
-# A/B of two libsfv builds on C2 and C3: gpu_ab.sh TAG VARIANT_A VARIANT_B  (variant "" = libsfv.so)
-TAG=${1:-ab}; A=${2:-base}; B=${3:-}
+# A/B of two libsfv builds on C2 and C3: gpu_ab.sh TAG VARIANT_A VARIANT_B  (variant "cur" = libsfv.so)
+TAG=${1:-ab}; A=${2:-base}; B=${3:-cur}
 set -x
 B_="python bench.py --no-cpu-baseline --no-e2e"
-lib() { if [ -z "$1" ]; then echo paper_2305_18057_b200/libsfv.so; else echo paper_2305_18057_b200/libsfv_$1.so; fi; }
+lib() { if [ "$1" = "cur" ]; then echo paper_2305_18057_b200/libsfv.so; else echo paper_2305_18057_b200/libsfv_$1.so; fi; }
 for rep in 1 2; do
 for v in "$A" "$B"; do
-  n=${v:-new}
+  n=$v
   SFV_LIB=$(lib "$v") timeout 300 $B_ --steps 3000 > gpurun_out/ab_${TAG}_c2_${n}_$rep.json 2>&1
   SFV_LIB=$(lib "$v") timeout 300 $B_ --workload C3 --steps 60 --warmup 5 > gpurun_out/ab_${TAG}_c3_${n}_$rep.json 2>&1
 done
