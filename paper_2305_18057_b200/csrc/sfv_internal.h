@@ -14,7 +14,7 @@ namespace sfv {
 // The partitioned index i is the slow one, so the 2 edge rows of an i-cut
 // are one contiguous run (zero-copy halo send/recv).
 // Metrics: memory row m in [0, ni] holds 7 fields, each PJ doubles at column
-// j + JOFF: i-face (m, j) nx, ny, A; j-face (m-1, j) nx, ny, A; 1/V(m-1, j),
+// j + JOFF: i-face (m, j) nx, ny, A/2; j-face (m-1, j) nx, ny, A/2; 1/V(m-1, j),
 // so the stage kernel's iteration over cell row v stages one metrics row
 // (m = v+1) holding its east face, its south face and its volume.
 constexpr int JOFF = 4;

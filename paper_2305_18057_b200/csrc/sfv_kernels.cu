@@ -199,7 +199,7 @@ __device__ __forceinline__ void muscl_cell(double w, double b, double f, const P
 // dissipation form; Roe averages with sqrt(rho) weights from one rsqrt per
 // side).  Returns false if rho <= 0, p <= 0 or a~^2 <= 0 on either side.
 __device__ __forceinline__ bool roe_flux(const double qL[4], const double qR[4], double nx, double ny,
-                                         double A, const Params &P, double G[4]) {
+                                         double hA, const Params &P, double G[4]) {
     const double gm1 = P.gm1;
     const double rsL = frsqrt(qL[0]), rsR = frsqrt(qR[0]);
     const double irL = rsL * rsL, irR = rsR * rsR;
@@ -256,8 +256,7 @@ __device__ __forceinline__ bool roe_flux(const double qL[4], const double qR[4],
     const double F1 = fma(qL[1], VnL, fma(qR[1], VnR, ps * nx));
     const double F2 = fma(qL[2], VnL, fma(qR[2], VnR, ps * ny));
     const double F3 = fma(EpL, VnL, EpR * VnR);
-    const double hA = 0.5 * A;
-    G[0] = (F0 - D0) * hA;
+    G[0] = (F0 - D0) * hA;  // hA = A/2 from the metrics
     G[1] = (F1 - D1) * hA;
     G[2] = (F2 - D2) * hA;
     G[3] = (F3 - D3) * hA;
@@ -636,23 +635,23 @@ __global__ void __launch_bounds__(NT, SFV_MINB) stage_kernel(const __grid_consta
 #pragma unroll
                     for (int c = 0; c < 4; ++c) R[c] -= rvv[k][c];
                 }
+                const double mcv = -coef * iV;  // -(stage coefficient x dt) / V, once per cell
 #pragma unroll
                 for (int c = 0; c < 4; ++c) {
-                    const double rv = R[c] * iV;
                     if constexpr (MODE == M_OWN) {
-                        U[c] = fma(-coef, rv, Wv[k][c]);
+                        U[c] = fma(mcv, R[c], Wv[k][c]);
                     } else if constexpr (MODE == M_UN) {
-                        U[c] = fma(-coef, rv, prow[c * WROW + o]);
+                        U[c] = fma(mcv, R[c], prow[c * WROW + o]);
                     } else if constexpr (MODE == M_RK4F) {
                         const double un = prow[c * WROW + o];
                         const double d2 = prow[(4 + c) * WROW + o] - un;
                         const double d3 = prow[(8 + c) * WROW + o] - un;
                         const double d4 = Wv[k][c] - un;
                         const double comb = (fma(2.0, d3, d2) + d4) * (1.0 / 3.0);
-                        U[c] = un + fma(-coef, rv, comb);
+                        U[c] = un + fma(mcv, R[c], comb);
                     } else {  // M_HEUNF
                         const double un = prow[c * WROW + o];
-                        U[c] = un + fma(-coef, rv, 0.5 * (Wv[k][c] - un));
+                        U[c] = un + fma(mcv, R[c], 0.5 * (Wv[k][c] - un));
                     }
                 }
                 if (is_out[k]) {
@@ -743,10 +742,11 @@ __global__ void __launch_bounds__(NT, SFV_MINB) stage_kernel(const __grid_consta
                         (fabs(fma(u, mv[3 * WROW + o], vv * mv[4 * WROW + o])) + snd) * mv[5 * WROW + o];
                     const double tN = (fabs(fma(u, mv[3 * WROW + o + 1], vv * mv[4 * WROW + o + 1])) + snd) *
                                       mv[5 * WROW + o + 1];
-                    double sv = (((tW + tE) + tS) + tN) * iV;
+                    // metrics hold A/2: twice the half-area sum (exact scaling)
+                    double sv = ((((tW + tE) + tS) + tN) * iV) * 2.0;
                     if constexpr (VISC) {  // viscous spectral radius (reading N-R6)
-                        const double sI = 0.5 * (wfA[k] + mv[2 * WROW + o]);
-                        const double sJ = 0.5 * (mv[5 * WROW + o] + mv[5 * WROW + o + 1]);
+                        const double sI = wfA[k] + mv[2 * WROW + o];  // (A/2 + A/2: the mean area)
+                        const double sJ = mv[5 * WROW + o] + mv[5 * WROW + o + 1];
                         sv = fma(P.visc_dt * ir * fma(sI, sI, sJ * sJ), iV * iV, sv);
                     }
                     smax = (is_out[k] && sv > smax) ? sv : smax;
@@ -1041,14 +1041,14 @@ __global__ void metrics_kernel(const MetricsArgs a) {
         const double A = __dsqrt_rn(__dadd_rn(__dmul_rn(tx, tx), __dmul_rn(ty, ty)));
         rowI[0 * (size_t)a.PJ] = __ddiv_rn(ty, A);
         rowI[1 * (size_t)a.PJ] = __ddiv_rn(-tx, A);
-        rowI[2 * (size_t)a.PJ] = A;
+        rowI[2 * (size_t)a.PJ] = 0.5 * A;  // A/2: the flux's 1/2 (F - D) factor (exact)
     }
     if (i < a.ni) {  // j-face (i, j)
         const double tx = __dsub_rn(X(i + 1, j), X(i, j)), ty = __dsub_rn(Y(i + 1, j), Y(i, j));
         const double A = __dsqrt_rn(__dadd_rn(__dmul_rn(tx, tx), __dmul_rn(ty, ty)));
         rowJ[3 * (size_t)a.PJ] = __ddiv_rn(-ty, A);
         rowJ[4 * (size_t)a.PJ] = __ddiv_rn(tx, A);
-        rowJ[5 * (size_t)a.PJ] = A;
+        rowJ[5 * (size_t)a.PJ] = 0.5 * A;
         if (j < a.nj) {
             const double V = __dmul_rn(
                 0.5, __dsub_rn(__dmul_rn(__dsub_rn(X(i + 1, j + 1), X(i, j)), __dsub_rn(Y(i, j + 1), Y(i + 1, j))),
@@ -1104,7 +1104,7 @@ __device__ __forceinline__ double *gradp(double *grad, int PG, int i, int j, int
 __device__ __forceinline__ void gg_cell(const double *met, int PJ, int i, int j, const double c[3], const double w[3],
                                         const double e[3], const double s[3], const double n[3], double g[6]) {
     // per face: n A / (2 V), so grad = sum_f (phi_L + phi_R) n A / (2 V) with outward signs
-    const double h = DM(0.5, metf(met, PJ, i + 1, 6, j));
+    const double h = metf(met, PJ, i + 1, 6, j);  // (the metrics hold A/2)
     const double hW = DM(metf(met, PJ, i, 2, j), h), hE = DM(metf(met, PJ, i + 1, 2, j), h);
     const double hS = DM(metf(met, PJ, i + 1, 5, j), h), hN = DM(metf(met, PJ, i + 1, 5, j + 1), h);
     const double kWx = DM(metf(met, PJ, i, 0, j), hW), kWy = DM(metf(met, PJ, i, 1, j), hW);
@@ -1159,7 +1159,8 @@ __device__ __forceinline__ void face_visc_core(const double gl[6], const double 
     const double hk = DM(0.5, P.kcond);
     const double thx = fma(hk, g[4], fma(v, txy, DM(u, txx)));
     const double thy = fma(hk, g[5], fma(v, tyy, DM(u, txy)));
-    const double ax = DM(nx, A), ay = DM(ny, A);
+    const double A2 = DA(A, A);  // the metrics hold A/2 (exact doubling)
+    const double ax = DM(nx, A2), ay = DM(ny, A2);
     F[0] = 0.0;
     F[1] = fma(txy, ay, DM(txx, ax));
     F[2] = fma(tyy, ay, DM(txy, ax));
@@ -1417,9 +1418,9 @@ __global__ void sigma_kernel(const double *buf, const double *met, int ni, int n
         const double tE = (fabs(fma(u, m(i + 1, 0, j), vv * m(i + 1, 1, j))) + snd) * m(i + 1, 2, j);
         const double tS = (fabs(fma(u, m(i + 1, 3, j), vv * m(i + 1, 4, j))) + snd) * m(i + 1, 5, j);
         const double tN = (fabs(fma(u, m(i + 1, 3, j + 1), vv * m(i + 1, 4, j + 1))) + snd) * m(i + 1, 5, j + 1);
-        s = (((tW + tE) + tS) + tN) * m(i + 1, 6, j);
+        s = ((((tW + tE) + tS) + tN) * m(i + 1, 6, j)) * 2.0;  // metrics hold A/2
         if (P.visc_dt > 0.0) {  // viscous spectral radius (reading N-R6)
-            const double sI = 0.5 * (m(i, 2, j) + m(i + 1, 2, j)), sJ = 0.5 * (m(i + 1, 5, j) + m(i + 1, 5, j + 1));
+            const double sI = m(i, 2, j) + m(i + 1, 2, j), sJ = m(i + 1, 5, j) + m(i + 1, 5, j + 1);
             const double iV = m(i + 1, 6, j);
             s = fma(P.visc_dt * ir * fma(sI, sI, sJ * sJ), iV * iV, s);
         }
