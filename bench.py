@@ -294,9 +294,29 @@ def main():
             else:
                 args.halo = "copy"
                 halo_note = f"copy (peer mapping unavailable on some rank: {why or 'other rank'})"
-    solver.set_state(U0)
-    solver.step(args.warmup)
-    solver.sync()
+    def warm():
+        solver.set_state(U0)
+        solver.step(args.warmup)
+        solver.sync()
+
+    if world > 1 and args.halo == "peer":
+        # a peer-mode failure on a real multi-GPU node (a neighbour's signal never
+        # arriving -> SFV_ERR_HALO after the device-side timeout) falls back,
+        # collectively, to NCCL copy-mode halos instead of losing the run
+        ok, why = 1, ""
+        try:
+            warm()
+        except sfv.SfvError as ex:
+            ok, why = 0, str(ex)
+        flag = torch.tensor([ok], dtype=torch.int32, device=dev)
+        dist.all_reduce(flag, op=dist.ReduceOp.MIN)
+        if int(flag.item()) == 0:
+            solver.set_halo_mode(sfv.HALO_COPY)
+            args.halo = "copy"
+            halo_note = f"copy (peer-mode warm-up failed on some rank: {why or 'other rank'})"
+            warm()
+    else:
+        warm()
 
     def barrier():
         torch.cuda.synchronize(dev)
