@@ -306,6 +306,8 @@ def main():
         ok, why = 1, ""
         try:
             warm()
+            if os.environ.get("SFV_BENCH_FAKE_PEER_FAILURE") == str(rank):  # exercises the fallback (tests only)
+                raise sfv.SfvError(sfv.ERR_HALO, "injected peer-mode failure")
         except sfv.SfvError as ex:
             ok, why = 0, str(ex)
         flag = torch.tensor([ok], dtype=torch.int32, device=dev)
