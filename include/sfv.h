@@ -15,7 +15,11 @@
  *   - the explicit s-stage Runge-Kutta update of Eq. 6
  *     applied to |Omega| dU/dt + R_h = 0, Eq. 4;
  *   - per step: the CFL time step (reading A-R6) and the residual norms of
- *     R(U^n) ("residual print"; reading A-R20).
+ *     R(U^n) ("residual print"; reading A-R20);
+ *   - optionally (sfv_config.viscous) the viscous normal flux of Eq. 2
+ *     (PAPER.md:73-79): R_h = sum_f (F - F_v) ds with Green-Gauss gradients,
+ *     no-slip adiabatic walls and a viscous term in the time step
+ *     (readings N-R1..N-R6).
  * Everything is IEEE binary64 on the device.
  *
  * Conventions
@@ -170,7 +174,8 @@ sfv_status sfv_set_state(sfv_ctx *ctx, const double *U_global);
 sfv_status sfv_step(sfv_ctx *ctx, int32_t nsteps);
 
 /* Wait for enqueued work; *device_ms (may be NULL) = CUDA-event time of the
- * steps enqueued since the previous sfv_sync.  Surfaces device errors. */
+ * steps enqueued since the previous sfv_sync.  Surfaces device errors
+ * (SFV_ERR_STATE; SFV_ERR_HALO when a device-side wait timed out). */
 sfv_status sfv_sync(sfv_ctx *ctx, double *device_ms);
 
 /* Steps completed (synchronising). */
