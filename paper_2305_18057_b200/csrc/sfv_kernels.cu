@@ -121,6 +121,9 @@ __device__ __forceinline__ double frcp(double d) {
 #ifndef SFV_LIM_RCP2
 #define SFV_LIM_RCP2 1
 #endif
+#ifndef SFV_RV_AHEAD
+#define SFV_RV_AHEAD 1  // NS: register double buffer for the viscous sums (+1.4%, profiles/r1_ns_rv_ahead.txt)
+#endif
 // Limiter reciprocal: one quadratic Newton step (relative error ~ seed^2,
 // ~1e-14) instead of the cubic one: the limiter value only scales a
 // difference.  C2 +1.5% (profiles/r1_ab_lim_rcp2.txt); parity margins in
@@ -541,18 +544,39 @@ __global__ void __launch_bounds__(NT, SFV_MINB) stage_kernel(const __grid_consta
 
         // ---- main loop: one output row per iteration ---------------------------
         double *outp = a.out + (size_t)((i_start + 2) * 4) * PJ + (jc + JOFF);
+#if SFV_RV_AHEAD
+        double rvn[CPL][4];  // NS: next row's viscous sums (register double buffer)
+        if constexpr (VISC) {
+#pragma unroll
+            for (int k = 0; k < CPL; ++k)
+#pragma unroll
+                for (int c = 0; c < 4; ++c)
+                    rvn[k][c] = __ldg(a.rv + (size_t)((i_start + 2) * 4 + c) * PJ + (jc + k + JOFF));
+        }
+#endif
 #pragma unroll kRowUnroll
         for (int v = i_start; v < i_end; ++v) {
             // NS: this row's viscous sum, loaded before the fluxes so the load
             // latency hides behind them
             double rvv[CPL][4];
             if constexpr (VISC) {
+#if SFV_RV_AHEAD
+                // rows v+1's sums load now, row v's were loaded one iteration ago
+#pragma unroll
+                for (int k = 0; k < CPL; ++k)
+#pragma unroll
+                    for (int c = 0; c < 4; ++c) {
+                        rvv[k][c] = rvn[k][c];
+                        rvn[k][c] = v + 1 < i_end ? __ldg(a.rv + (size_t)((v + 3) * 4 + c) * PJ + (jc + k + JOFF)) : 0.0;
+                    }
+#else
 #pragma unroll
                 for (int k = 0; k < CPL; ++k) {
                     const double *rvp = a.rv + (size_t)((v + 2) * 4) * PJ + (jc + k + JOFF);
 #pragma unroll
                     for (int c = 0; c < 4; ++c) rvv[k][c] = __ldg(rvp + (size_t)c * PJ);
                 }
+#endif
             }
             wait_w(v + 2);
             double qD[CPL][4], qU[CPL][4], qS[CPL][4], qN[CPL][4], Wv[CPL][4];
