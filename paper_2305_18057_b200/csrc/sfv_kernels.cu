@@ -1241,7 +1241,7 @@ constexpr int VG_J = VT_J + 2, VG_I = VT_I + 2;  // gradient region
 
 __global__ void __launch_bounds__(VT_J * VT_I) gradvisc_kernel(const ViscArgs a) {
     __shared__ double pr[VP_I][VP_J][3];
-    __shared__ double gs[VG_I][VG_J][6];
+    __shared__ double gs[VG_I][VG_J][7];  // (6 gradients, padded: conflict-free banks)
     const int i0 = blockIdx.y * VT_I, j0 = blockIdx.x * VT_J;
     const int tid = threadIdx.y * VT_J + threadIdx.x;
     // (u, v, T) of cells i0-2 .. i0+VT_I+1, j0-2 .. j0+VT_J+1 inside the ghost frame
