@@ -1235,7 +1235,7 @@ __global__ void visc_kernel(const ViscArgs a) {
 // CTA takes a VT_I x VT_J tile, stages the (u, v, T) of the tile + 2 rings
 // and the gradients of the tile + 1 ring in shared memory, so gradients are
 // computed once and never go through global memory.
-constexpr int VT_J = 32, VT_I = 8;
+constexpr int VT_J = 32, VT_I = 12;  // (tile height sweep: profiles/r1_ns_tile_height.txt)
 constexpr int VP_J = VT_J + 4, VP_I = VT_I + 4;  // (u, v, T) region
 constexpr int VG_J = VT_J + 2, VG_I = VT_I + 2;  // gradient region
 
