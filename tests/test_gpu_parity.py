@@ -419,3 +419,15 @@ def test_thousand_steps_at_the_oracles_own_sensitivity(sfv_mod, oracle_mod):
     e = state_error(g.get_state(), a.get_state()).max()
     assert sens > 1e-10          # the case is ill-conditioned at this horizon
     assert e <= 5.0 * sens, (e, sens)
+
+
+@pytest.mark.parametrize("ni,nj", [(1440, 720), (64, 32), (5760, 2880), (180, 720), (1441, 95)])
+def test_perfmodel_geometry_matches_library(sfv_mod, ni, nj):
+    """The performance model's launch geometry (paper_2305_18057_b200/perfmodel.py)
+    is the library's own segment choice (sfv_launch_info)."""
+    from paper_2305_18057_b200 import perfmodel as M
+    X, Y = I.ramp_nodes(ni, nj, 15.0)
+    g = sfv_mod.Solver(I.default_config(ni, nj), X, Y)
+    li = g.launch_info()
+    strips, segs, _, _ = M.launch_geometry(ni, nj, slots=148 * li["ctas_per_sm"])
+    assert (strips, segs) == (li["strips"], li["segments"])
