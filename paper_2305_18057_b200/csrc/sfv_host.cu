@@ -1,7 +1,8 @@
 // sfv_host.cu -- host runtime behind include/sfv.h: validation, partition
 // and ghost maps, workspace carve-up, per-step CUDA graph, halo exchange
-// (device copies between local blocks, NCCL send/recv between ranks), and
-// history / error bookkeeping.  See DESIGN.md §3-§6.
+// (device copies between local blocks, NCCL send/recv between ranks, or the
+// device-initiated peer mode with CUDA-IPC mappings), the Navier-Stokes
+// per-stage kernels, and history / error bookkeeping.  See DESIGN.md §3-§6.
 #include <dlfcn.h>
 #include <nccl.h>
 

@@ -21,6 +21,12 @@
 // computed once per cell, direction and component (the paper's §5
 // de-duplication), on chip.  No CTA-wide barrier in the main
 // loop; kernels chain with programmatic dependent launch.
+//
+// Template variants: PEER -- the edge tasks also store their edge layers
+// into the neighbour block's ghost frame and signal / wait on per-edge flags
+// (device-initiated halo exchange); VISC -- the Navier-Stokes
+// mode subtracts the viscous residual formed by gradvisc_kernel /
+// grad_kernel + visc_kernel (further below).
 #include "sfv_internal.h"
 
 #include <cstdio>
