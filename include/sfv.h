@@ -181,6 +181,15 @@ sfv_status sfv_sync(sfv_ctx *ctx, double *device_ms);
 /* Steps completed (synchronising). */
 sfv_status sfv_steps_done(sfv_ctx *ctx, int64_t *out);
 
+/* The spatial residual R_h(U) of Eq. 5 (Navier-Stokes
+ * mode: sum_f (F - F_v) ds) of a given host state (full grid, sfv_set_state
+ * layout) into R (same layout): ghost fill of U by the boundary conditions
+ * and the partition exchange, then the fused residual kernel.  Does not
+ * touch the solver's state or histories (uses a stage scratch buffer).
+ * Synchronising; single rank (loopback blocks).  STATE: an invalid face
+ * state of U (cell in sfv_error_info).  UNSUPPORTED: nranks > 1. */
+sfv_status sfv_residual(sfv_ctx *ctx, const double *U_global, double *R_global_out);
+
 /* Residual norms of steps first..first+count-1 (count x 8 doubles), reduced
  * over all blocks and ranks (collective when nranks > 1).  Synchronising.
  * SEQUENCE: range not completed or older than max_history steps. */

@@ -101,6 +101,7 @@ struct Block {
     unsigned *ecnt = nullptr;             // writer arrival counters [4 * CNT_STRIDE]
     PeerView pv[4];                       // neighbour per edge (peer mode)
     double *grad = nullptr, *rv = nullptr;  // Navier-Stokes: gradients (1-layer ghost frame), viscous residual
+    double *resb = nullptr;                 // sfv_residual output (state layout)
     int PG = 0;
     CUtensorMap tm_buf[4], tm_met;  // 2D TMA descriptors (made at sfv_bind)
     size_t buf_elems() const { return (size_t)(ni + 4) * 4 * PJ + PADD; }
@@ -398,6 +399,7 @@ size_t layout(sfv_ctx *c, bool assign) {
         const int PG = b.nj + 2;
         size_t og = take(c->cfg.viscous ? sizeof(double) * (size_t)(b.ni + 2) * 6 * PG : 0);
         size_t orv = take(c->cfg.viscous ? sizeof(double) * b.buf_elems() : 0);
+        size_t ors = take(sizeof(double) * b.buf_elems());
         size_t ox[4];
         for (int k = 0; k < 4; ++k) ox[k] = take(c->nranks > 1 ? sizeof(double) * 8 * (size_t)b.ni : 0);
         if (assign) {
@@ -415,6 +417,7 @@ size_t layout(sfv_ctx *c, bool assign) {
             b.PG = PG;
             b.grad = c->cfg.viscous ? reinterpret_cast<double *>(c->ws + og) : nullptr;
             b.rv = c->cfg.viscous ? reinterpret_cast<double *>(c->ws + orv) : nullptr;
+            b.resb = reinterpret_cast<double *>(c->ws + ors);
         }
     }
     return off;
@@ -1359,6 +1362,64 @@ sfv_status sfv_set_halo_mode(sfv_ctx *c, int32_t mode) {
     c->gexec = c->gexec_norms = nullptr;
     c->graph_failed = false;
     c->have_state = false;  // flags and step counter restart at sfv_set_state
+    return SFV_OK;
+}
+
+sfv_status sfv_residual(sfv_ctx *c, const double *U, double *R) {
+    if (!c || !U || !R) return SFV_ERR_ARG;
+    if (!c->bound) return fail(c, SFV_ERR_SEQUENCE, "sfv_residual before sfv_bind");
+    if (c->nranks > 1) return fail(c, SFV_ERR_UNSUPPORTED, "sfv_residual is single-rank (loopback blocks)");
+    cudaStream_t st = c->st;
+    CK(cudaStreamSynchronize(st));
+    if (c->have_state) {  // a failed run reports first
+        sfv_status s0 = check_device_error(c);
+        if (s0 != SFV_OK) return s0;
+    }
+    CK(cudaMemsetAsync(c->err, 0xff, 8, st));
+    const int NI = c->cfg.ni, k = 1;  // stage buffer 1 is scratch between steps
+    int bcfill[4];
+    for (Block &b : c->blocks) {
+        CK(cudaMemcpy2DAsync(b.stage, (size_t)b.ni * 32, U + ((size_t)b.j0 * NI + b.i0) * 4, (size_t)NI * 32,
+                             (size_t)b.ni * 32, b.nj, cudaMemcpyHostToDevice, st));
+        CK(launch_scatter(b.stage, b.buf[k], b.ni, b.nj, b.PJ, st));
+        for (int e = 0; e < 4; ++e) bcfill[e] = b.edge[e] == E_CONNECTED ? -1 : b.edge[e];
+        CK(launch_poison_corners(b.buf[k], b.ni, b.nj, b.PJ, st));
+        CK(launch_bc_fill(b.buf[k], b.met, b.ni, b.nj, b.PJ, bcfill, c->cfg.inflow_U, st));
+    }
+    sfv_status r = exchange(c, k, st);
+    if (r != SFV_OK) return r;
+    if (c->cfg.viscous) {
+        r = enqueue_viscous(c, k, st);
+        if (r != SFV_OK) return r;
+    }
+    for (Block &b : c->blocks) {
+        StageArgs a = make_args(c, b, 1);
+        a.tm_in = b.tm_buf[k];
+        for (int q = 0; q < 3; ++q) a.tm_pw[q] = b.tm_buf[k];
+        a.in = b.buf[k];
+        a.out = b.resb;
+        a.pw0 = a.pw1 = a.pw2 = nullptr;
+        a.bump = 0;
+        a.row_lo = 0;
+        a.row_hi = b.ni;
+        CK(launch_stage(a, M_RES, false, false, false, c->cfg.viscous != 0, st));
+    }
+    CK(cudaStreamSynchronize(st));
+    unsigned long long e = ~0ull;
+    CK(cudaMemcpy(&e, c->err, sizeof e, cudaMemcpyDeviceToHost));
+    if (e != ~0ull) {  // an invalid face state of U: report it, leave the solver's error word clean
+        CK(cudaMemset(c->err, 0xff, 8));
+        const long long cell = (long long)(e & 0xffffffffull);
+        c->einfo[0] = -1; c->einfo[1] = -1; c->einfo[2] = cell % NI; c->einfo[3] = cell / NI;
+        return fail(c, SFV_ERR_STATE, "invalid face state of the given state at cell (%lld,%lld)", c->einfo[2],
+                    c->einfo[3]);
+    }
+    for (Block &b : c->blocks) {
+        CK(launch_gather(b.resb, b.stage, b.ni, b.nj, b.PJ, st));
+        CK(cudaMemcpy2DAsync(R + ((size_t)b.j0 * NI + b.i0) * 4, (size_t)NI * 32, b.stage, (size_t)b.ni * 32,
+                             (size_t)b.ni * 32, b.nj, cudaMemcpyDeviceToHost, st));
+    }
+    CK(cudaStreamSynchronize(st));
     return SFV_OK;
 }
 

@@ -31,7 +31,7 @@ constexpr int WOUT = 32 * CPL - 2;  // output columns per warp strip (+1 halo co
 constexpr int WROW = 32 * CPL + 4;  // staged doubles per row: columns j0-2 .. j0+32*CPL+1
 
 
-enum Mode { M_OWN = 0, M_UN = 1, M_RK4F = 2, M_HEUNF = 3 };
+enum Mode { M_OWN = 0, M_UN = 1, M_RK4F = 2, M_HEUNF = 3, M_RES = 4 };  // M_RES: write R, no update
 enum Edge { E_INFLOW = 0, E_OUTFLOW = 1, E_SLIP = 2, E_NOSLIP = 3, E_CONNECTED = 4 };
 
 struct Params {

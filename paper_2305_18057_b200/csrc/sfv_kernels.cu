@@ -309,7 +309,7 @@ __device__ __forceinline__ void store4(double *buf, int PJ, int i, int j, const 
 #endif
 template <int MODE>
 struct StageTraits {
-    static constexpr int NPW = MODE == M_OWN ? 0 : (MODE == M_RK4F ? 3 : 1);
+    static constexpr int NPW = (MODE == M_OWN || MODE == M_RES) ? 0 : (MODE == M_RK4F ? 3 : 1);
     // the RK4 final stage (3 pointwise inputs) keeps 1 row in flight per ring
     // (12 CTAs/SM fit in 228 KB only so)
     static constexpr bool DEEP = MODE != M_RK4F;
@@ -679,9 +679,11 @@ __global__ void __launch_bounds__(NT, SFV_MINB) stage_kernel(const __grid_consta
                         const double d4 = Wv[k][c] - un;
                         const double comb = (fma(2.0, d3, d2) + d4) * (1.0 / 3.0);
                         U[c] = un + fma(mcv, R[c], comb);
-                    } else {  // M_HEUNF
+                    } else if constexpr (MODE == M_HEUNF) {
                         const double un = prow[c * WROW + o];
                         U[c] = un + fma(mcv, R[c], 0.5 * (Wv[k][c] - un));
+                    } else {  // M_RES: the residual itself (sfv_residual)
+                        U[c] = R[c];
                     }
                 }
                 if (is_out[k]) {
@@ -689,12 +691,12 @@ __global__ void __launch_bounds__(NT, SFV_MINB) stage_kernel(const __grid_consta
                     for (int c = 0; c < 4; ++c) outp[(size_t)c * PJ + k] = U[c];
                 }
                 // new-state validity: rho > 0 and 2 rho E > |m|^2 (<=> p > 0)
-                const bool st_ok = (U[0] > 0.0) & (2.0 * U[0] * U[3] > fma(U[1], U[1], U[2] * U[2]));
+                const bool st_ok = MODE == M_RES || ((U[0] > 0.0) & (2.0 * U[0] * U[3] > fma(U[1], U[1], U[2] * U[2])));
                 const int jk = jc + k;
                 bad |= (is_out[k] & (!okE[k] | !st_ok)) | (jflux[k] & !okS[k]);
                 // physical-boundary ghosts of the new state (reading A-R11), behind one
                 // warp-uniform test: only strips at the S / N walls and rows 0, 1, ni-2, ni-1
-                if ((ghost_sn || (ghost_w && v <= 1) || (ghost_e && v >= a.ni - 2)) && is_out[k]) {
+                if (MODE != M_RES && (ghost_sn || (ghost_w && v <= 1) || (ghost_e && v >= a.ni - 2)) && is_out[k]) {
                     if (a.bc[2] == E_SLIP && jk <= 1) {
                         double g[4];
                         const int k0 = o - jk;  // column 0
@@ -803,7 +805,7 @@ __global__ void __launch_bounds__(NT, SFV_MINB) stage_kernel(const __grid_consta
                         if (J > a.NJ - 1) J = a.NJ - 1;
                         atomicMin(a.err, err_key(n, a.nstages, a.stage, 0, (long long)J * a.NI + a.gi0 + v));
                     }
-                    if (is_out[k]) {
+                    if (MODE != M_RES && is_out[k]) {
                         const double *pr = outp - (size_t)4 * PJ;  // the row just stored
                         const double u0 = pr[k], u3 = pr[(size_t)3 * PJ + k];
                         const double u1 = pr[(size_t)PJ + k], u2 = pr[(size_t)2 * PJ + k];
@@ -1002,6 +1004,7 @@ static cudaError_t occ_t(int *n) {
         case M_RK4F * 4 + 0: return FN<M_RK4F, false, false, F, Q, V>(__VA_ARGS__);      \
         case M_HEUNF * 4 + 1: return FN<M_HEUNF, false, true, F, Q, V>(__VA_ARGS__);     \
         case M_HEUNF * 4 + 0: return FN<M_HEUNF, false, false, F, Q, V>(__VA_ARGS__);    \
+        case M_RES * 4 + 0: return FN<M_RES, false, false, F, Q, V>(__VA_ARGS__);        \
         default: return cudaErrorInvalidValue;                                           \
     }
 // (peer halos and Navier-Stokes are not combined: NS runs in copy mode)
@@ -1033,8 +1036,8 @@ static cudaError_t stage_occupancy_v(int mode, bool norms, bool dtmax, bool fast
     SFV_DISPATCH(occ_t, n)
 }
 cudaError_t prepare_stage_kernels() {
-    const int variants[8][3] = {{M_OWN, 1, 0}, {M_OWN, 0, 0}, {M_UN, 0, 0}, {M_UN, 0, 1},
-                                {M_RK4F, 0, 1}, {M_RK4F, 0, 0}, {M_HEUNF, 0, 1}, {M_HEUNF, 0, 0}};
+    const int variants[9][3] = {{M_OWN, 1, 0}, {M_OWN, 0, 0}, {M_UN, 0, 0}, {M_UN, 0, 1},  {M_RK4F, 0, 1},
+                                {M_RK4F, 0, 0}, {M_HEUNF, 0, 1}, {M_HEUNF, 0, 0}, {M_RES, 0, 0}};
     for (auto &v : variants)
         for (int f = 0; f < 6; ++f) {
             int n = 0;
@@ -1046,6 +1049,7 @@ cudaError_t prepare_stage_kernels() {
 }
 size_t stage_smem_bytes(int mode) {
     switch (mode) {
+        case M_RES: return stage_smem<M_RES>();
         case M_OWN: return stage_smem<M_OWN>();
         case M_UN: return stage_smem<M_UN>();
         case M_RK4F: return stage_smem<M_RK4F>();

@@ -27,7 +27,7 @@ ABI_SYMBOLS = ["sfv_create", "sfv_partition", "sfv_nccl_unique_id", "sfv_partiti
                "sfv_workspace_size", "sfv_bind", "sfv_set_state", "sfv_step", "sfv_sync", "sfv_steps_done",
                "sfv_get_residual_norms", "sfv_get_dt", "sfv_get_state", "sfv_error_info", "sfv_launch_info",
                "sfv_debug_math", "sfv_set_halo_mode", "sfv_peer_handle", "sfv_peer_connect",
-               "sfv_debug_block_buffer",
+               "sfv_debug_block_buffer", "sfv_residual",
                "sfv_last_error", "sfv_destroy"]
 
 
@@ -85,6 +85,7 @@ def lib():
         L.sfv_peer_handle.argtypes = [_VP, _VP]
         L.sfv_peer_connect.argtypes = [_VP, _VP]
         L.sfv_debug_block_buffer.argtypes = [_VP, C.c_int32, C.c_int32, _D]
+        L.sfv_residual.argtypes = [_VP, _D, _D]
         L.sfv_last_error.argtypes = [_VP]
         L.sfv_last_error.restype = C.c_char_p
         L.sfv_destroy.argtypes = [_VP]
@@ -261,6 +262,13 @@ class Solver:
 
     def get_state_ptr(self, ptr):
         self._check(lib().sfv_get_state(self._h, C.cast(C.c_void_p(ptr), _D)))
+
+    def residual(self, U):
+        """R_h(U) of Eq. 5 on the device (sfv_residual), [nj, ni, 4]."""
+        U = np.ascontiguousarray(U, np.float64)
+        out = np.empty((self.nj, self.ni, 4))
+        self._check(lib().sfv_residual(self._h, _dp(U), _dp(out)))
+        return out
 
     def residual_norms(self, first=0, count=None):
         if count is None:
