@@ -304,7 +304,8 @@ __device__ __forceinline__ void store4(double *buf, int PJ, int i, int j, const 
 #ifndef SFV_DEEP_MASK
 // rings with 2 rows in flight instead of 1 (bit 0: stencil, 1: metrics, 2:
 // pointwise).  Measured on C2 / C3 (profiles/r1_ab_ring_depth.txt): pointwise
-// +0.3% / +1.3%, stencil -0.2% / +0.3%, all three -8% / -1%
+// +0.3% / +1.3%, stencil -0.2% / +0.3%, all three -8% / -1%; on v20 stencil+pointwise
+// -1.3%, metrics+pointwise -8.6% (C2)
 #define SFV_DEEP_MASK 4
 #endif
 template <int MODE>
