@@ -21,6 +21,12 @@
  * (SPEC.md:309), the 4-face CFL time step, the largest
  * remainder partition.
  *
+ * Parity unpinned (conventions, checked only by GPU-vs-oracle consistency;
+ * DESIGN.md §2): the Harten constant and wave set, the bounded van Albada
+ * form among admissible limiters, the CFL number, the ramp node
+ * distribution, the Jameson-4 coefficients, the NS ghost-gradient /
+ * face-average rules beyond their exactness pins, the viscous dt constant.
+ *
  * Only tests/, __graft_entry__.smoke() and bench.py's oracle legs use this
  * file.  It is built with -O2 -ffp-contract=off; '/' and sqrt() are IEEE.
  * No blocking, fusion or reordering: each step of the algorithm is a
