@@ -15,6 +15,8 @@ for (ni, nj, px, py, rk, peer, ns) in [(64, 32, 1, 1, 0, 0, 0), (40, 36, 2, 2, 0
         g.enable_peer_halo()
     g.set_state(I.perturbed_state(ni, nj, 1)); g.step(3); g.sync()
     assert np.all(np.isfinite(g.get_state()))
+    R = g.residual(I.perturbed_state(ni, nj, 2))   # sfv_residual (M_RES kernel variant)
+    assert np.all(np.isfinite(R))
     print("ok", ni, nj, px, py, rk, "peer" if peer else "copy", "ns" if ns else "euler", g.residual_norms()[-1][:2])
 PY
 for tool in memcheck racecheck synccheck; do
