@@ -163,22 +163,43 @@ sfv_status sfv_workspace_size(const sfv_ctx *ctx, size_t *bytes);
  * OOM: workspace too small.  CUDA: no device / launch failure. */
 sfv_status sfv_bind(sfv_ctx *ctx, void *device_workspace, size_t bytes, void *cuda_stream);
 
-/* Load the initial state (host array, full grid; every rank passes the full
- * array and keeps its blocks), fill the ghost frames (boundary conditions +
- * halo exchange), compute dt_0, reset the step counter, history and error
- * word.  Synchronous.  STATE: some rho <= 0 or p <= 0. */
+/* Load the initial state U^0 of the explicit scheme (Eq. 6, PAPER.md:105-113:
+ * the RK stages start from U^n; the paper's host side "sets up" the data,
+ * PAPER.md:120) from a host array, full grid, layout (j*ni + i)*4 + k,
+ * k = rho, rho u, rho v, rho E (states must have rho > 0, p > 0);
+ * every rank passes the full array and keeps its blocks.  Fills the ghost
+ * frames (boundary conditions, + halo exchange),
+ * computes dt_0, resets the step counter, histories and
+ * error word.  The caller's array is only read during the call.  Synchronous;
+ * collective when nranks > 1 (all ranks agree on the error before returning).
+ * STATE: some rho <= 0 or p <= 0 (the globally first cell in sfv_error_info).
+ * NCCL: exchange / all-reduce failed or timed out (see sfv_set_comm_timeout). */
 sfv_status sfv_set_state(sfv_ctx *ctx, const double *U_global);
 
-/* Enqueue nsteps full RK steps on the bound stream (a CUDA graph per step);
- * returns immediately.  SEQUENCE: before sfv_set_state. */
+/* Enqueue nsteps full explicit RK steps U^n -> U^{n+1} (Eq. 6, PAPER.md:105-113;
+ * each stage: ghost refresh, limiter + MUSCL Eq. 7,
+ * PAPER.md:141-151, Roe flux, residual Eq. 5, PAPER.md:97-101,
+ * update) on the bound stream (a CUDA graph per step); returns immediately.
+ * Invalid states found on the device are reported by the next synchronising
+ * call ("aborts the step with stage index").  Collective in the
+ * sense that every rank must step the same number of times.
+ * SEQUENCE: before sfv_set_state.  NCCL: communicator aborted earlier. */
 sfv_status sfv_step(sfv_ctx *ctx, int32_t nsteps);
 
 /* Wait for enqueued work; *device_ms (may be NULL) = CUDA-event time of the
- * steps enqueued since the previous sfv_sync.  Surfaces device errors
- * (SFV_ERR_STATE; SFV_ERR_HALO when a device-side wait timed out). */
+ * steps enqueued since the previous sfv_sync (the per-iteration time the
+ * paper's model is written in, Eq. 8/14).  Surfaces this
+ * rank's device errors (SFV_ERR_STATE with step, stage, i, j: SPEC.md:241,
+ * :289; SFV_ERR_HALO when a device-side peer wait timed out).  With NCCL
+ * ranks the wait is bounded: no step completing within the comm timeout (a
+ * neighbour that never sends), or an NCCL async error, aborts the
+ * communicator and returns SFV_ERR_NCCL naming this rank's edges and the
+ * pending step ("missing neighbor message beyond a configurable
+ * timeout -> deadlock error naming the edge"). */
 sfv_status sfv_sync(sfv_ctx *ctx, double *device_ms);
 
-/* Steps completed (synchronising). */
+/* Steps completed, n of U^n (Eq. 6).  Synchronising (bounded
+ * wait as sfv_sync). */
 sfv_status sfv_steps_done(sfv_ctx *ctx, int64_t *out);
 
 /* The spatial residual R_h(U) of Eq. 5 (Navier-Stokes
@@ -190,17 +211,29 @@ sfv_status sfv_steps_done(sfv_ctx *ctx, int64_t *out);
  * state of U (cell in sfv_error_info).  UNSUPPORTED: nranks > 1. */
 sfv_status sfv_residual(sfv_ctx *ctx, const double *U_global, double *R_global_out);
 
-/* Residual norms of steps first..first+count-1 (count x 8 doubles), reduced
- * over all blocks and ranks (collective when nranks > 1).  Synchronising.
+/* The "residual print" of the solver loop (reading A-R20):
+ * per step n in first..first+count-1, out[n*8 + k] = L2_k = sqrt(sum_c
+ * R_k(U^n)_c^2 / (ni nj)) and out[n*8 + 4 + k] = Linf_k = max_c |R_k(U^n)_c|,
+ * R the Eq. 5 residual of the step's first stage, raw
+ * units, count x 8 host doubles owned by the caller.  Reduced over all
+ * blocks and ranks in a fixed order (deterministic).  Synchronising;
+ * collective when nranks > 1 (device errors are agreed over ranks first).
  * SEQUENCE: range not completed or older than max_history steps. */
 sfv_status sfv_get_residual_norms(sfv_ctx *ctx, int64_t first, int64_t count, double *out);
 
-/* Time steps dt_n used by steps first..first+count-1.  Synchronising. */
+/* Time steps dt_n used by steps first..first+count-1 (count host doubles):
+ * dt_n = CFL min_c V_c / sum_f (|u.n_f| + a) A_f of U^n (SPEC.md:294-302,
+ * reading A-R6; "if stability conditions are satisfied"), or
+ * dt_fixed.  Identical on every rank.  Synchronising (bounded wait).
+ * SEQUENCE: range not available. */
 sfv_status sfv_get_dt(sfv_ctx *ctx, int64_t first, int64_t count, double *out);
 
-/* Copy the current interior state to a host array (full grid, same layout
- * as sfv_set_state).  Collective when nranks > 1 (all ranks receive the
- * full state).  Synchronising. */
+/* "Solution output": copy the current interior state U^n to a
+ * host array owned by the caller (full grid, same layout as sfv_set_state).
+ * Collective when nranks > 1: every rank receives the full state (each
+ * rank's block is broadcast in turn through a device buffer the size of the
+ * largest block).  Synchronising; device errors are agreed over ranks first.
+ * STATE: the run hit an invalid state.  NCCL: gather failed / timed out. */
 sfv_status sfv_get_state(sfv_ctx *ctx, double *U_global_out);
 
 /* Details of the last SFV_ERR_STATE / GEOMETRY: out4 = step, stage, i, j
@@ -248,10 +281,36 @@ sfv_status sfv_peer_connect(sfv_ctx *ctx, const void *handles);
  * Synchronising.  ARG: block not local or k out of range. */
 sfv_status sfv_debug_block_buffer(sfv_ctx *ctx, int32_t block, int32_t k, double *out);
 
+/* Per-class stage timing (the paper's iteration breakdown: interior
+ * residual, boundary work and data exchange, PAPER.md:157, :172, :195;
+ * SPEC.md:338-341 StageTimings).  on != 0: subsequent sfv_step calls enqueue
+ * each stage without the CUDA graph, with CUDA events around every class of
+ * work (slower per step: a diagnostic mode); accumulators are reset.
+ * Synchronising.  SEQUENCE: before sfv_bind. */
+sfv_status sfv_set_profiling(sfv_ctx *ctx, int32_t on);
+
+/* Accumulated device milliseconds since sfv_set_profiling(ctx, 1), out[9]:
+ * [0] edge-row stage kernels (launched first when a connected i-cut is
+ * overlapped), [1] interior stage kernels (all stage kernels when not split),
+ * [2] row-halo exchange (on the comm stream when overlapped; every exchange
+ * when not), [3] column-halo pack/exchange/unpack, [4] exposed wait of the
+ * compute stream for the comm stream, [5] dt all-reduce, [6] Navier-Stokes
+ * viscous kernels, [7] norms batches, [8] number of profiled steps.
+ * Classes on different streams overlap in time.  Synchronising. */
+sfv_status sfv_get_stage_timings(sfv_ctx *ctx, double *out9);
+
+/* Failure detection of the NCCL path: a synchronising call
+ * that sees no step complete for `seconds` (default 60) aborts the
+ * communicator and returns SFV_ERR_NCCL naming the edges.  ARG: seconds <= 0. */
+sfv_status sfv_set_comm_timeout(sfv_ctx *ctx, double seconds);
+
 /* Text of the last error on ctx (ctx-owned, valid until the next call). */
 const char *sfv_last_error(const sfv_ctx *ctx);
 
-/* Free library-owned host, CUDA-graph and NCCL resources (not the workspace). */
+/* Free library-owned host, CUDA-graph and NCCL resources (not the workspace).
+ * Drains the bound stream first (and, in peer mode across ranks, an
+ * all-reduce barrier so no neighbour still stores into this workspace), so
+ * the caller may release the workspace once this returns. */
 void sfv_destroy(sfv_ctx *ctx);
 
 #ifdef __cplusplus

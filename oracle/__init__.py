@@ -15,6 +15,7 @@ import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "liboracle.so")
+LIB_OMP_PATH = os.path.join(HERE, "liboracle_omp.so")  # same source, -fopenmp (bench.py all-cores baseline)
 SRC = os.path.join(HERE, "oracle.c")
 
 ORC_OK, ORC_ERR_ARG, ORC_ERR_GEOMETRY, ORC_ERR_STATE, ORC_ERR_SEQUENCE = range(5)
@@ -28,17 +29,20 @@ class OracleError(RuntimeError):
         self.info = info
 
 
-def build(force=False):
-    """Compile liboracle.so: -O2 -ffp-contract=off (no FMA contraction)."""
-    if (not force and os.path.exists(LIB_PATH)
-            and os.path.getmtime(LIB_PATH) >= max(os.path.getmtime(SRC),
-                                                  os.path.getmtime(os.path.join(HERE, "oracle.h")))):
-        return LIB_PATH
+def build(force=False, omp=False):
+    """Compile liboracle.so: -O2 -ffp-contract=off (no FMA contraction);
+    omp=True: liboracle_omp.so, the same source with -fopenmp (row loops
+    shared among threads, bitwise equal to the single-threaded build)."""
+    path = LIB_OMP_PATH if omp else LIB_PATH
+    if (not force and os.path.exists(path)
+            and os.path.getmtime(path) >= max(os.path.getmtime(SRC),
+                                              os.path.getmtime(os.path.join(HERE, "oracle.h")))):
+        return path
     cmd = ["gcc", "-std=c99", "-O2", "-ffp-contract=off", "-fno-fast-math",
-           "-fPIC", "-shared", "-o", LIB_PATH + ".tmp", SRC, "-lm"]
+           *(["-fopenmp"] if omp else []), "-fPIC", "-shared", "-o", path + ".tmp", SRC, "-lm"]
     subprocess.check_call(cmd)
-    os.replace(LIB_PATH + ".tmp", LIB_PATH)
-    return LIB_PATH
+    os.replace(path + ".tmp", path)
+    return path
 
 
 class orc_config(C.Structure):
@@ -59,11 +63,24 @@ _I32 = C.POINTER(C.c_int32)
 _I64 = C.POINTER(C.c_int64)
 
 
-def lib():
-    global _lib
+_lib_omp = None
+
+
+def lib(omp=False):
+    global _lib, _lib_omp
+    if omp:
+        if _lib_omp is None:
+            build(omp=True)
+            _lib_omp = _declare(C.CDLL(LIB_OMP_PATH))
+        return _lib_omp
     if _lib is None:
         build()
-        L = C.CDLL(LIB_PATH)
+        _lib = _declare(C.CDLL(LIB_PATH))
+    return _lib
+
+
+def _declare(L):
+    if True:
         L.orc_metrics.argtypes = [C.c_int32, C.c_int32, _D, _D, _D, _D, _D, _I64]
         L.orc_primitive.argtypes = [_D, C.c_double, _D]
         L.orc_limiter.argtypes = [C.c_int32, C.c_double, C.c_double, C.c_double]
@@ -95,8 +112,7 @@ def lib():
         L.orc_last_error.restype = C.c_char_p
         L.orc_destroy.argtypes = [C.c_void_p]
         L.orc_destroy.restype = None
-        _lib = L
-    return _lib
+    return L
 
 
 def _dp(a):
@@ -197,13 +213,15 @@ def make_config(d, residual_kind=RES_EULER, linear_rate=0.0):
 class Oracle:
     """Mirror of the sfv C ABI on the CPU (SURVEY.md §8(b) 'oracle mirror')."""
 
-    def __init__(self, cfg, X, Y, residual_kind=RES_EULER, linear_rate=0.0):
+    def __init__(self, cfg, X, Y, residual_kind=RES_EULER, linear_rate=0.0, omp=False):
+        """omp=True: the -fopenmp build (thread count from OMP_NUM_THREADS)."""
+        self._L = lib(omp)
         self.cfg = dict(cfg)
         self._c = make_config(cfg, residual_kind, linear_rate)
         self._X = _f64(X); self._Y = _f64(Y)
         h = C.c_void_p()
         self._h = None
-        st = lib().orc_create(C.byref(self._c), _dp(self._X), _dp(self._Y), C.byref(h))
+        st = self._L.orc_create(C.byref(self._c), _dp(self._X), _dp(self._Y), C.byref(h))
         if st:
             raise OracleError(st, "orc_create failed")
         self._h = h
@@ -212,72 +230,72 @@ class Oracle:
     def _check(self, st):
         if st:
             info = np.zeros(4, np.int64)
-            lib().orc_error_info(self._h, info.ctypes.data_as(_I64))
-            raise OracleError(st, lib().orc_last_error(self._h).decode(), tuple(int(v) for v in info))
+            self._L.orc_error_info(self._h, info.ctypes.data_as(_I64))
+            raise OracleError(st, self._L.orc_last_error(self._h).decode(), tuple(int(v) for v in info))
 
     def partition(self, px, py, wx=None, wy=None):
         wxa = None if wx is None else np.ascontiguousarray(wx, np.int32)
         wya = None if wy is None else np.ascontiguousarray(wy, np.int32)
-        self._check(lib().orc_partition(self._h, px, py,
+        self._check(self._L.orc_partition(self._h, px, py,
                                         None if wxa is None else wxa.ctypes.data_as(_I32),
                                         None if wya is None else wya.ctypes.data_as(_I32)))
         self.nblocks = px * py
 
     def partition_map(self, block):
         out = np.zeros(8, np.int32)
-        self._check(lib().orc_partition_map(self._h, block, out.ctypes.data_as(_I32)))
+        self._check(self._L.orc_partition_map(self._h, block, out.ctypes.data_as(_I32)))
         return out
 
     def set_state(self, U):
         U = _f64(U, (self.nj, self.ni, 4))
-        self._check(lib().orc_set_state(self._h, _dp(U)))
+        self._check(self._L.orc_set_state(self._h, _dp(U)))
 
     def step(self, n=1):
-        self._check(lib().orc_step(self._h, n))
+        self._check(self._L.orc_step(self._h, n))
 
     def get_state(self):
         U = np.empty((self.nj, self.ni, 4))
-        self._check(lib().orc_get_state(self._h, _dp(U)))
+        self._check(self._L.orc_get_state(self._h, _dp(U)))
         return U
 
     @property
     def steps_done(self):
-        return lib().orc_steps_done(self._h)
+        return self._L.orc_steps_done(self._h)
 
     def residual_norms(self, first=0, count=None):
         if count is None:
             count = self.steps_done - first
         out = np.empty((count, 8))
-        self._check(lib().orc_get_residual_norms(self._h, first, count, _dp(out)))
+        self._check(self._L.orc_get_residual_norms(self._h, first, count, _dp(out)))
         return out
 
     def dt(self, first=0, count=None):
         if count is None:
             count = self.steps_done - first
         out = np.empty(count)
-        self._check(lib().orc_get_dt(self._h, first, count, _dp(out)))
+        self._check(self._L.orc_get_dt(self._h, first, count, _dp(out)))
         return out
 
     def residual(self, U):
         U = _f64(U, (self.nj, self.ni, 4)); R = np.empty_like(U)
-        self._check(lib().orc_residual(self._h, _dp(U), _dp(R)))
+        self._check(self._L.orc_residual(self._h, _dp(U), _dp(R)))
         return R
 
     def gradients(self, U):
         """Green-Gauss cell gradients (u_x, u_y, v_x, v_y, T_x, T_y), [nj, ni, 6]."""
         U = _f64(U, (self.nj, self.ni, 4)); G = np.empty((self.nj, self.ni, 6))
-        self._check(lib().orc_gradients(self._h, _dp(U), _dp(G)))
+        self._check(self._L.orc_gradients(self._h, _dp(U), _dp(G)))
         return G
 
     def ghost_frame(self, U):
         U = _f64(U, (self.nj, self.ni, 4))
         F = np.empty((self.nj + 4, self.ni + 4, 4))
-        self._check(lib().orc_ghost_frame(self._h, _dp(U), _dp(F)))
+        self._check(self._L.orc_ghost_frame(self._h, _dp(U), _dp(F)))
         return F
 
     def close(self):
         if self._h is not None:
-            lib().orc_destroy(self._h)
+            self._L.orc_destroy(self._h)
             self._h = None
 
     def __del__(self):

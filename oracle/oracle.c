@@ -29,6 +29,12 @@
  *
  * Only tests/, __graft_entry__.smoke() and bench.py's oracle legs use this
  * file.  It is built with -O2 -ffp-contract=off; '/' and sqrt() are IEEE.
+ * The same source built with -fopenmp (liboracle_omp.so, bench.py's
+ * all-cores CPU baseline only) shares the row loops among threads: every
+ * cell, face and stage value is computed by the same expression, the norm
+ * sums stay serial and the dt minimum / first-error key are exact min
+ * reductions, so it is bitwise equal to the single-threaded build
+ * (tests/test_oracle_pins.py::test_openmp_build_is_bitwise_single_thread).
  * No blocking, fusion or reordering: each step of the algorithm is a
  * separate loop in the order SURVEY.md §8(c).2 lists them.
  */
@@ -622,6 +628,7 @@ static int residual_block(orc_ctx *c, orc_block *bk, double *R, int64_t *bad)
                                           * bk->W[FR(bk, i, j) + k];
         return ORC_OK;
     }
+#pragma omp parallel for schedule(static)
     for (int32_t j = 0; j < bk->nj; ++j)
         for (int32_t i = 0; i <= bk->ni; ++i) {
             double QL[4], QR[4], F[4];
@@ -634,8 +641,11 @@ static int residual_block(orc_ctx *c, orc_block *bk, double *R, int64_t *bad)
             if (orc_roe_flux(QL, QR, f[0], f[1], cf->gamma, cf->harten_eps, F) != ORC_OK) {
                 int64_t gi = bk->i0 + i; if (gi > NI - 1) gi = NI - 1;
                 int64_t key = (bk->j0 + j) * NI + gi;
-                if (*bad < 0 || key < *bad) *bad = key;
-                status = ORC_ERR_STATE;
+#pragma omp critical(orc_bad)
+                {
+                    if (*bad < 0 || key < *bad) *bad = key;
+                    status = ORC_ERR_STATE;
+                }
                 for (int k = 0; k < 4; ++k) F[k] = NAN;
             }
             if (cf->viscous) {
@@ -645,6 +655,7 @@ static int residual_block(orc_ctx *c, orc_block *bk, double *R, int64_t *bad)
             }
             for (int k = 0; k < 4; ++k) bk->GI[((int64_t)j * (bk->ni + 1) + i) * 4 + k] = F[k] * f[2];
         }
+#pragma omp parallel for schedule(static)
     for (int32_t j = 0; j <= bk->nj; ++j)
         for (int32_t i = 0; i < bk->ni; ++i) {
             double QL[4], QR[4], F[4];
@@ -657,8 +668,11 @@ static int residual_block(orc_ctx *c, orc_block *bk, double *R, int64_t *bad)
             if (orc_roe_flux(QL, QR, f[0], f[1], cf->gamma, cf->harten_eps, F) != ORC_OK) {
                 int64_t gj = bk->j0 + j; if (gj > NJ - 1) gj = NJ - 1;
                 int64_t key = gj * NI + (bk->i0 + i);
-                if (*bad < 0 || key < *bad) *bad = key;
-                status = ORC_ERR_STATE;
+#pragma omp critical(orc_bad)
+                {
+                    if (*bad < 0 || key < *bad) *bad = key;
+                    status = ORC_ERR_STATE;
+                }
                 for (int k = 0; k < 4; ++k) F[k] = NAN;
             }
             if (cf->viscous) {
@@ -668,6 +682,7 @@ static int residual_block(orc_ctx *c, orc_block *bk, double *R, int64_t *bad)
             }
             for (int k = 0; k < 4; ++k) bk->GJ[((int64_t)j * bk->ni + i) * 4 + k] = F[k] * f[2];
         }
+#pragma omp parallel for schedule(static)
     for (int32_t j = 0; j < bk->nj; ++j)
         for (int32_t i = 0; i < bk->ni; ++i)
             for (int k = 0; k < 4; ++k) {
@@ -686,14 +701,18 @@ static int check_states(orc_ctx *c, int use_W, int64_t *bad)
     int status = ORC_OK;
     for (int32_t n = 0; n < c->nblocks; ++n) {
         orc_block *bk = &c->b[n];
+#pragma omp parallel for schedule(static)
         for (int32_t j = 0; j < bk->nj; ++j)
             for (int32_t i = 0; i < bk->ni; ++i) {
                 const double *u = use_W ? bk->W + FR(bk, i, j) : bk->Un + IN(bk, i, j);
                 double prim[4];
                 if (orc_primitive(u, c->cfg.gamma, prim) != ORC_OK) {
                     int64_t key = (int64_t)(bk->j0 + j) * c->cfg.ni + (bk->i0 + i);
-                    if (*bad < 0 || key < *bad) *bad = key;
-                    status = ORC_ERR_STATE;
+#pragma omp critical(orc_bad)
+                    {
+                        if (*bad < 0 || key < *bad) *bad = key;
+                        status = ORC_ERR_STATE;
+                    }
                 }
             }
     }
@@ -737,8 +756,10 @@ static int compute_dt(orc_ctx *c, double *dt)
 {
     if (c->cfg.dt_fixed > 0.0) { *dt = c->cfg.dt_fixed; return ORC_OK; }
     double mn = INFINITY;
+    int bad = 0;
     for (int32_t n = 0; n < c->nblocks; ++n) {
         orc_block *bk = &c->b[n];
+#pragma omp parallel for schedule(static) reduction(min : mn) reduction(| : bad)
         for (int32_t j = 0; j < bk->nj; ++j)
             for (int32_t i = 0; i < bk->ni; ++i) {
                 double r;
@@ -749,10 +770,12 @@ static int compute_dt(orc_ctx *c, double *dt)
                                       bk->jface + ((int64_t)(j + 1) * bk->ni + i) * 3,
                                       bk->vol[(int64_t)j * bk->ni + i], c->cfg.gamma, visc_factor(&c->cfg),
                                       &r) != ORC_OK)
-                    return ORC_ERR_STATE;
-                if (r < mn) mn = r;
+                    bad = 1;
+                else if (r < mn)
+                    mn = r;
             }
     }
+    if (bad) return ORC_ERR_STATE;
     *dt = c->cfg.cfl * mn;
     return ORC_OK;
 }
@@ -825,6 +848,7 @@ int orc_step(orc_ctx *c, int32_t nsteps)
         h[0] = dt;
         for (int32_t n = 0; n < c->nblocks; ++n) {
             orc_block *bk = &c->b[n];
+#pragma omp parallel for schedule(static)
             for (int32_t j = 0; j < bk->nj; ++j)
                 for (int32_t i = 0; i < bk->ni; ++i)
                     memcpy(bk->W + FR(bk, i, j), bk->Un + IN(bk, i, j), 4 * sizeof(double));
@@ -864,6 +888,7 @@ int orc_step(orc_ctx *c, int32_t nsteps)
             }
             for (int32_t n = 0; n < c->nblocks; ++n) {
                 orc_block *bk = &c->b[n];
+#pragma omp parallel for schedule(static)
                 for (int32_t j = 0; j < bk->nj; ++j)
                     for (int32_t i = 0; i < bk->ni; ++i) {
                         double V = bk->vol[(int64_t)j * bk->ni + i];

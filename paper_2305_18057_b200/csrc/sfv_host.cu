@@ -6,8 +6,12 @@
 #include <dlfcn.h>
 #include <nccl.h>
 
+#include <unistd.h>
+
 #include <algorithm>
+#include <chrono>
 #include <cmath>
+#include <deque>
 #include <cstdarg>
 #include <cstdio>
 #include <cstdlib>
@@ -37,6 +41,9 @@ struct Nccl {
     ncclResult_t (*GroupEnd)() = nullptr;
     ncclResult_t (*AllReduce)(const void *, void *, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
                               cudaStream_t) = nullptr;
+    ncclResult_t (*Broadcast)(const void *, void *, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*CommGetAsyncError)(ncclComm_t, ncclResult_t *) = nullptr;
+    ncclResult_t (*CommAbort)(ncclComm_t) = nullptr;
     const char *(*GetErrorString)(ncclResult_t) = nullptr;
 };
 
@@ -57,10 +64,13 @@ Nccl &nccl() {
     SFV_SYM(GroupStart);
     SFV_SYM(GroupEnd);
     SFV_SYM(AllReduce);
+    SFV_SYM(Broadcast);
+    SFV_SYM(CommGetAsyncError);
+    SFV_SYM(CommAbort);
     SFV_SYM(GetErrorString);
 #undef SFV_SYM
     n.ok = n.GetUniqueId && n.CommInitRank && n.CommDestroy && n.Send && n.Recv && n.GroupStart && n.GroupEnd &&
-           n.AllReduce && n.GetErrorString;
+           n.AllReduce && n.Broadcast && n.CommGetAsyncError && n.CommAbort && n.GetErrorString;
     return n;
 }
 
@@ -88,10 +98,11 @@ struct Block {
     int i0 = 0, i1 = 0, j0 = 0, j1 = 0, ni = 0, nj = 0, PJ = 0;
     int nbr[4] = {-1, -1, -1, -1};
     int edge[4] = {0, 0, 0, 0};  // Edge kind per W, E, S, N
-    int nstrips = 1, nseg = 1;
+    int nstrips = 1, nseg = 1, nsegF = 1;
     // launch plan of a stage: edge rows first (2 rows per connected i-cut,
     // exchanged while the interior runs), then the interior rows
     int nlaunch = 1, row_lo[3] = {0, 0, 0}, row_hi[3] = {0, 0, 0}, lseg[3] = {1, 1, 1}, lbase[3] = {0, 0, 0};
+    int lsegF[3] = {1, 1, 1};  // segments per launch part for the RK4 final stage (its own occupancy)
     int ncta_total = 1;
     bool split = false;
     double *buf[4] = {nullptr, nullptr, nullptr, nullptr};
@@ -142,6 +153,8 @@ StageSpec stage_spec(int rk, int k) {
 
 }  // namespace
 
+enum ProfClass { P_EDGE = 0, P_INTERIOR, P_XROW, P_XCOL, P_WAIT, P_DT, P_VISC, P_NORMS, NPROF };
+
 struct sfv_ctx {
     sfv_config cfg{};
     std::vector<double> X, Y;
@@ -161,7 +174,7 @@ struct sfv_ctx {
     unsigned long long *err = nullptr, *geo_bad = nullptr;
     double *dt_hist = nullptr, *norm_hist = nullptr, *gbuf = nullptr;
     size_t gbuf_elems = 0;
-    int nsm = 148, occ = 1;
+    int nsm = 148, occ = 1, occ_f = 1;  // resident stage-kernel CTAs per SM (RK4 final stage: occ_f)
     Params P{};
     long long steps_enq = 0;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
@@ -180,6 +193,25 @@ struct sfv_ctx {
     unsigned long long *sig_flag = nullptr;  // [SIG_RANKS_MAX]
     double **rtab = nullptr;                 // device array [nranks]
     unsigned long long **rflag = nullptr;    // device array [nranks]
+    // failure detection of the NCCL path (a missing neighbour
+    // message beyond a configurable timeout is a deadlock error naming the
+    // edge): one event per enqueued step marks progress; a synchronising call
+    // that sees no step complete for comm_timeout seconds (or an NCCL async
+    // error) aborts the communicator and returns SFV_ERR_NCCL
+    double comm_timeout = 60.0;
+    bool comm_dead = false;
+    std::deque<std::pair<cudaEvent_t, long long>> prog;  // (event, step index) in stream order
+    std::vector<cudaEvent_t> ev_pool;
+    // profiling mode (sfv_set_profiling): steps enqueued stage by stage with
+    // CUDA events around each class of work (edge / interior stage kernels,
+    // row exchange on the comm stream, column exchange, exposed wait for the
+    // comm stream, dt all-reduce, viscous kernels, norms batch)
+    bool prof = false;
+    struct Span { int cls; cudaEvent_t a, b; };
+    std::vector<Span> spans;
+    std::vector<cudaEvent_t> tev_pool;
+    double prof_ms[NPROF] = {0};
+    long long prof_steps = 0;
     std::string msg;
     long long einfo[4] = {-1, -1, -1, -1};
 };
@@ -267,9 +299,8 @@ void build_params(sfv_ctx *c) {
 
 // Launch geometry: strips of <= NT-4 columns (even starts), segments along i
 // so that strips*segments fills the device in whole waves.
-void choose_launch(sfv_ctx *c, Block &b) {
-    b.nstrips = (b.nj + WOUT - 1) / WOUT;
-    const int slots = c->nsm * std::max(1, c->occ) * WPC;  // resident warps
+int choose_nseg(const sfv_ctx *c, const Block &b, int occ) {
+    const int slots = c->nsm * std::max(1, occ) * WPC;  // resident warps
     // minimise (longest segment + prologue) x waves: a segment's time is its
     // row count plus ~1.5 rows of prologue / pipeline fill, and a launch lasts
     // as long as its longest segment in each wave
@@ -285,12 +316,21 @@ void choose_launch(sfv_ctx *c, Block &b) {
             best = s;
         }
     }
-    b.nseg = std::min(best, b.ni);
+    int nseg = std::min(best, b.ni);
     // experiment override: SFV_WAVES = w forces about w waves of warp tasks
     if (const char *ev = getenv("SFV_WAVES")) {
         const double w = atof(ev);
-        if (w > 0) b.nseg = std::max(1, std::min(cap, (int)std::lround(w * slots / b.nstrips)));
+        if (w > 0) nseg = std::max(1, std::min(cap, (int)std::lround(w * slots / b.nstrips)));
     }
+    return nseg;
+}
+// Launch geometry of a block: warp tasks = strips x segments, one segment
+// count per occupancy class (the RK4 final stage keeps fewer resident warps
+// than the other stage kernels)
+void choose_launch(sfv_ctx *c, Block &b) {
+    b.nstrips = (b.nj + WOUT - 1) / WOUT;
+    b.nseg = choose_nseg(c, b, c->occ);
+    b.nsegF = choose_nseg(c, b, c->occ_f);
 }
 
 // Stage launch plan of a block: with a connected i-cut and
@@ -306,15 +346,15 @@ void plan_launches(sfv_ctx *c, Block &b) {
     int n = 0;
     int lo = 0, hi = b.ni;
     if (b.split) {
-        if (cw) { b.row_lo[n] = 0; b.row_hi[n] = 2; b.lseg[n] = 1; ++n; lo = 2; }
-        if (ce) { b.row_lo[n] = b.ni - 2; b.row_hi[n] = b.ni; b.lseg[n] = 1; ++n; hi = b.ni - 2; }
+        if (cw) { b.row_lo[n] = 0; b.row_hi[n] = 2; b.lseg[n] = b.lsegF[n] = 1; ++n; lo = 2; }
+        if (ce) { b.row_lo[n] = b.ni - 2; b.row_hi[n] = b.ni; b.lseg[n] = b.lsegF[n] = 1; ++n; hi = b.ni - 2; }
         // interior: re-run the segment choice on the interior rows
         Block t = b;
         t.ni = hi - lo;
         choose_launch(c, t);
-        b.row_lo[n] = lo; b.row_hi[n] = hi; b.lseg[n] = t.nseg; ++n;
+        b.row_lo[n] = lo; b.row_hi[n] = hi; b.lseg[n] = t.nseg; b.lsegF[n] = t.nsegF; ++n;
     } else {
-        b.row_lo[0] = 0; b.row_hi[0] = b.ni; b.lseg[0] = b.nseg; n = 1;
+        b.row_lo[0] = 0; b.row_hi[0] = b.ni; b.lseg[0] = b.nseg; b.lsegF[0] = b.nsegF; n = 1;
     }
     b.nlaunch = n;
     int base = 0;
@@ -369,7 +409,13 @@ size_t layout(sfv_ctx *c, bool assign) {
     size_t o_dt = take(sizeof(double) * cap);
     size_t o_norm = take(sizeof(double) * (size_t)cap * c->nblocks_total * 8);
     size_t gb = 0;
-    if (c->nranks > 1) gb = std::max((size_t)c->cfg.ni * c->cfg.nj * 4, (size_t)c->nblocks_total * 8 * 4096);
+    if (c->nranks > 1) {  // get_state's per-block broadcast, get_residual_norms' chunked all-reduce
+        size_t big = 0;
+        for (int bx = 0; bx < c->px; ++bx)
+            for (int by = 0; by < c->py; ++by)
+                big = std::max(big, (size_t)(c->xs[bx + 1] - c->xs[bx]) * (c->ys[by + 1] - c->ys[by]) * 4);
+        gb = std::max(big, (size_t)c->nblocks_total * 8 * 4096);
+    }
     size_t o_g = take(sizeof(double) * gb);
     if (assign) {
         c->sig = reinterpret_cast<double *>(c->ws + o_misc);
@@ -716,6 +762,39 @@ sfv_status enqueue_norms(sfv_ctx *c, long long first, int count, cudaStream_t st
     return SFV_OK;
 }
 
+// Profiling spans (active only in profiling mode, never inside graph capture).
+int span_begin(sfv_ctx *c, int cls, cudaStream_t st) {
+    if (!c->prof) return -1;
+    auto get = [&]() {
+        cudaEvent_t e = nullptr;
+        if (!c->tev_pool.empty()) {
+            e = c->tev_pool.back();
+            c->tev_pool.pop_back();
+        } else if (cudaEventCreate(&e) != cudaSuccess) {
+            e = nullptr;
+        }
+        return e;
+    };
+    sfv_ctx::Span sp{cls, get(), get()};
+    if (!sp.a || !sp.b || cudaEventRecord(sp.a, st) != cudaSuccess) return -1;
+    c->spans.push_back(sp);
+    return (int)c->spans.size() - 1;
+}
+void span_end(sfv_ctx *c, int id, cudaStream_t st) {
+    if (id >= 0) cudaEventRecord(c->spans[id].b, st);
+}
+// after the stream has drained: accumulate and recycle
+void spans_collect(sfv_ctx *c) {
+    for (auto &sp : c->spans) {
+        float ms = 0.f;
+        if (cudaEventElapsedTime(&ms, sp.a, sp.b) == cudaSuccess) c->prof_ms[sp.cls] += ms;
+        c->tev_pool.push_back(sp.a);
+        c->tev_pool.push_back(sp.b);
+    }
+    c->spans.clear();
+    cudaGetLastError();
+}
+
 sfv_status enqueue_step(sfv_ctx *c, cudaStream_t st, bool norms_batch) {
     const int s = nstages_of(c->cfg.rk);
     const bool cflmode = !(c->cfg.dt_fixed > 0.0);
@@ -724,8 +803,10 @@ sfv_status enqueue_step(sfv_ctx *c, cudaStream_t st, bool norms_batch) {
     for (int k = 1; k <= s; ++k) {
         const StageSpec sp = stage_spec(c->cfg.rk, k);
         if (c->cfg.viscous) {
+            const int sv = span_begin(c, P_VISC, st);
             sfv_status r = enqueue_viscous(c, sp.in, st);
             if (r != SFV_OK) return r;
+            span_end(c, sv, st);
         }
         auto launch_part = [&](Block &b, int q) -> sfv_status {
             StageArgs a = make_args(c, b, k);
@@ -733,7 +814,7 @@ sfv_status enqueue_step(sfv_ctx *c, cudaStream_t st, bool norms_batch) {
             a.bump = (k == s && &b == &c->blocks.back() && q == b.nlaunch - 1) ? 1 : 0;
             a.row_lo = b.row_lo[q];
             a.row_hi = b.row_hi[q];
-            a.nseg = b.lseg[q];
+            a.nseg = sp.mode == M_RK4F ? b.lsegF[q] : b.lseg[q];
             a.part_base = b.lbase[q];
             for (int e = 0; e < 4; ++e) a.edge_writers[e] = a.peer_out[e] ? edge_writers(b, a.nseg, e) : 0;
             CK(launch_stage(a, sp.mode, k == 1, k == s && cflmode, c->halo == SFV_HALO_PEER, c->cfg.viscous != 0, st));
@@ -741,46 +822,164 @@ sfv_status enqueue_step(sfv_ctx *c, cudaStream_t st, bool norms_batch) {
         };
         if (any_split) {
             // edge rows -> [comm stream: row exchange] || interior rows -> join
+            const int se = span_begin(c, P_EDGE, st);
             for (Block &b : c->blocks)
                 for (int q = 0; q + 1 < b.nlaunch; ++q) {
                     sfv_status r = launch_part(b, q);
                     if (r != SFV_OK) return r;
                 }
+            span_end(c, se, st);
             CK(cudaEventRecord(c->ev_edge, st));
             CK(cudaStreamWaitEvent(c->comm_st, c->ev_edge, 0));
+            const int sx = span_begin(c, P_XROW, c->comm_st);
             sfv_status r = exchange_rows(c, sp.out, c->comm_st);
             if (r != SFV_OK) return r;
+            span_end(c, sx, c->comm_st);
             CK(cudaEventRecord(c->ev_comm, c->comm_st));
+            const int si = span_begin(c, P_INTERIOR, st);
             for (Block &b : c->blocks) {
                 r = launch_part(b, b.nlaunch - 1);
                 if (r != SFV_OK) return r;
             }
+            span_end(c, si, st);
         } else {
+            const int si = span_begin(c, P_INTERIOR, st);
             for (Block &b : c->blocks) {
                 sfv_status r = launch_part(b, 0);
                 if (r != SFV_OK) return r;
             }
+            span_end(c, si, st);
         }
         if (c->halo == SFV_HALO_PEER) continue;  // the stage kernels exchanged the halos
         if (any_split) {
+            const int sc = span_begin(c, P_XCOL, st);
             sfv_status r = exchange_cols(c, sp.out, st);
             if (r != SFV_OK) return r;
+            span_end(c, sc, st);
+            const int sw = span_begin(c, P_WAIT, st);  // compute stream idles until the rows arrived
             CK(cudaStreamWaitEvent(st, c->ev_comm, 0));
+            span_end(c, sw, st);
         } else {
+            const int sx = span_begin(c, P_XROW, st);
             sfv_status r = exchange(c, sp.out, st);
             if (r != SFV_OK) return r;
+            span_end(c, sx, st);
         }
     }
     // dt max across ranks: in the bump CTA through peer memory (peer mode), else NCCL
     const bool dev_dt = c->halo == SFV_HALO_PEER && c->sig_dev;
-    if (c->nranks > 1 && cflmode && !dev_dt)
+    if (c->nranks > 1 && cflmode && !dev_dt) {
+        const int sd = span_begin(c, P_DT, st);
         NK(nccl().AllReduce(c->sig, c->sig, 2, ncclDouble, ncclMax, c->comm, st));
-    if (norms_batch) return enqueue_norms(c, -1, c->pring, st);
+        span_end(c, sd, st);
+    }
+    if (norms_batch) {
+        const int sn = span_begin(c, P_NORMS, st);
+        sfv_status r = enqueue_norms(c, -1, c->pring, st);
+        span_end(c, sn, st);
+        return r;
+    }
     return SFV_OK;
 }
 
-sfv_status check_device_error(sfv_ctx *c) {
-    if (c->halo == SFV_HALO_PEER) {
+// Neighbours of this rank's block, for error messages ("W: rank 1, E: rank 3").
+std::string edge_names(const sfv_ctx *c) {
+    static const char *nm[4] = {"W", "E", "S", "N"};
+    std::string r;
+    if (c->blocks.empty()) return r;
+    for (int e = 0; e < 4; ++e)
+        if (c->blocks[0].nbr[e] >= 0) {
+            if (!r.empty()) r += ", ";
+            r += std::string(nm[e]) + " edge <-> rank " + std::to_string(c->blocks[0].nbr[e]);
+        }
+    return r.empty() ? std::string("no connected edge") : r;
+}
+
+// Wait for the bound stream.  With NCCL ranks (copy-mode halos, all-reduces)
+// the wait polls the stream, the per-step progress events and
+// ncclCommGetAsyncError: an async error, or no step completing within
+// comm_timeout seconds, aborts the communicator (unblocking the stream) and
+// returns SFV_ERR_NCCL naming this rank's edges and the pending step
+// instead of hanging.
+sfv_status wait_stream(sfv_ctx *c, const char *what) {
+    if (c->comm_dead) return fail(c, SFV_ERR_NCCL, "%s: the NCCL communicator was aborted by an earlier failure", what);
+    if (c->nranks <= 1 || !c->comm) {
+        CK(cudaStreamSynchronize(c->st));
+        for (auto &pe : c->prog) c->ev_pool.push_back(pe.first);
+        c->prog.clear();
+        if (!c->spans.empty()) {
+            CK(cudaStreamSynchronize(c->comm_st));
+            spans_collect(c);
+        }
+        return SFV_OK;
+    }
+    Nccl &N = nccl();
+    using clk = std::chrono::steady_clock;
+    auto last = clk::now();
+    for (;;) {
+        const cudaError_t q = cudaStreamQuery(c->st);
+        if (q == cudaSuccess) break;
+        if (q != cudaErrorNotReady) return fail(c, SFV_ERR_CUDA, "%s: %s", what, cudaGetErrorString(q));
+        bool moved = false;
+        while (!c->prog.empty() && cudaEventQuery(c->prog.front().first) == cudaSuccess) {
+            c->ev_pool.push_back(c->prog.front().first);
+            c->prog.pop_front();
+            moved = true;
+        }
+        if (moved) last = clk::now();
+        ncclResult_t ar = ncclSuccess;
+        N.CommGetAsyncError(c->comm, &ar);
+        const double idle = std::chrono::duration<double>(clk::now() - last).count();
+        if ((ar != ncclSuccess && ar != ncclInProgress) || idle > c->comm_timeout) {
+            const long long pend = c->prog.empty() ? -1 : c->prog.front().second;
+            N.CommAbort(c->comm);
+            c->comm = nullptr;
+            c->comm_dead = true;
+            c->have_state = false;
+            if (ar != ncclSuccess && ar != ncclInProgress)
+                return fail(c, SFV_ERR_NCCL, "%s: NCCL async error '%s' on rank %d (%s), step %lld; communicator aborted",
+                            what, N.GetErrorString(ar), c->rank, edge_names(c).c_str(), pend);
+            return fail(c, SFV_ERR_NCCL,
+                        "%s: deadlock: no progress for %.1f s on rank %d -- halo exchange / all-reduce with (%s) "
+                        "pending at step %lld; communicator aborted",
+                        what, c->comm_timeout, c->rank, edge_names(c).c_str(), pend);
+        }
+        usleep(200);
+    }
+    for (auto &pe : c->prog) c->ev_pool.push_back(pe.first);
+    c->prog.clear();
+    if (!c->spans.empty()) {
+        CK(cudaStreamSynchronize(c->comm_st));  // (joined into st: complete)
+        spans_collect(c);
+    }
+    return SFV_OK;
+}
+#define SYNC(what)                                \
+    do {                                          \
+        sfv_status s_ = wait_stream(c, (what));   \
+        if (s_ != SFV_OK) return s_;              \
+    } while (0)
+
+// With NCCL ranks every rank must take the same branch before a collective
+// (an error one rank sees must not leave the others blocked in the next
+// all-reduce): the sticky words are agreed over ranks -- the smallest error
+// key (the global first failure: keys carry global cell indices) and the
+// max of the halo-timeout flag.
+sfv_status agree_errors(sfv_ctx *c) {
+    if (c->nranks <= 1 || !c->comm) return SFV_OK;
+    Nccl &N = nccl();
+    NK(N.AllReduce(c->err, c->err, 1, ncclUint64, ncclMin, c->comm, c->st));
+    NK(N.AllReduce(c->halo_err, c->halo_err, 1, ncclUint32, ncclMax, c->comm, c->st));
+    SYNC("error agreement");
+    return SFV_OK;
+}
+
+sfv_status check_device_error(sfv_ctx *c, bool collective = false) {
+    if (collective) {
+        sfv_status a = agree_errors(c);
+        if (a != SFV_OK) return a;
+    }
+    if (c->halo == SFV_HALO_PEER || collective) {
         unsigned h = 0;
         CK(cudaMemcpy(&h, c->halo_err, sizeof h, cudaMemcpyDeviceToHost));
         if (h) {
@@ -950,6 +1149,8 @@ sfv_status sfv_bind(sfv_ctx *c, void *ws, size_t bytes, void *stream) {
     CK(prepare_stage_kernels());
     CK(stage_occupancy(M_UN, false, false, fast_path(c->P), false, &o));
     c->occ = std::max(1, o);
+    CK(stage_occupancy(M_RK4F, false, true, fast_path(c->P), false, &o));
+    c->occ_f = std::max(1, o);
     CK(cudaEventCreate(&c->ev0));
     CK(cudaEventCreate(&c->ev1));
     CK(cudaEventCreateWithFlags(&c->ev_edge, cudaEventDisableTiming));
@@ -1024,7 +1225,11 @@ sfv_status sfv_set_state(sfv_ctx *c, const double *U) {
     CK(cudaMemsetAsync(c->done, 0, sizeof(unsigned), st));
     CK(cudaMemsetAsync(c->dt_hist, 0, sizeof(double) * c->cfg.max_history, st));
     CK(cudaMemsetAsync(c->norm_hist, 0, sizeof(double) * c->cfg.max_history * c->nblocks_total * 8, st));
-    CK(cudaStreamSynchronize(st));
+    SYNC("sfv_set_state");
+    {  // every rank branches on the same (global) first invalid cell
+        sfv_status ag = agree_errors(c);
+        if (ag != SFV_OK) return ag;
+    }
     unsigned long long e = ~0ull;
     CK(cudaMemcpy(&e, c->err, 8, cudaMemcpyDeviceToHost));
     if (e != ~0ull) {
@@ -1039,7 +1244,7 @@ sfv_status sfv_set_state(sfv_ctx *c, const double *U) {
     if (c->halo == SFV_HALO_PEER && c->sig_dev)  // every rank's slot 0 = the global sigma_0 (flags = 0)
         for (int r = 0; r < c->nranks; ++r)
             CK(cudaMemcpyAsync(c->sig_tab + r, c->sig, sizeof(double), cudaMemcpyDeviceToDevice, st));
-    CK(cudaStreamSynchronize(st));
+    SYNC("sfv_set_state");
     c->steps_enq = 0;
     c->have_state = true;
     c->timing_open = false;
@@ -1083,24 +1288,38 @@ sfv_status sfv_step(sfv_ctx *c, int32_t nsteps) {
         CK(cudaEventRecord(c->ev0, c->st));
         c->timing_open = true;
     }
+    if (c->comm_dead) return fail(c, SFV_ERR_NCCL, "the NCCL communicator was aborted by an earlier failure");
+    const bool track = c->nranks > 1 && c->comm;  // progress events for the deadlock timeout
     for (int s = 0; s < nsteps; ++s) {
         const bool batch = (c->steps_enq + s + 1) % c->pring == 0;
-        if (c->gexec) {
+        if (c->gexec && !c->prof) {
             CK(cudaGraphLaunch(batch ? c->gexec_norms : c->gexec, c->st));
         } else {
             sfv_status r = enqueue_step(c, c->st, batch);
             if (r != SFV_OK) return r;
         }
+        if (track) {
+            cudaEvent_t ev = nullptr;
+            if (!c->ev_pool.empty()) {
+                ev = c->ev_pool.back();
+                c->ev_pool.pop_back();
+            } else {
+                CK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+            }
+            CK(cudaEventRecord(ev, c->st));
+            c->prog.emplace_back(ev, c->steps_enq + s);
+        }
     }
     CK(cudaEventRecord(c->ev1, c->st));
     c->steps_enq += nsteps;
+    if (c->prof) c->prof_steps += nsteps;
     return SFV_OK;
 }
 
 sfv_status sfv_sync(sfv_ctx *c, double *ms) {
     if (!c) return SFV_ERR_ARG;
     if (!c->bound) return fail(c, SFV_ERR_SEQUENCE, "not bound");
-    CK(cudaStreamSynchronize(c->st));
+    SYNC("sfv_sync");
     if (ms) *ms = 0.0;
     if (c->timing_open) {
         float f = 0.f;
@@ -1114,7 +1333,7 @@ sfv_status sfv_sync(sfv_ctx *c, double *ms) {
 sfv_status sfv_steps_done(sfv_ctx *c, int64_t *out) {
     if (!c || !out) return SFV_ERR_ARG;
     if (!c->bound) return fail(c, SFV_ERR_SEQUENCE, "not bound");
-    CK(cudaStreamSynchronize(c->st));
+    SYNC("sfv_steps_done");
     long long n = 0;
     CK(cudaMemcpy(&n, c->step_ctr, 8, cudaMemcpyDeviceToHost));
     *out = n;
@@ -1135,13 +1354,13 @@ sfv_status sfv_get_residual_norms(sfv_ctx *c, int64_t first, int64_t count, doub
     long long done = 0;
     sfv_status s = hist_range(c, first, count, &done);
     if (s != SFV_OK) return s;
-    s = check_device_error(c);
+    s = check_device_error(c, true);  // collective: every rank takes the same path
     if (s != SFV_OK) return s;
     // steps after the last batched reduction: reduce them now (idempotent)
     if (done % c->pring) {
         s = enqueue_norms(c, done - done % c->pring, (int)(done % c->pring), c->st);
         if (s != SFV_OK) return s;
-        CK(cudaStreamSynchronize(c->st));
+        SYNC("sfv_get_residual_norms");
     }
     const int nb = c->nblocks_total;
     const long long cap = c->cfg.max_history;
@@ -1161,7 +1380,7 @@ sfv_status sfv_get_residual_norms(sfv_ctx *c, int64_t first, int64_t count, doub
             CK(cudaMemcpy(c->gbuf, h.data() + (size_t)q0 * nb * 8, sizeof(double) * m * nb * 8,
                           cudaMemcpyHostToDevice));
             NK(nccl().AllReduce(c->gbuf, c->gbuf, (size_t)m * nb * 8, ncclDouble, ncclSum, c->comm, c->st));
-            CK(cudaStreamSynchronize(c->st));
+            SYNC("sfv_get_residual_norms");
             CK(cudaMemcpy(h.data() + (size_t)q0 * nb * 8, c->gbuf, sizeof(double) * m * nb * 8,
                           cudaMemcpyDeviceToHost));
         }
@@ -1200,8 +1419,8 @@ sfv_status sfv_get_dt(sfv_ctx *c, int64_t first, int64_t count, double *out) {
 sfv_status sfv_get_state(sfv_ctx *c, double *U) {
     if (!c || !U) return SFV_ERR_ARG;
     if (!c->have_state) return fail(c, SFV_ERR_SEQUENCE, "no state");
-    CK(cudaStreamSynchronize(c->st));
-    sfv_status s = check_device_error(c);
+    SYNC("sfv_get_state");
+    sfv_status s = check_device_error(c, true);  // collective: every rank takes the same path
     if (s != SFV_OK) return s;
     const int NI = c->cfg.ni;
     if (c->nranks == 1) {
@@ -1213,14 +1432,20 @@ sfv_status sfv_get_state(sfv_ctx *c, double *U) {
         CK(cudaStreamSynchronize(c->st));
         return SFV_OK;
     }
+    // all-gather, one block at a time: rank r broadcasts its block (packed
+    // [j][i][4]) into gbuf, which is sized for the largest block, and every
+    // rank copies it into place in U (no full-grid device buffer)
     Block &b = c->blocks[0];
-    CK(cudaMemsetAsync(c->gbuf, 0, sizeof(double) * (size_t)c->cfg.ni * c->cfg.nj * 4, c->st));
     CK(launch_gather(b.buf[0], b.stage, b.ni, b.nj, b.PJ, c->st));
-    CK(cudaMemcpy2DAsync(c->gbuf + ((size_t)b.j0 * NI + b.i0) * 4, (size_t)NI * 32, b.stage, (size_t)b.ni * 32,
-                         (size_t)b.ni * 32, b.nj, cudaMemcpyDeviceToDevice, c->st));
-    NK(nccl().AllReduce(c->gbuf, c->gbuf, (size_t)c->cfg.ni * c->cfg.nj * 4, ncclDouble, ncclSum, c->comm, c->st));
-    CK(cudaMemcpyAsync(U, c->gbuf, sizeof(double) * (size_t)c->cfg.ni * c->cfg.nj * 4, cudaMemcpyDeviceToHost, c->st));
-    CK(cudaStreamSynchronize(c->st));
+    for (int r = 0; r < c->nranks; ++r) {
+        const int bx = r % c->px, by = r / c->px;
+        const int i0 = c->xs[bx], ni = c->xs[bx + 1] - i0, j0 = c->ys[by], nj = c->ys[by + 1] - j0;
+        const size_t n = (size_t)ni * nj * 4;
+        NK(nccl().Broadcast(r == c->rank ? b.stage : c->gbuf, c->gbuf, n, ncclDouble, r, c->comm, c->st));
+        CK(cudaMemcpy2DAsync(U + ((size_t)j0 * NI + i0) * 4, (size_t)NI * 32, c->gbuf, (size_t)ni * 32,
+                             (size_t)ni * 32, nj, cudaMemcpyDeviceToHost, c->st));
+        SYNC("sfv_get_state");  // gbuf is reused by the next block
+    }
     return SFV_OK;
 }
 
@@ -1441,10 +1666,46 @@ sfv_status sfv_debug_block_buffer(sfv_ctx *c, int32_t block, int32_t k, double *
     return SFV_OK;
 }
 
+sfv_status sfv_set_profiling(sfv_ctx *c, int32_t on) {
+    if (!c) return SFV_ERR_ARG;
+    if (!c->bound) return fail(c, SFV_ERR_SEQUENCE, "sfv_set_profiling before sfv_bind");
+    SYNC("sfv_set_profiling");
+    c->prof = on != 0;
+    for (double &v : c->prof_ms) v = 0.0;
+    c->prof_steps = 0;
+    return SFV_OK;
+}
+
+sfv_status sfv_get_stage_timings(sfv_ctx *c, double *out) {
+    if (!c || !out) return SFV_ERR_ARG;
+    if (!c->bound) return fail(c, SFV_ERR_SEQUENCE, "not bound");
+    SYNC("sfv_get_stage_timings");
+    for (int k = 0; k < NPROF; ++k) out[k] = c->prof_ms[k];
+    out[NPROF] = (double)c->prof_steps;
+    return SFV_OK;
+}
+
+sfv_status sfv_set_comm_timeout(sfv_ctx *c, double seconds) {
+    if (!c || !(seconds > 0.0)) return SFV_ERR_ARG;
+    c->comm_timeout = seconds;
+    return SFV_OK;
+}
+
 const char *sfv_last_error(const sfv_ctx *c) { return c ? c->msg.c_str() : "null ctx"; }
 
 void sfv_destroy(sfv_ctx *c) {
     if (!c) return;
+    if (c->bound) {
+        // peer mode across ranks: neighbours store into this workspace; a
+        // barrier (all-reduce) before anyone releases it, then drain the stream
+        if (c->halo == SFV_HALO_PEER && c->nranks > 1 && c->comm && !c->comm_dead)
+            nccl().AllReduce(c->sig, c->sig, 1, ncclDouble, ncclMax, c->comm, c->st);
+        if (wait_stream(c, "sfv_destroy") != SFV_OK) cudaGetLastError();
+    }
+    for (auto &pe : c->prog) cudaEventDestroy(pe.first);
+    for (cudaEvent_t e : c->ev_pool) cudaEventDestroy(e);
+    for (auto &sp : c->spans) { cudaEventDestroy(sp.a); cudaEventDestroy(sp.b); }
+    for (cudaEvent_t e : c->tev_pool) cudaEventDestroy(e);
     if (c->gexec) cudaGraphExecDestroy(c->gexec);
     if (c->gexec_norms) cudaGraphExecDestroy(c->gexec_norms);
     if (c->ev0) cudaEventDestroy(c->ev0);

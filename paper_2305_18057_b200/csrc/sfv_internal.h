@@ -21,7 +21,10 @@ constexpr int JOFF = 4;
 constexpr int NMET = 7;
 constexpr int SMEM_ROW = 132;     // doubles per staged row in shared memory
 constexpr int ROW_COLS = 130;     // columns staged per row: j0-2 .. j0+127
-constexpr int NT = 32;            // threads per CTA of the stage kernel: one independent warp
+#ifndef SFV_NT
+#define SFV_NT 32
+#endif
+constexpr int NT = SFV_NT;        // threads per CTA of the stage kernel (independent warps)
 constexpr int WPC = NT / 32;      // independent warps per CTA
 #ifndef SFV_CPL
 #define SFV_CPL 1                 // columns per lane of the stage kernel
@@ -146,6 +149,7 @@ cudaError_t launch_visc(const ViscArgs &v, cudaStream_t st);
 cudaError_t launch_gradvisc(const ViscArgs &v, cudaStream_t st);  // blocks without connected edges
 cudaError_t launch_norms(const NormsArgs &f, cudaStream_t st);
 cudaError_t stage_occupancy(int mode, bool norms, bool dtmax, bool fast, bool peer, int *ctas_per_sm);
+cudaError_t stage_occupancy_visc(int mode, bool norms, bool dtmax, bool fast, int *ctas_per_sm);
 bool fast_path(const Params &P);
 cudaError_t prepare_stage_kernels();
 size_t stage_smem_bytes(int mode);

@@ -301,6 +301,9 @@ __device__ __forceinline__ void store4(double *buf, int PJ, int i, int j, const 
 // and mbarriers.  j-face states / fluxes move between lanes by __shfl, so the
 // main loop has no CTA-wide barrier; warps drift independently.
 
+#ifndef SFV_MIN_WARPS
+#define SFV_MIN_WARPS (CPL == 1 ? 12 : 8)  // resident warps per SM the register allocation targets (no spills)
+#endif
 #ifndef SFV_DEEP_MASK
 // rings with 2 rows in flight instead of 1 (bit 0: stencil, 1: metrics, 2:
 // pointwise).  Measured on C2 / C3 (profiles/r1_ab_ring_depth.txt): pointwise
@@ -308,21 +311,38 @@ __device__ __forceinline__ void store4(double *buf, int PJ, int i, int j, const 
 // -1.3%, metrics+pointwise -8.6% (C2)
 #define SFV_DEEP_MASK 4
 #endif
+#ifndef SFV_PARK
+#define SFV_PARK 0  // park the row-carried values in shared memory (fewer registers, more resident warps)
+#endif
+#ifndef SFV_XSHFL
+#define SFV_XSHFL 0  // lane exchange of j-face states / fluxes by shuffles instead of shared memory
+#endif
+#ifndef SFV_PARK_WARPS
+#define SFV_PARK_WARPS 14  // resident warps per SM targeted by the parked variants
+#endif
 template <int MODE>
 struct StageTraits {
     static constexpr int NPW = (MODE == M_OWN || MODE == M_RES) ? 0 : (MODE == M_RK4F ? 3 : 1);
+    // parked variants: the i-direction values carried from row to row (the
+    // cell's last upper-face state, its forward difference, its west-face
+    // flux) and the stage-1 norm accumulators live in a per-lane shared-memory
+    // slot instead of registers across the two Roe evaluations
+    static constexpr bool PARK = SFV_PARK && MODE != M_RK4F;
+    static constexpr int PK_PER_COL = 12 + (MODE == M_OWN ? 8 : 0);  // QL[4] fp[4] GW[4] (+ nrm[8])
+    static constexpr int K_SLOT = PARK ? CPL * PK_PER_COL * 32 : 0;
+    static constexpr int MINW = PARK ? SFV_PARK_WARPS : SFV_MIN_WARPS;
     // the RK4 final stage (3 pointwise inputs) keeps 1 row in flight per ring
     // (12 CTAs/SM fit in 228 KB only so)
     static constexpr bool DEEP = MODE != M_RK4F;
     static constexpr int WS = DEEP && (SFV_DEEP_MASK & 1) ? 5 : 4;  // stencil ring: rows v..v+2 resident + (WS-3) in flight
     static constexpr int MS = DEEP && (SFV_DEEP_MASK & 2) ? 3 : 2;  // metrics ring: row v + (MS-1) in flight
-    static constexpr int PS = DEEP && (SFV_DEEP_MASK & 4) ? 3 : 2;  // pointwise ring: row v + (PS-1) in flight
+    static constexpr int PS = DEEP && (SFV_DEEP_MASK & 4) && !(PARK && SFV_PARK_WARPS > 12) ? 3 : 2;  // pointwise ring: row v + (PS-1) in flight
     static constexpr int W_SLOT = 4 * WROW;           // 1152 B
     static constexpr int M_SLOT = (NMET * WROW + 15) / 16 * 16;  // 128 B aligned
     static constexpr int P_SLOT = 4 * NPW * WROW;
-    static constexpr int X_SLOT = 8 * 32;             // lane exchange: north states [4][32], south fluxes [4][32]
+    static constexpr int X_SLOT = SFV_XSHFL ? 0 : 8 * 32;  // lane exchange: north states [4][32], south fluxes [4][32]
     static constexpr int NBAR = WS + MS + PS;
-    static constexpr int WARP_DBL = WS * W_SLOT + MS * M_SLOT + PS * P_SLOT + X_SLOT + 16;  // + <= 16 mbarriers
+    static constexpr int WARP_DBL = WS * W_SLOT + MS * M_SLOT + PS * P_SLOT + X_SLOT + 16 + K_SLOT;  // + <= 16 mbarriers
 };
 
 template <int MODE>
@@ -330,10 +350,6 @@ __host__ __device__ constexpr size_t stage_smem() {
     return sizeof(double) * ((size_t)WPC * StageTraits<MODE>::WARP_DBL + 8 * (NT / 32));
 }
 
-#ifndef SFV_MIN_WARPS
-#define SFV_MIN_WARPS (CPL == 1 ? 12 : 8)  // resident warps per SM the register allocation targets (no spills)
-#endif
-constexpr int SFV_MINB = SFV_MIN_WARPS / WPC;
 #ifndef SFV_UNROLL
 #define SFV_UNROLL 1  // row-loop unroll: lets ptxas rename the carried window instead of moving it
 #endif
@@ -341,7 +357,7 @@ constexpr int kRowUnroll = SFV_UNROLL;
 
 
 template <int MODE, bool NORMS, bool DTMAX, bool FAST, bool PEER, bool VISC>
-__global__ void __launch_bounds__(NT, SFV_MINB) stage_kernel(const __grid_constant__ StageArgs a) {
+__global__ void __launch_bounds__(NT, StageTraits<MODE>::MINW / WPC) stage_kernel(const __grid_constant__ StageArgs a) {
     using TR = StageTraits<MODE>;
     extern __shared__ __align__(128) double smem[];
     const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
@@ -353,6 +369,7 @@ __global__ void __launch_bounds__(NT, SFV_MINB) stage_kernel(const __grid_consta
     uint64_t *wbar = reinterpret_cast<uint64_t *>(xch + TR::X_SLOT);   // [WS]
     uint64_t *mbar = wbar + TR::WS;                                      // [MS]
     uint64_t *pbar = mbar + TR::MS;                                      // [PS]
+    double *park = xch + TR::X_SLOT + 16;       // [CPL][PK_PER_COL][32] parked row-carried values
     double *red = smem + WPC * TR::WARP_DBL;    // [8][WPC]
 
     const Params &P = a.P;
@@ -439,6 +456,7 @@ __global__ void __launch_bounds__(NT, SFV_MINB) stage_kernel(const __grid_consta
         constexpr unsigned ROWB = WROW * 8u;
 
         auto wslot = [&](int r) -> const double * { return wring + ((unsigned)(r - r0) % TR::WS) * TR::W_SLOT; };
+        auto pk = [&](int k, int q) { return (k * TR::PK_PER_COL + q) * 32 + lane; };  // parked value q of column k
         auto mslot = [&](int r) -> const double * { return mring + ((unsigned)(r - m0) % TR::MS) * TR::M_SLOT; };
         // one 2D TMA box per ring row (36 columns x 4 / 7 rows), issued by the
         // whole warp through elect.sync (operands are warp-uniform: 1 warp/CTA);
@@ -546,6 +564,18 @@ __global__ void __launch_bounds__(NT, SFV_MINB) stage_kernel(const __grid_consta
                 wfx[k] = nx; wfy[k] = ny; wfA[k] = A;
 #pragma unroll
                 for (int c = 0; c < 4; ++c) QLp[k][c] = qU[c];
+                if constexpr (TR::PARK) {
+#pragma unroll
+                    for (int c = 0; c < 4; ++c) {
+                        park[pk(k, c)] = QLp[k][c];
+                        park[pk(k, 4 + c)] = fp[k][c];
+                        park[pk(k, 8 + c)] = GW[k][c];
+                    }
+                    if constexpr (NORMS) {
+#pragma unroll
+                        for (int q = 0; q < 8; ++q) park[pk(k, 12 + q)] = 0.0;
+                    }
+                }
             }
         }
 
@@ -585,6 +615,19 @@ __global__ void __launch_bounds__(NT, SFV_MINB) stage_kernel(const __grid_consta
                 }
 #endif
             }
+            if constexpr (TR::PARK) {
+                // the row-carried values come back from the lane's parked slot;
+                // W(v+1) from the stencil ring (row v+1 is resident)
+                const double *s1 = wslot(v + 1);
+#pragma unroll
+                for (int k = 0; k < CPL; ++k)
+#pragma unroll
+                    for (int c = 0; c < 4; ++c) {
+                        fp[k][c] = park[pk(k, 4 + c)];
+                        QLp[k][c] = park[pk(k, c)];
+                        Wc[k][c] = s1[c * WROW + own + k];
+                    }
+            }
             wait_w(v + 2);
             double qD[CPL][4], qU[CPL][4], qS[CPL][4], qN[CPL][4], Wv[CPL][4];
             {
@@ -599,6 +642,10 @@ __global__ void __launch_bounds__(NT, SFV_MINB) stage_kernel(const __grid_consta
                         muscl_cell<FAST>(Wc[k][c], fp[k][c], f, P, qU[k][c], qD[k][c]);
                         fp[k][c] = f;
                         Wc[k][c] = wn;
+                        if constexpr (TR::PARK) {
+                            park[pk(k, c)] = qU[k][c];  // (this row's QLp was loaded above)
+                            park[pk(k, 4 + c)] = f;
+                        }
                     }
                 double qNup[CPL][4];
 #pragma unroll
@@ -614,7 +661,10 @@ __global__ void __launch_bounds__(NT, SFV_MINB) stage_kernel(const __grid_consta
                     }
 #pragma unroll
                 for (int c = 0; c < 4; ++c) {
-                    xch[c * 32 + lane] = qNup[CPL - 1][c];  // north state of the last column, read by the lane above
+                    if constexpr (SFV_XSHFL)  // lane 0 keeps its own value (as the shared-memory form)
+                        qN[0][c] = __shfl_up_sync(0xffffffffu, qNup[CPL - 1][c], 1);
+                    else
+                        xch[c * 32 + lane] = qNup[CPL - 1][c];  // north state of the last column, read by the lane above
 #pragma unroll
                     for (int k = 1; k < CPL; ++k) qN[k][c] = qNup[k - 1][c];
                 }
@@ -626,8 +676,10 @@ __global__ void __launch_bounds__(NT, SFV_MINB) stage_kernel(const __grid_consta
             if (v + TR::PS - 1 < i_end) issue_p(v + TR::PS - 1);
             wait_m(v);
             const double *mv = mslot(v);
+            if constexpr (!SFV_XSHFL) {
 #pragma unroll
-            for (int c = 0; c < 4; ++c) qN[0][c] = xch[c * 32 + (lane > 0 ? lane - 1 : 0)];
+                for (int c = 0; c < 4; ++c) qN[0][c] = xch[c * 32 + (lane > 0 ? lane - 1 : 0)];
+            }
             double GE[CPL][4], GS[CPL][4];
             bool okE[CPL], okS[CPL];
             // all face fluxes of this row: 2 x CPL independent Roe evaluations
@@ -642,13 +694,18 @@ __global__ void __launch_bounds__(NT, SFV_MINB) stage_kernel(const __grid_consta
             for (int c = 0; c < 4; ++c) {
 #pragma unroll
                 for (int k = 0; k < CPL; ++k) QLp[k][c] = qU[k][c];
-                xch[(4 + c) * 32 + lane] = GS[0][c];  // south flux of column 0 = north flux of the lane below
+                if constexpr (SFV_XSHFL)
+                    GN[CPL - 1][c] = __shfl_down_sync(0xffffffffu, GS[0][c], 1);  // lane 31 keeps its own
+                else
+                    xch[(4 + c) * 32 + lane] = GS[0][c];  // south flux of column 0 = north flux of the lane below
 #pragma unroll
                 for (int k = 0; k + 1 < CPL; ++k) GN[k][c] = GS[k + 1][c];
             }
             __syncwarp();
+            if constexpr (!SFV_XSHFL) {
 #pragma unroll
-            for (int c = 0; c < 4; ++c) GN[CPL - 1][c] = xch[(4 + c) * 32 + (lane < 31 ? lane + 1 : 31)];
+                for (int c = 0; c < 4; ++c) GN[CPL - 1][c] = xch[(4 + c) * 32 + (lane < 31 ? lane + 1 : 31)];
+            }
             const double *prow = pring + ((unsigned)(v - i_start) % TR::PS) * TR::P_SLOT;
             if constexpr (TR::NPW > 0)
                 mbar_wait_s(pbar_s + 8u * ((unsigned)(v - i_start) % TR::PS), ((unsigned)(v - i_start) / TR::PS) & 1u);
@@ -659,6 +716,14 @@ __global__ void __launch_bounds__(NT, SFV_MINB) stage_kernel(const __grid_consta
                 // ---- residual (Eq. 5) and stage update (Eq. 6): every lane computes,
                 // output lanes store (no divergence in the common path)
                 const double iV = mv[6 * WROW + o];
+                if constexpr (TR::PARK) {
+                    const double *svr = wslot(v);  // row v is still resident
+#pragma unroll
+                    for (int c = 0; c < 4; ++c) {
+                        GW[k][c] = park[pk(k, 8 + c)];
+                        Wv[k][c] = svr[c * WROW + o];
+                    }
+                }
                 double R[4], U[4];
 #pragma unroll
                 for (int c = 0; c < 4; ++c) R[c] = ((GE[k][c] - GW[k][c]) + GN[k][c]) - GS[k][c];
@@ -724,7 +789,10 @@ __global__ void __launch_bounds__(NT, SFV_MINB) stage_kernel(const __grid_consta
                     }
                     if (a.bc[0] == E_SLIP && v <= 1) {  // segments start at 0 or >= 4 (choose_launch)
                         double g[4];
-                        mirror(U, nWx[k], nWy[k], g);
+                        if constexpr (TR::PARK)  // i-face(0) normal: metrics row 0 (rare path)
+                            mirror(U, a.met[(size_t)0 * PJ + jk + JOFF], a.met[(size_t)1 * PJ + jk + JOFF], g);
+                        else
+                            mirror(U, nWx[k], nWy[k], g);
                         store4(a.out, PJ, -1 - v, jk, g);
                     } else if (a.bc[0] == E_OUTFLOW && v == 0) {
                         store4(a.out, PJ, -1, jk, U);
@@ -755,10 +823,19 @@ __global__ void __launch_bounds__(NT, SFV_MINB) stage_kernel(const __grid_consta
                     if (pcol & (2u << (2 * k))) store4(a.peer_out[3], a.peer_PJ[3], v, jk - a.nj, U);
                 }
                 if constexpr (NORMS) {
+                    if constexpr (TR::PARK) {
 #pragma unroll
-                    for (int c = 0; c < 4; ++c) {
-                        nrm[c] = is_out[k] ? fma(R[c], R[c], nrm[c]) : nrm[c];
-                        nrm[4 + c] = is_out[k] ? fmax(nrm[4 + c], fabs(R[c])) : nrm[4 + c];
+                        for (int c = 0; c < 4; ++c) {
+                            const double s2 = park[pk(k, 12 + c)], mx = park[pk(k, 16 + c)];
+                            park[pk(k, 12 + c)] = is_out[k] ? fma(R[c], R[c], s2) : s2;
+                            park[pk(k, 16 + c)] = is_out[k] ? fmax(mx, fabs(R[c])) : mx;
+                        }
+                    } else {
+#pragma unroll
+                        for (int c = 0; c < 4; ++c) {
+                            nrm[c] = is_out[k] ? fma(R[c], R[c], nrm[c]) : nrm[c];
+                            nrm[4 + c] = is_out[k] ? fmax(nrm[4 + c], fabs(R[c])) : nrm[4 + c];
+                        }
                     }
                 }
                 if constexpr (DTMAX) {
@@ -788,7 +865,10 @@ __global__ void __launch_bounds__(NT, SFV_MINB) stage_kernel(const __grid_consta
                     wfA[k] = mv[2 * WROW + o];
                 }
 #pragma unroll
-                for (int c = 0; c < 4; ++c) GW[k][c] = GE[k][c];
+                for (int c = 0; c < 4; ++c) {
+                    GW[k][c] = GE[k][c];
+                    if constexpr (TR::PARK) park[pk(k, 8 + c)] = GE[k][c];
+                }
             }
             outp += (size_t)4 * PJ;
             // rare path behind one warp vote: invalid face or new states (reading A-R28)
@@ -816,6 +896,15 @@ __global__ void __launch_bounds__(NT, SFV_MINB) stage_kernel(const __grid_consta
                     }
                 }
             }
+        }
+        if constexpr (TR::PARK && NORMS) {
+#pragma unroll
+            for (int k = 0; k < CPL; ++k)
+#pragma unroll
+                for (int c = 0; c < 4; ++c) {
+                    nrm[c] += park[pk(k, 12 + c)];
+                    nrm[4 + c] = fmax(nrm[4 + c], park[pk(k, 16 + c)]);
+                }
         }
         if constexpr (PEER) {
             // arrival of this task on every peer edge it touches; the last of
@@ -1032,7 +1121,7 @@ cudaError_t stage_occupancy(int mode, bool norms, bool dtmax, bool fast, bool pe
     const bool visc = false;
     SFV_DISPATCH(occ_t, n)
 }
-static cudaError_t stage_occupancy_v(int mode, bool norms, bool dtmax, bool fast, int *n) {
+cudaError_t stage_occupancy_visc(int mode, bool norms, bool dtmax, bool fast, int *n) {
     const bool peer = false, visc = true;
     SFV_DISPATCH(occ_t, n)
 }
@@ -1043,7 +1132,7 @@ cudaError_t prepare_stage_kernels() {
         for (int f = 0; f < 6; ++f) {
             int n = 0;
             cudaError_t e = f < 4 ? stage_occupancy(v[0], v[1] != 0, v[2] != 0, (f & 1) != 0, (f & 2) != 0, &n)
-                                  : stage_occupancy_v(v[0], v[1] != 0, v[2] != 0, (f & 1) != 0, &n);
+                                  : stage_occupancy_visc(v[0], v[1] != 0, v[2] != 0, (f & 1) != 0, &n);
             if (e != cudaSuccess) return e;
         }
     return cudaSuccess;

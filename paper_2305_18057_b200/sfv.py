@@ -27,8 +27,8 @@ ABI_SYMBOLS = ["sfv_create", "sfv_partition", "sfv_nccl_unique_id", "sfv_partiti
                "sfv_workspace_size", "sfv_bind", "sfv_set_state", "sfv_step", "sfv_sync", "sfv_steps_done",
                "sfv_get_residual_norms", "sfv_get_dt", "sfv_get_state", "sfv_error_info", "sfv_launch_info",
                "sfv_debug_math", "sfv_set_halo_mode", "sfv_peer_handle", "sfv_peer_connect",
-               "sfv_debug_block_buffer", "sfv_residual",
-               "sfv_last_error", "sfv_destroy"]
+               "sfv_debug_block_buffer", "sfv_residual", "sfv_set_profiling", "sfv_get_stage_timings",
+               "sfv_set_comm_timeout", "sfv_last_error", "sfv_destroy"]
 
 
 class SfvError(RuntimeError):
@@ -86,6 +86,9 @@ def lib():
         L.sfv_peer_connect.argtypes = [_VP, _VP]
         L.sfv_debug_block_buffer.argtypes = [_VP, C.c_int32, C.c_int32, _D]
         L.sfv_residual.argtypes = [_VP, _D, _D]
+        L.sfv_set_profiling.argtypes = [_VP, C.c_int32]
+        L.sfv_get_stage_timings.argtypes = [_VP, _D]
+        L.sfv_set_comm_timeout.argtypes = [_VP, C.c_double]
         L.sfv_last_error.argtypes = [_VP]
         L.sfv_last_error.restype = C.c_char_p
         L.sfv_destroy.argtypes = [_VP]
@@ -188,9 +191,12 @@ class Solver:
         dev = torch.device("cuda", self.device)
         n = C.c_size_t()
         self._check(lib().sfv_workspace_size(self._h, C.byref(n)))
-        self.ws = torch.empty(n.value, dtype=torch.uint8, device=dev)
         if stream is None:
             stream = torch.cuda.current_stream(dev)
+        # allocated on the stream the kernels run on, so the caching allocator
+        # cannot hand the memory out again while this stream still uses it
+        with torch.cuda.stream(stream):
+            self.ws = torch.empty(n.value, dtype=torch.uint8, device=dev)
         self.stream = stream
         self._check(lib().sfv_bind(self._h, C.c_void_p(self.ws.data_ptr()), n.value,
                                    C.c_void_p(stream.cuda_stream)))
@@ -301,6 +307,25 @@ class Solver:
         out = np.empty((nib + 2, 6, njb + 2)) if k == -2 else np.empty((nib + 4, 4, njb + 4))
         self._check(lib().sfv_debug_block_buffer(self._h, block, k, _dp(out)))
         return out
+
+    def set_profiling(self, on=True):
+        """sfv_set_profiling: per-class CUDA-event timers (no CUDA graph)."""
+        self._check(lib().sfv_set_profiling(self._h, 1 if on else 0))
+
+    PROFILE_CLASSES = ("edge", "interior", "row_exchange", "col_exchange", "exposed_wait", "dt_allreduce",
+                       "viscous", "norms")
+
+    def stage_timings(self):
+        """sfv_get_stage_timings -> dict of accumulated ms per class + 'steps'."""
+        out = np.zeros(9)
+        self._check(lib().sfv_get_stage_timings(self._h, _dp(out)))
+        d = {k: float(v) for k, v in zip(self.PROFILE_CLASSES, out[:8])}
+        d["steps"] = int(out[8])
+        return d
+
+    def set_comm_timeout(self, seconds):
+        """sfv_set_comm_timeout: NCCL deadlock detection."""
+        self._check(lib().sfv_set_comm_timeout(self._h, float(seconds)))
 
     @property
     def error_info(self):

@@ -1,3 +1,17 @@
-for v in base "" w1 w4 w7c; do lib=paper_2305_18057_b200/libsfv${v:+_$v}.so; SFV_LIB=$lib python scripts/occ_probe.py >> gpurun_out/occ.txt 2>&1; done
-bash scripts/gpu_ab.sh rw1 base w1
-bash scripts/gpu_ab.sh rw2 w4 w7c
+# A/B/C... of libsfv builds on C2 and C3 inside one gpurun call (same box):
+#   bash scripts/ab_multi.sh TAG VARIANT...   (variant "cur" = libsfv.so, else libsfv_VARIANT.so)
+TAG=$1; shift
+B_="python bench.py --no-cpu-baseline --no-e2e"
+lib() { if [ "$1" = "cur" ]; then echo paper_2305_18057_b200/libsfv.so; else echo paper_2305_18057_b200/libsfv_$1.so; fi; }
+for rep in 1 2; do
+for v in "$@"; do
+  SFV_LIB=$(lib "$v") timeout 300 $B_ --steps 3000 > gpurun_out/ab_${TAG}_c2_${v}_$rep.json 2>&1
+  SFV_LIB=$(lib "$v") timeout 300 $B_ --workload C3 --steps 60 --warmup 5 > gpurun_out/ab_${TAG}_c3_${v}_$rep.json 2>&1
+done
+done
+for f in gpurun_out/ab_${TAG}_*.json; do python -c "
+import json
+L=[l for l in open('$f').read().splitlines() if l.startswith('{')]
+d=json.loads(L[-1]) if L else {}
+print('$f', round(d.get('value',0)), d.get('clocks',{}).get('sm_mhz'), d.get('clocks',{}).get('reasons'))
+"; done > gpurun_out/ab_${TAG}_summary.txt

@@ -140,3 +140,88 @@ def test_nccl_navier_stokes_ranks(oracle_mod, world, px, py):
     o = oracle_mod.Oracle(cfg, X, Y)
     o.set_state(U0); o.step(steps)
     assert np.all(state_error(U, o.get_state()) <= 1e-11)
+
+
+def _fault_worker(rank, world, port, mode, out_q):
+    """mode 'dead_peer': rank 1 dies after set_state; rank 0 must get
+    SFV_ERR_NCCL from sfv_sync within the comm timeout instead of hanging
+    (SPEC.md:357).  mode 'bad_cell': an invalid cell in rank 1's slab only;
+    every rank must return SFV_ERR_STATE from set_state with the same (global)
+    cell, none may block in a collective."""
+    os.environ.update({"MASTER_ADDR": "127.0.0.1", "MASTER_PORT": str(port),
+                       "NCCL_HOSTID": f"sfv-sim-host-{rank}", "NCCL_SOCKET_IFNAME": "lo",
+                       "NCCL_IB_DISABLE": "1", "NCCL_NVLS_ENABLE": "0"})
+    import sys
+    import time
+    sys.path.insert(0, ROOT)
+    import torch.distributed as dist
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2305_18057_b200 import inputs as I
+        from paper_2305_18057_b200 import sfv
+        ni, nj = 160, 64
+        X, Y = I.ramp_nodes(ni, nj, 30.0)
+        cfg = I.default_config(ni, nj)
+        obj = [sfv.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        s = sfv.Solver(cfg, X, Y, px=world, py=1, rank=rank, nranks=world, nccl_id=obj[0], device=0)
+        s.set_comm_timeout(5.0)
+        U0 = I.perturbed_state(ni, nj, 7)
+        if mode == "bad_cell":
+            U0[10, 150, 0] = -1.0            # rho < 0 in the last slab only (i = 150)
+            try:
+                s.set_state(U0)
+                out_q.put((rank, "no error", None, None))
+            except sfv.SfvError as ex:
+                out_q.put((rank, ex.code, ex.info, str(ex)))
+            return
+        s.set_state(U0)
+        s.step(5); s.sync()
+        dist.barrier()
+        if rank == 1:
+            os._exit(0)                      # the neighbour disappears
+        time.sleep(1.0)
+        t0 = time.time()
+        try:
+            s.step(50)
+            s.sync()
+            out_q.put((rank, "no error", None, time.time() - t0))
+        except sfv.SfvError as ex:
+            out_q.put((rank, ex.code, str(ex), time.time() - t0))
+        os._exit(0)                          # (the communicator is aborted; skip teardown)
+    except Exception as ex:
+        out_q.put((rank, repr(ex), None, None))
+
+
+def _run_fault(mode, world=2, expect=2):
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    ps = [ctx.Process(target=_fault_worker, args=(r, world, port, mode, q)) for r in range(world)]
+    for p in ps:
+        p.start()
+    try:
+        res = sorted((q.get(timeout=240) for _ in range(expect)), key=lambda r: r[0])
+    finally:
+        for p in ps:
+            p.join(timeout=60)
+            if p.is_alive():
+                p.kill()
+    return res
+
+
+def test_nccl_dead_peer_is_an_error_not_a_hang():
+    from paper_2305_18057_b200 import sfv
+    (rank, code, msg, secs), = _run_fault("dead_peer", expect=1)
+    assert rank == 0 and code == sfv.ERR_NCCL, (code, msg)
+    assert "rank 1" in msg and ("deadlock" in msg or "async error" in msg), msg   # names the edge
+    assert secs < 60, secs
+
+
+def test_nccl_invalid_cell_on_one_rank_every_rank_errors():
+    from paper_2305_18057_b200 import sfv
+    res = _run_fault("bad_cell", expect=2)
+    codes = [r[1] for r in res]
+    assert codes == [sfv.ERR_STATE, sfv.ERR_STATE], res
+    assert res[0][2] == res[1][2] and res[0][2][2:] == (150, 10), res   # same global cell (i, j)

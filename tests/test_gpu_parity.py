@@ -431,3 +431,34 @@ def test_perfmodel_geometry_matches_library(sfv_mod, ni, nj):
     li = g.launch_info()
     strips, segs, _, _ = M.launch_geometry(ni, nj, slots=148 * li["ctas_per_sm"])
     assert (strips, segs) == (li["strips"], li["segments"])
+
+
+def test_stage_timings_profiling_mode(oracle_mod):
+    """sfv_set_profiling / sfv_get_stage_timings (per-class CUDA-event timers,
+    PAPER.md:157 iteration breakdown): loopback 2 x 1 slabs with the overlap
+    split report edge, interior, row-exchange and exposed-wait time, and the
+    profiled (graph-less) steps give bitwise the graph's results."""
+    from paper_2305_18057_b200 import inputs as I
+    from paper_2305_18057_b200 import sfv
+    ni, nj, steps = 256, 128, 20
+    X, Y = I.ramp_nodes(ni, nj, 30.0)
+    cfg = I.default_config(ni, nj)
+    U0 = I.perturbed_state(ni, nj, 2)
+    a = sfv.Solver(cfg, X, Y, px=2, py=1)
+    a.set_state(U0); a.step(steps); a.sync()
+    b = sfv.Solver(cfg, X, Y, px=2, py=1)
+    b.set_profiling(True)
+    b.set_state(U0); b.step(steps); b.sync()
+    t = b.stage_timings()
+    np.testing.assert_array_equal(a.get_state(), b.get_state())
+    np.testing.assert_array_equal(a.dt(), b.dt())
+    assert t["steps"] == steps
+    for k in ("edge", "interior", "row_exchange"):
+        assert t[k] > 0.0, t
+    assert t["exposed_wait"] >= 0.0 and t["dt_allreduce"] == 0.0
+    # one block: everything is interior
+    c = sfv.Solver(cfg, X, Y)
+    c.set_profiling(True)
+    c.set_state(U0); c.step(4); c.sync()
+    tc = c.stage_timings()
+    assert tc["interior"] > 0 and tc["edge"] == 0 and tc["row_exchange"] == 0

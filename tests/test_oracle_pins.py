@@ -4,6 +4,7 @@ retyping its formulas: each expected value is a printed number (golden
 file, cited), a closed form derived independently, an invariant, or a
 textbook solution (tests/exact.py)."""
 import math
+import os
 
 import numpy as np
 import pytest
@@ -471,3 +472,36 @@ def test_stable_dt_matches_solver_dt(oracle_mod):
         o = oracle_mod.Oracle(I.default_config(ni, nj), X, Y)
         o.set_state(U); o.step(1)
         assert o.dt()[0] == oracle_mod.stable_dt(X, Y, U)
+
+
+def test_openmp_build_is_bitwise_single_thread(tmp_path):
+    """The -fopenmp build of oracle.c (bench.py's all-cores CPU baseline) is
+    bitwise the single-threaded oracle: state, norm and dt histories after
+    30 RK4 steps of a perturbed 30-degree inlet on 4 threads, incl. 2x2
+    blocks (row loops shared; norm sums serial; dt min exact)."""
+    import subprocess
+    import sys
+    code = r'''
+import sys, numpy as np
+sys.path.insert(0, %r); sys.path.insert(0, %r)
+import oracle
+from paper_2305_18057_b200 import inputs as I
+ni, nj = 96, 48
+X, Y = I.ramp_nodes(ni, nj, 30.0)
+cfg = I.default_config(ni, nj)
+U0 = I.perturbed_state(ni, nj, 4)
+out = []
+for omp in (False, True):
+    for (px, py) in ((1, 1), (2, 2)):
+        o = oracle.Oracle(cfg, X, Y, omp=omp)
+        o.partition(px, py)
+        o.set_state(U0); o.step(30)
+        out.append((o.get_state(), o.residual_norms(), o.dt()))
+for a, b in zip(out[:2], out[2:]):
+    for x, y in zip(a, b):
+        assert np.array_equal(x, y)
+print("bitwise")
+''' % (os.path.dirname(os.path.dirname(os.path.abspath(__file__))), os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True,
+                       env={**os.environ, "OMP_NUM_THREADS": "4"}, timeout=300)
+    assert r.returncode == 0 and "bitwise" in r.stdout, r.stdout + r.stderr
