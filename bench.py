@@ -11,10 +11,21 @@ RK stages x steps / device time (reading A-R21: a cell-update is one cell
 through one RK stage, so Mcell-updates/s = np x ssspnt of Eq. 14).
 
 N = 1 runs BASELINE config C2 (1440 x 720 = 1,036,800 cells, 30-degree
-inlet).  N > 1 (torchrun, one process per GPU, NCCL) runs C2 per GPU as
-weak scaling: global grid (1440 N) x 720 in N slabs along i.
---workload C3 / C4 select the strong (66.4 M cells) / weak (16.6 M per GPU)
-scaling configurations instead.
+inlet).  N > 1 (torchrun, one process per GPU, NCCL) runs BASELINE config C3
+by default: the 11520 x 5760 = 66.4 M-cell inlet in N slabs along i
+(PAPER.md:174), strong scaling -- the north star's >= 80 % efficiency target
+at 8 GPUs on >= 64 M cells.  Rank 0 also times the same C3 grid on its one
+GPU first ("strong_scaling_base"), each rank times its own slab alone (the
+measured halo time fraction), and a short copy-mode run with the per-class
+CUDA-event timers gives the edge / interior / exchange / exposed-wait / dt
+breakdown.  --workload C2 / C4 select weak scaling (1440 N x 720, 5760 N x
+2880) instead.
+
+Timing: W warm-up steps, then R repeats of exactly K steps, each bracketed by
+a barrier + device sync and timed with CUDA events on the solver's stream
+(max over ranks); `value` / `ms_per_step` come from the median repeat.  R is
+chosen so the repeats span >= 0.5 s, so nvidia-smi samples the clocks
+during the timed region.
 
 --impl reference times the plain CPU oracle (oracle/, test infrastructure)
 as it stands on the host cores, on a bounded sample of the same workload.
@@ -142,28 +153,75 @@ def measured_peak():
 NS_MU = 1.0e-3
 
 
-def cpu_baseline_oracle(budget_s=15.0, steps_cap=None, ns=False):
-    """The oracle, as it stands, single-threaded on a bounded sample: the
-    bottom rows of the C2 grid (ramp included) for a few RK4 steps."""
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def _time_oracle(omp, budget_s, ni, rows, ns, threads=None):
     import oracle
-    oracle.build()
-    ni = 1440
-    rows = 16
     X, Y = I.ramp_nodes(ni, rows, 30.0)
     cfg = I.default_config(ni, rows, **(dict(viscous=1, mu=NS_MU) if ns else {}))
-    o = oracle.Oracle(cfg, X, Y)
+    o = oracle.Oracle(cfg, X, Y, omp=omp)
     o.set_state(I.uniform_state(ni, rows))
     o.step(1)  # warm
     t0 = time.perf_counter()
     n = 0
-    while time.perf_counter() - t0 < budget_s and (steps_cap is None or n < steps_cap):
+    while time.perf_counter() - t0 < budget_s:
         o.step(1)
         n += 1
     dt = time.perf_counter() - t0
-    v = ni * rows * 4 * n / dt / 1e6
-    return {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle",
-            "sample": f"C2 grid bottom {rows} rows ({ni}x{rows} cells incl. ramp), {n} RK4 steps"
-                      f"{' (Navier-Stokes)' if ns else ''}, {dt:.1f} s single-threaded -O2 -ffp-contract=off"}
+    return ni * rows * 4 * n / dt / 1e6, n, dt, o
+
+
+def cpu_baseline_oracle(budget_s=12.0, ns=False):
+    """The oracle, as it stands, on a bounded sample (the bottom rows of the
+    C2 grid, ramp included, for as many RK4 steps as fit the budget):
+    single-threaded pinned to one host core (taskset-equivalent
+    sched_setaffinity), then the same source built with -fopenmp on every
+    core of this process's affinity mask (bitwise equal to one thread:
+    tests/test_oracle_pins.py::test_openmp_build_is_bitwise_single_thread,
+    re-checked here on the sample)."""
+    import numpy as _np
+    import oracle
+    oracle.build()
+    ni, rows = 1440, 16
+    cores = sorted(os.sched_getaffinity(0))
+    pinned = cores[-1]
+    try:
+        os.sched_setaffinity(0, {pinned})
+        v1, n1, dt1, o1 = _time_oracle(False, budget_s, ni, rows, ns)
+    finally:
+        os.sched_setaffinity(0, set(cores))
+    out = {"value": v1, "unit": UNIT, "cores": 1, "kind": "oracle",
+           "sample": f"C2 grid bottom {rows} rows ({ni}x{rows} cells incl. ramp), {n1} RK4 steps"
+                     f"{' (Navier-Stokes)' if ns else ''}, {dt1:.1f} s single-threaded -O2 -ffp-contract=off, "
+                     f"pinned to core {pinned}",
+           "cpu_model": cpu_model(), "affinity_cores": len(cores)}
+    try:
+        oracle.build(omp=True)
+        os.environ["OMP_NUM_THREADS"] = str(len(cores))
+        vN, nN, dtN, oN = _time_oracle(True, budget_s / 2, ni, rows, ns)
+        # bitwise check against the single-threaded run over the common steps
+        same = None
+        k = min(n1, nN) + 1
+        if k >= 2:
+            a = oracle.Oracle(dict(o1.cfg), *I.ramp_nodes(ni, rows, 30.0))
+            a.set_state(I.uniform_state(ni, rows)); a.step(k)
+            b = oracle.Oracle(dict(oN.cfg), *I.ramp_nodes(ni, rows, 30.0), omp=True)
+            b.set_state(I.uniform_state(ni, rows)); b.step(k)
+            same = bool(_np.array_equal(a.get_state(), b.get_state()) and _np.array_equal(a.dt(), b.dt()))
+        out["all_cores"] = {"value": vN, "unit": UNIT, "cores": len(cores), "kind": "oracle (-fopenmp build)",
+                            "bitwise_equal_to_single_thread": same,
+                            "sample": f"same sample, {nN} RK4 steps, {dtN:.1f} s, OMP_NUM_THREADS={len(cores)}"}
+    except Exception as ex:  # the all-cores leg is context; never lose the line for it
+        out["all_cores"] = {"unavailable": repr(ex)[:200]}
+    return out
 
 
 def run_reference(args, rank, world):
@@ -193,7 +251,8 @@ def run_reference(args, rank, world):
             "higher_is_better": True, "scaling": scaling, "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded inputs)",
             "config": {"workload": desc, "sample_cells": cells, "rk_stages": 4},
-            "cpu_baseline": {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample},
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample,
+                             "cpu_model": cpu_model(), "affinity_cores": len(os.sched_getaffinity(0))},
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -201,10 +260,14 @@ def run_reference(args, rank, world):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=6000)
+    ap.add_argument("--steps", type=int, default=None,
+                    help="K steps per timed repeat (default: C2 2000, C3 100, C4 200)")
     ap.add_argument("--warmup", type=int, default=50)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="C2", choices=["C2", "C3", "C4"])
+    ap.add_argument("--workload", default="auto", choices=["auto", "C2", "C3", "C4"],
+                    help="auto: C2 at N = 1, C3 strong scaling at N > 1")
+    ap.add_argument("--min-timed-s", type=float, default=0.5,
+                    help="repeat the K-step timed region until it spans this long (clock sampling)")
     ap.add_argument("--rk", default="rk4", choices=["rk4", "heun", "jst4"],
                     help="RK tableau (reading A-R5; SURVEY §8(f) f1: per-substep cost RK2 vs RK4, PAPER.md:276)")
     ap.add_argument("--halo", default="peer", choices=["copy", "peer"],
@@ -217,10 +280,15 @@ def main():
                     help="Navier-Stokes mode (SURVEY §8(f) f4): viscous flux with mu = 1e-3")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-extras", action="store_true", help="N > 1: skip the strong-scaling base, halo and breakdown runs")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
     world = env_int("WORLD_SIZE", 1)
+    if args.workload == "auto":
+        args.workload = "C2" if world == 1 else "C3"
+    if args.steps is None:
+        args.steps = {"C2": 2000, "C3": 100, "C4": 200}[args.workload]
     rank = env_int("RANK", 0)
     local_rank = env_int("LOCAL_RANK", 0)
     if args.impl == "reference":
@@ -326,15 +394,29 @@ def main():
             dist.barrier()
 
     # ---- device-timed region (inputs resident in HBM) ----
-    barrier()
-    with Clocks(local_rank) as clk:
+    # R repeats of exactly K steps (each bracketed by barrier + sync, CUDA
+    # events on the solver's stream, max over ranks); median repeat reported
+    def timed_once():
+        barrier()
         solver.step(args.steps)
-        ms = solver.sync()
-    barrier()
-    t = torch.tensor([ms], dtype=torch.float64, device=dev)
+        ms_ = solver.sync()
+        barrier()
+        return ms_
+
+    probe = timed_once()  # (also a last warm-up; not reported)
+    tp = torch.tensor([probe], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(tp, op=dist.ReduceOp.MAX)
+    reps = int(min(2000, max(5, np.ceil(args.min_timed_s * 1e3 / max(float(tp.item()), 1e-3)))))
+    rep_ms = []
+    with Clocks(local_rank) as clk:
+        for _ in range(reps):
+            rep_ms.append(timed_once())
+    t = torch.tensor(rep_ms, dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ms_max = float(t.item())
+    rep_max = [float(x) for x in t.cpu().numpy()]
+    ms_max = float(statistics.median(rep_max))
     cells_total = ni * nj
     stages = I.RK_STAGES[rk]
     value = cells_total * stages * args.steps / (ms_max * 1e-3) / 1e6
@@ -350,9 +432,7 @@ def main():
         edges = 0 if nblk == 1 else 2 * (nblk - 1) / nblk  # average per loopback block
     if args.halo == "peer":
         edges = 0
-    nbatch = (args.warmup + args.steps) // 32 - args.warmup // 32
-    # (Navier-Stokes: + gradient and viscous-residual kernels per stage)
-    launches = int(round(nblk * (stages * (1 + edges + (2 if args.ns else 0)) * args.steps + nbatch)))
+    launches = int(round(nblk * (stages * (1 + edges + (2 if args.ns else 0)) * args.steps + args.steps / 32.0)))
     stage_launches = stages * args.steps * nblk
 
     # ---- roofline of the dominant kernel (the fused stage kernel) ----
@@ -381,28 +461,45 @@ def main():
                 "hbm": hbm,
                 **({"note": "NS: the FP64 count per cell-stage is the Euler stage kernel's (ncu); the gradient / "
                             "viscous-flux kernels add work not counted here (profiles/r1_ns_*)"} if args.ns else {})}
+
     # ---- end to end through the public API with host buffers ----
+    # set_state(pinned host U) + K steps + residual norms of the K steps
+    # (64 B/step) + the solution back to pinned host memory (N = 1: the full
+    # grid; N > 1: every rank its own slab, sfv_get_block_state)
     e2e = None
     if not args.no_e2e:
         Uh = torch.from_numpy(np.ascontiguousarray(U0)).pin_memory()
-        Uout = torch.empty_like(Uh)
+        if world == 1:
+            Uout = torch.empty(Uh.shape, dtype=torch.float64, pin_memory=True)
+        else:
+            m = solver.partition_map(rank)
+            Uout = torch.empty((int(m[3] - m[2]), int(m[1] - m[0]), 4), dtype=torch.float64, pin_memory=True)
         K = args.steps
         barrier()
         t0 = time.perf_counter()
         solver.set_state_ptr(Uh.data_ptr())
+        t1 = time.perf_counter()
         solver.step(K)
         norms = solver.residual_norms(0, K)
-        solver.get_state_ptr(Uout.data_ptr())
+        t2 = time.perf_counter()
+        if world == 1:
+            solver.get_state_ptr(Uout.data_ptr())
+        else:
+            solver.get_block_state_ptr(rank, Uout.data_ptr())
         barrier()
-        wall = time.perf_counter() - t0
-        tw = torch.tensor([wall], dtype=torch.float64, device=dev)
+        t3 = time.perf_counter()
+        tw = torch.tensor([t3 - t0, t1 - t0, t2 - t1, t3 - t2], dtype=torch.float64, device=dev)
         if world > 1:
             dist.all_reduce(tw, op=dist.ReduceOp.MAX)
-        wall = float(tw.item())
-        sbytes = cells_total * 4 * 8
+        wall, w_set, w_step, w_get = (float(x) for x in tw.cpu().numpy())
+        rank_bytes = Uout.numel() * 8
         e2e = {"value": cells_total * stages * K / wall / 1e6, "unit": UNIT,
-               "h2d_bytes_per_step": sbytes / K, "d2h_bytes_per_step": sbytes / K + 64.0,
-               "note": "set_state(pinned host U) + K steps + residual norms (64 B/step) + get_state, wall clock"}
+               "h2d_bytes_per_step": rank_bytes * world / K, "d2h_bytes_per_step": (rank_bytes * world + 64.0 * K) / K,
+               "phases_ms": {"set_state": 1e3 * w_set, "steps_and_norms": 1e3 * w_step, "get_state": 1e3 * w_get},
+               "fixed_overhead_ms": 1e3 * wall - ms_max,
+               "note": "set_state(pinned host U) + K steps + residual norms (64 B/step) + solution to pinned host "
+                       "memory (" + ("full grid" if world == 1 else "each rank its slab") + "), wall clock, max over ranks; "
+                       "fixed_overhead_ms = wall - device time of K steps"}
         assert np.all(np.isfinite(norms))
 
     cpu = None
@@ -411,15 +508,18 @@ def main():
 
     li = solver.launch_info()
     halo_info = None
+    extras = {}
     if px > 1:
         # halo traffic per step of the busiest rank (2 edge rows x 4 components per
         # connected cut, every stage) and the time it would take at NVLink 5's
-        # 900 GB/s per direction, as a fraction of the measured step: a bandwidth
-        # model (multi-GPU exchange is not timed separately on this pool)
+        # 900 GB/s per direction (a bandwidth model, next to the measured fraction below)
         cuts = 2 if px > 2 or world == 1 else 1
         hb = cuts * 2 * 4 * 8 * nj * stages
         halo_info = {"bytes_per_step_per_rank": hb, "nvlink_gbs": 900.0,
                      "nvlink_time_fraction_model": hb / 900e9 / (ms_max * 1e-3 / args.steps)}
+    if world > 1 and not args.no_extras:
+        extras = multi_gpu_extras(args, solver, dev, rank, world, ni, nj, theta, cfg, U0, ms_max, barrier, sfv,
+                                  torch, dist, local_rank)
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": n_gpus, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
@@ -431,13 +531,89 @@ def main():
                            **({"simulated_ranks_on_one_gpu": True} if sim else {}),
                            "l2": f"no flush: working set {solver.ws.numel() / 1e6:.0f} MB per GPU vs 126 MB L2",
                            "launch": li,
+                           "timing": {"repeats": reps, "steps_per_repeat": args.steps,
+                                      "ms_per_repeat_median": ms_max, "ms_per_repeat_min": min(rep_max),
+                                      "ms_per_repeat_max": max(rep_max)},
                            "mcell_steps_per_s": value / stages,
-                           "pct_hbm_roofline_8TBs": 100.0 * value * 1e6 * ALG_BYTES_PER_CELL_STAGE / n_gpus / 8e12},
-                "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
+                           "pct_hbm_roofline_8TBs": 100.0 * value * 1e6 * ALG_BYTES_PER_CELL_STAGE / n_gpus / 8e12,
+                           **extras},
+                "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches * reps,
                 "clocks": clk.summary()}
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+def multi_gpu_extras(args, solver, dev, rank, world, ni, nj, theta, cfg, U0, ms_multi, barrier, sfv, torch, dist,
+                     local_rank):
+    """N > 1 context measured in the same job (BASELINE configs[2]/[3]):
+    * strong_scaling_base (C3): rank 0 times the whole grid on its one GPU;
+    * halo: each rank times its own slab as an isolated single-block run; the
+      measured halo time fraction is 1 - t_alone / t_multi (PAPER.md:157,
+      :172 -- exchange cost as the paper's model separates it);
+    * breakdown_copy_mode: a short run with copy-mode (NCCL send/recv) halos
+      and the per-class CUDA-event timers (sfv_get_stage_timings), ms per step,
+      max over ranks.
+    Each measurement runs one rank at a time where it would otherwise share a
+    GPU with other ranks' work."""
+    K = max(args.steps, 10)
+    out = {}
+    stages = I.RK_STAGES[cfg["rk"]]
+
+    def single(ni_, nj_, steps):
+        X_, Y_ = I.ramp_nodes(ni_, nj_, theta)
+        c_ = dict(cfg, ni=ni_, nj=nj_)
+        s_ = sfv.Solver(c_, X_, Y_, device=local_rank)
+        s_.set_state(I.uniform_state(ni_, nj_))
+        s_.step(args.warmup); s_.sync()
+        s_.step(steps)
+        ms_ = s_.sync()
+        s_.close()
+        return ms_
+
+    if args.workload == "C3":
+        barrier()
+        base = None
+        if rank == 0:
+            base = single(ni, nj, K)
+            out["strong_scaling_base"] = {"n_gpus": 1, "ms_per_step": base / K,
+                                          "value": ni * nj * stages * K / (base * 1e-3) / 1e6, "unit": UNIT,
+                                          "note": "the same C3 grid on rank 0's one GPU, timed in this job"}
+        barrier()
+    m = solver.partition_map(rank)
+    nib, njb = int(m[1] - m[0]), int(m[3] - m[2])
+    alone = 0.0
+    for r in range(world):  # one rank at a time
+        barrier()
+        if r == rank:
+            alone = single(nib, njb, K)
+        barrier()
+    frac = 1.0 - (alone / K) / (ms_multi / args.steps)
+    ft = torch.tensor([frac, alone / K], dtype=torch.float64, device=dev)
+    lst = [torch.zeros_like(ft) for _ in range(world)]
+    dist.all_gather(lst, ft)
+    fr = [float(x[0]) for x in lst]
+    out["halo"] = {"time_fraction_measured_max": max(fr), "time_fraction_measured_mean": sum(fr) / len(fr),
+                   "slab_alone_ms_per_step_max": max(float(x[1]) for x in lst),
+                   "multi_ms_per_step": ms_multi / args.steps, "mode": args.halo}
+    # copy-mode breakdown with the per-class timers
+    try:
+        solver.set_halo_mode(sfv.HALO_COPY)
+        solver.set_state(U0)
+        solver.step(args.warmup); solver.sync()
+        solver.set_profiling(True)
+        barrier()
+        solver.step(10)
+        solver.sync()
+        tm = solver.stage_timings()
+        solver.set_profiling(False)
+        keys = list(sfv.Solver.PROFILE_CLASSES)
+        v = torch.tensor([tm[k] / max(tm["steps"], 1) for k in keys], dtype=torch.float64, device=dev)
+        dist.all_reduce(v, op=dist.ReduceOp.MAX)
+        out["breakdown_copy_mode_ms_per_step_max_over_ranks"] = {k: float(x) for k, x in zip(keys, v.cpu().numpy())}
+    except sfv.SfvError as ex:
+        out["breakdown_copy_mode_ms_per_step_max_over_ranks"] = {"unavailable": str(ex)[:200]}
+    return out
 
 
 if __name__ == "__main__":

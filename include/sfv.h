@@ -236,6 +236,15 @@ sfv_status sfv_get_dt(sfv_ctx *ctx, int64_t first, int64_t count, double *out);
  * STATE: the run hit an invalid state.  NCCL: gather failed / timed out. */
 sfv_status sfv_get_state(sfv_ctx *ctx, double *U_global_out);
 
+/* "Solution output" of one local block (each rank writes its
+ * own part, as the paper's MPI ranks do): U^n of block `block` (a block of
+ * this rank: sfv_partition_map gives its extent [i0,i1) x [j0,j1)) into a
+ * caller-owned host array of (i1-i0)*(j1-j0)*4 doubles, index
+ * ((j-j0)*(i1-i0) + (i-i0))*4 + k.  Not collective; synchronising.
+ * ARG: block not local.  SEQUENCE: no state.  STATE: the run hit an invalid
+ * state (this rank's view). */
+sfv_status sfv_get_block_state(sfv_ctx *ctx, int32_t block, double *U_block_out);
+
 /* Details of the last SFV_ERR_STATE / GEOMETRY: out4 = step, stage, i, j
  * (-1 where not applicable). */
 sfv_status sfv_error_info(const sfv_ctx *ctx, int64_t *out4);

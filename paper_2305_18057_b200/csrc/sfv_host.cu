@@ -1449,6 +1449,20 @@ sfv_status sfv_get_state(sfv_ctx *c, double *U) {
     return SFV_OK;
 }
 
+sfv_status sfv_get_block_state(sfv_ctx *c, int32_t block, double *U) {
+    if (!c || !U) return SFV_ERR_ARG;
+    if (!c->have_state) return fail(c, SFV_ERR_SEQUENCE, "no state");
+    Block *b = local_block(c, block);
+    if (!b) return fail(c, SFV_ERR_ARG, "block %d is not local to rank %d", block, c->rank);
+    SYNC("sfv_get_block_state");
+    sfv_status s = check_device_error(c);
+    if (s != SFV_OK) return s;
+    CK(launch_gather(b->buf[0], b->stage, b->ni, b->nj, b->PJ, c->st));
+    CK(cudaMemcpyAsync(U, b->stage, sizeof(double) * 4 * (size_t)b->ni * b->nj, cudaMemcpyDeviceToHost, c->st));
+    SYNC("sfv_get_block_state");
+    return SFV_OK;
+}
+
 sfv_status sfv_error_info(const sfv_ctx *c, int64_t *out4) {
     if (!c || !out4) return SFV_ERR_ARG;
     for (int k = 0; k < 4; ++k) out4[k] = c->einfo[k];

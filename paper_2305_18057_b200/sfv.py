@@ -28,7 +28,7 @@ ABI_SYMBOLS = ["sfv_create", "sfv_partition", "sfv_nccl_unique_id", "sfv_partiti
                "sfv_get_residual_norms", "sfv_get_dt", "sfv_get_state", "sfv_error_info", "sfv_launch_info",
                "sfv_debug_math", "sfv_set_halo_mode", "sfv_peer_handle", "sfv_peer_connect",
                "sfv_debug_block_buffer", "sfv_residual", "sfv_set_profiling", "sfv_get_stage_timings",
-               "sfv_set_comm_timeout", "sfv_last_error", "sfv_destroy"]
+               "sfv_set_comm_timeout", "sfv_get_block_state", "sfv_last_error", "sfv_destroy"]
 
 
 class SfvError(RuntimeError):
@@ -89,6 +89,7 @@ def lib():
         L.sfv_set_profiling.argtypes = [_VP, C.c_int32]
         L.sfv_get_stage_timings.argtypes = [_VP, _D]
         L.sfv_set_comm_timeout.argtypes = [_VP, C.c_double]
+        L.sfv_get_block_state.argtypes = [_VP, C.c_int32, _D]
         L.sfv_last_error.argtypes = [_VP]
         L.sfv_last_error.restype = C.c_char_p
         L.sfv_destroy.argtypes = [_VP]
@@ -265,6 +266,18 @@ class Solver:
             out = np.empty((self.nj, self.ni, 4))
         self._check(lib().sfv_get_state(self._h, _dp(out)))
         return out
+
+    def get_block_state(self, block=None, out=None):
+        """sfv_get_block_state: this rank's block (default: block `rank`), [nj_b, ni_b, 4]."""
+        b = self.rank if block is None else block
+        m = self.partition_map(b)
+        if out is None:
+            out = np.empty((int(m[3] - m[2]), int(m[1] - m[0]), 4))
+        self._check(lib().sfv_get_block_state(self._h, b, _dp(out)))
+        return out
+
+    def get_block_state_ptr(self, block, ptr):
+        self._check(lib().sfv_get_block_state(self._h, block, C.cast(C.c_void_p(ptr), _D)))
 
     def get_state_ptr(self, ptr):
         self._check(lib().sfv_get_state(self._h, C.cast(C.c_void_p(ptr), _D)))
