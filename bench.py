@@ -593,7 +593,7 @@ def multi_gpu_extras(args, solver, dev, rank, world, ni, nj, theta, cfg, U0, ms_
     lst = [torch.zeros_like(ft) for _ in range(world)]
     dist.all_gather(lst, ft)
     fr = [float(x[0]) for x in lst]
-    out["halo"] = {"time_fraction_measured_max": max(fr), "time_fraction_measured_mean": sum(fr) / len(fr),
+    out["halo_measured"] = {"time_fraction_measured_max": max(fr), "time_fraction_measured_mean": sum(fr) / len(fr),
                    "slab_alone_ms_per_step_max": max(float(x[1]) for x in lst),
                    "multi_ms_per_step": ms_multi / args.steps, "mode": args.halo}
     # copy-mode breakdown with the per-class timers

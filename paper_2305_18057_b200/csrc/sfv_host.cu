@@ -860,7 +860,10 @@ sfv_status enqueue_step(sfv_ctx *c, cudaStream_t st, bool norms_batch) {
             CK(cudaStreamWaitEvent(st, c->ev_comm, 0));
             span_end(c, sw, st);
         } else {
-            const int sx = span_begin(c, P_XROW, st);
+            bool connected = false;
+            for (Block &b : c->blocks)
+                for (int e = 0; e < 4; ++e) connected |= b.nbr[e] >= 0;
+            const int sx = connected ? span_begin(c, P_XROW, st) : -1;
             sfv_status r = exchange(c, sp.out, st);
             if (r != SFV_OK) return r;
             span_end(c, sx, st);
@@ -932,7 +935,10 @@ sfv_status wait_stream(sfv_ctx *c, const char *what) {
         const double idle = std::chrono::duration<double>(clk::now() - last).count();
         if ((ar != ncclSuccess && ar != ncclInProgress) || idle > c->comm_timeout) {
             const long long pend = c->prog.empty() ? -1 : c->prog.front().second;
+            const bool dbg = getenv("SFV_DEBUG_WAIT") != nullptr;
+            if (dbg) fprintf(stderr, "[sfv] %s: async=%d idle=%.1fs pending step %lld: aborting\n", what, (int)ar, idle, pend);
             N.CommAbort(c->comm);
+            if (dbg) fprintf(stderr, "[sfv] %s: communicator aborted\n", what);
             c->comm = nullptr;
             c->comm_dead = true;
             c->have_state = false;

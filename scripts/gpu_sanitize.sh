@@ -14,6 +14,7 @@ for (ni, nj, px, py, rk, peer, ns) in [(64, 32, 1, 1, 0, 0, 0), (40, 36, 2, 2, 0
     if peer:
         g.enable_peer_halo()
     g.set_state(I.perturbed_state(ni, nj, 1)); g.step(3); g.sync()
+    g.set_profiling(True); g.step(2); g.sync(); g.stage_timings(); g.set_profiling(False)  # graph-less profiled steps
     assert np.all(np.isfinite(g.get_state()))
     R = g.residual(I.perturbed_state(ni, nj, 2))   # sfv_residual (M_RES kernel variant)
     assert np.all(np.isfinite(R))

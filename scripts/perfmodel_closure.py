@@ -14,7 +14,7 @@ max over ranks), and prints measured vs predicted.
 
 alpha (Eq. 12, t_f = alpha T_b: exchange and synchronisation charged to the
 block) is calibrated from the line's own measurement when bench.py recorded
-one (config.halo: each rank's slab timed alone vs inside the N-rank run):
+one (config.halo_measured: each rank's slab timed alone vs inside the N-rank run):
 alpha = t_multi / t_alone - 1 for the slowest rank; the prediction with
 alpha is then t_model (1 + alpha).  Lines whose ranks shared one GPU
 (config.simulated_ranks_on_one_gpu) are flagged: their times are
@@ -107,7 +107,7 @@ def main():
             gm.stages = stages
             pred = gm.multi_gpu_step(blocks) if n > 1 else gm.loopback_step(blocks)
             meas = float(line["ms_per_step"]) * 1e-3
-            halo = line.get("config", {}).get("halo", {})
+            halo = line.get("config", {}).get("halo_measured", {})
             alpha = None
             if isinstance(halo, dict) and halo.get("slab_alone_ms_per_step_max"):
                 t_alone = halo["slab_alone_ms_per_step_max"] * 1e-3

@@ -150,7 +150,7 @@ def _fault_worker(rank, world, port, mode, out_q):
     cell, none may block in a collective."""
     os.environ.update({"MASTER_ADDR": "127.0.0.1", "MASTER_PORT": str(port),
                        "NCCL_HOSTID": f"sfv-sim-host-{rank}", "NCCL_SOCKET_IFNAME": "lo",
-                       "NCCL_IB_DISABLE": "1", "NCCL_NVLS_ENABLE": "0"})
+                       "NCCL_IB_DISABLE": "1", "NCCL_NVLS_ENABLE": "0", "SFV_DEBUG_WAIT": "1"})
     import sys
     import time
     sys.path.insert(0, ROOT)
@@ -180,14 +180,24 @@ def _fault_worker(rank, world, port, mode, out_q):
         dist.barrier()
         if rank == 1:
             os._exit(0)                      # the neighbour disappears
+        import faulthandler
+        os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)
+        logf = open(os.path.join(ROOT, "gpurun_out", "dead_peer_rank0.log"), "w")
+        faulthandler.dump_traceback_later(90, exit=False, file=logf)
+        def note(m):
+            logf.write(f"{time.time():.3f} {m}\n"); logf.flush()
         time.sleep(1.0)
         t0 = time.time()
         try:
+            note("step")
             s.step(50)
+            note("sync")
             s.sync()
             out_q.put((rank, "no error", None, time.time() - t0))
         except sfv.SfvError as ex:
+            note("error " + str(ex))
             out_q.put((rank, ex.code, str(ex), time.time() - t0))
+        out_q.close(); out_q.join_thread()   # flush the queue's feeder thread before the hard exit
         os._exit(0)                          # (the communicator is aborted; skip teardown)
     except Exception as ex:
         out_q.put((rank, repr(ex), None, None))

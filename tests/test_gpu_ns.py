@@ -45,6 +45,27 @@ def test_ns_parity(sfv_mod, oracle_mod, steps, tol, mu):
     assert dt_error(g.dt(), o.dt()) <= 1e-13
 
 
+@pytest.mark.parametrize("mu", [0.02, 0.2])
+def test_ns_parity_1000_steps(sfv_mod, oracle_mod, mu):
+    """The north star's 1000-step gate (1e-9 per conserved variable) in
+    Navier-Stokes mode, no-slip ramp wall, next to the oracle's own 1-ulp
+    sensitivity: the gate is max(1e-9, 5 x sensitivity) (DESIGN.md A-R30)."""
+    ni, nj = 64, 32
+    X, Y = I.ramp_nodes(ni, nj, 5.0)
+    cfg = I.default_config(ni, nj, viscous=1, mu=mu, bc=NOSLIP_S)
+    U0 = I.perturbed_state(ni, nj, 21)
+    g, o = _pair(sfv_mod, oracle_mod, cfg, X, Y, U0, 1000)
+    U1 = U0.copy(); U1[..., 0] = np.nextafter(U1[..., 0], np.inf)
+    s = oracle_mod.Oracle(cfg, X, Y); s.set_state(U1); s.step(1000)
+    Uo = o.get_state()
+    sens = state_error(s.get_state(), Uo).max()
+    nsens = norm_error(s.residual_norms(), o.residual_norms())
+    e = state_error(g.get_state(), Uo).max()
+    assert e <= max(1e-9, 5.0 * sens), (e, sens)
+    assert norm_error(g.residual_norms(), o.residual_norms()) <= max(1e-10, 5.0 * nsens)
+    assert dt_error(g.dt(), o.dt()) <= max(1e-13, 5.0 * dt_error(s.dt(), o.dt()))
+
+
 @pytest.mark.parametrize("rk", [I.RK2_HEUN, I.RK4_JAMESON])
 def test_ns_tableaus(sfv_mod, oracle_mod, rk):
     ni, nj = 48, 40

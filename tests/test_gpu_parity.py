@@ -76,15 +76,33 @@ def test_c1_wedge_1000_steps(sfv_mod, oracle_mod):
 
 
 @pytest.mark.parametrize("seed", [0, 1, 2])
-def test_inlet_256x128_perturbed(sfv_mod, oracle_mod, seed):
+def test_inlet_256x128_perturbed_1000_steps(sfv_mod, oracle_mod, seed):
+    """SURVEY §8(c).5 on the primitive-perturbed 256 x 128 inlet, seeds 0-2:
+    1 step <= 1e-12 and 100 steps <= 1e-10 (state), norms 1e-10, dt 1e-13;
+    1000 steps against the oracle's own sensitivity (reading A-R30): this
+    flow is ill-conditioned at that horizon -- the oracle started with every
+    density moved by one ulp differs from itself by 3e-7 .. 3.5e-6
+    (profiles/r2_parity_margins.md), so the 1000-step gate is
+    max(1e-9, 5 x that sensitivity), and likewise for the norm and dt
+    histories."""
     ni, nj = 256, 128
     X, Y = I.ramp_nodes(ni, nj, 30.0)
     cfg = I.default_config(ni, nj)
     U0 = I.perturbed_state(ni, nj, seed)
     g, o = run_pair(sfv_mod, oracle_mod, cfg, X, Y, U0, 1)
     check(g, o, 1e-12)
-    g.step(49); g.sync(); o.step(49)
+    g.step(99); g.sync(); o.step(99)
     check(g, o, 1e-10)
+    g.step(900); g.sync(); o.step(900)
+    U1 = U0.copy(); U1[..., 0] = np.nextafter(U1[..., 0], np.inf)
+    s = oracle_mod.Oracle(cfg, X, Y); s.set_state(U1); s.step(1000)
+    Uo = o.get_state()
+    sens = state_error(s.get_state(), Uo).max()
+    e = state_error(g.get_state(), Uo).max()
+    assert e <= max(1e-9, 5.0 * sens), (e, sens)
+    nsens = norm_error(s.residual_norms(), o.residual_norms())
+    assert norm_error(g.residual_norms(), o.residual_norms()) <= max(1e-10, 5.0 * nsens)
+    assert dt_error(g.dt(), o.dt()) <= max(1e-13, 5.0 * dt_error(s.dt(), o.dt()))
 
 
 def test_inlet_256x128_1000_steps(sfv_mod, oracle_mod):
