@@ -128,8 +128,8 @@ class Clocks:
                 "reasons": reasons, "samples": len(rows)}
 
 
-def load_profile_traffic():
-    p = os.path.join(ROOT, "profiles", "ncu_stage_kernel.json")
+def load_profile_traffic(ns=False):
+    p = os.path.join(ROOT, "profiles", "ncu_ns.json" if ns else "ncu_stage_kernel.json")
     try:
         with open(p) as f:
             d = json.load(f)
@@ -443,7 +443,7 @@ def main():
     alg_bytes = ALG_BYTES_PER_CELL_STAGE * cells_launch
     hbm_achieved = alg_bytes / avg_launch_s / 1e9
     peak, peak_src = measured_peak()
-    traffic_pc, prof = load_profile_traffic()
+    traffic_pc, prof = load_profile_traffic(ns=args.ns)
     hbm = {"bound": "hbm", "achieved": hbm_achieved, "peak": peak, "unit": "GB/s", "frac": hbm_achieved / peak,
            "traffic": (traffic_pc * cells_launch) if traffic_pc else None,
            "alg_bytes_per_cell_stage": ALG_BYTES_PER_CELL_STAGE, "peak_source": peak_src}
@@ -459,8 +459,9 @@ def main():
                 "profile": prof.get("source"), "kernel": ("sfv::stage_kernel + NS gradient/viscous kernels (per stage, averaged)" if args.ns
                            else "sfv::stage_kernel (4 launches per step, averaged)"),
                 "hbm": hbm,
-                **({"note": "NS: the FP64 count per cell-stage is the Euler stage kernel's (ncu); the gradient / "
-                            "viscous-flux kernels add work not counted here (profiles/r1_ns_*)"} if args.ns else {})}
+                **({"note": "NS: FP64 instructions and DRAM bytes per cell-stage summed over the stage kernel and "
+                            "the fused gradient / viscous-flux kernel of each stage (ncu, profiles/ncu_ns.json); "
+                            "achieved = that count x cell-stages / the average stage time"} if args.ns else {})}
 
     # ---- end to end through the public API with host buffers ----
     # set_state(pinned host U) + K steps + residual norms of the K steps

@@ -27,6 +27,7 @@ using namespace sfv;
 namespace {
 
 constexpr int NSEG_MAX = 256;
+constexpr long long kMaxInflight = 8;  // NCCL-rank steps enqueued ahead of completion
 constexpr size_t PADD = 512;  // padding doubles after each array (bulk-copy over-read)
 
 // ------------------------------------------------------------- NCCL (dlopen)
@@ -904,30 +905,25 @@ std::string edge_names(const sfv_ctx *c) {
 // comm_timeout seconds, aborts the communicator (unblocking the stream) and
 // returns SFV_ERR_NCCL naming this rank's edges and the pending step
 // instead of hanging.
-sfv_status wait_stream(sfv_ctx *c, const char *what) {
-    if (c->comm_dead) return fail(c, SFV_ERR_NCCL, "%s: the NCCL communicator was aborted by an earlier failure", what);
-    if (c->nranks <= 1 || !c->comm) {
-        CK(cudaStreamSynchronize(c->st));
-        for (auto &pe : c->prog) c->ev_pool.push_back(pe.first);
-        c->prog.clear();
-        if (!c->spans.empty()) {
-            CK(cudaStreamSynchronize(c->comm_st));
-            spans_collect(c);
-        }
-        return SFV_OK;
-    }
+// Poll until the stream has drained (inflight < 0) or at most `inflight`
+// tracked steps are still pending, watching NCCL's async error and progress.
+sfv_status poll_wait(sfv_ctx *c, const char *what, long long inflight) {
     Nccl &N = nccl();
     using clk = std::chrono::steady_clock;
     auto last = clk::now();
     for (;;) {
-        const cudaError_t q = cudaStreamQuery(c->st);
-        if (q == cudaSuccess) break;
-        if (q != cudaErrorNotReady) return fail(c, SFV_ERR_CUDA, "%s: %s", what, cudaGetErrorString(q));
         bool moved = false;
         while (!c->prog.empty() && cudaEventQuery(c->prog.front().first) == cudaSuccess) {
             c->ev_pool.push_back(c->prog.front().first);
             c->prog.pop_front();
             moved = true;
+        }
+        if (inflight >= 0) {
+            if ((long long)c->prog.size() <= inflight) return SFV_OK;
+        } else {
+            const cudaError_t q = cudaStreamQuery(c->st);
+            if (q == cudaSuccess) return SFV_OK;
+            if (q != cudaErrorNotReady) return fail(c, SFV_ERR_CUDA, "%s: %s", what, cudaGetErrorString(q));
         }
         if (moved) last = clk::now();
         ncclResult_t ar = ncclSuccess;
@@ -950,7 +946,17 @@ sfv_status wait_stream(sfv_ctx *c, const char *what) {
                         "pending at step %lld; communicator aborted",
                         what, c->comm_timeout, c->rank, edge_names(c).c_str(), pend);
         }
-        usleep(200);
+        usleep(inflight >= 0 ? 20 : 200);
+    }
+}
+
+sfv_status wait_stream(sfv_ctx *c, const char *what) {
+    if (c->comm_dead) return fail(c, SFV_ERR_NCCL, "%s: the NCCL communicator was aborted by an earlier failure", what);
+    if (c->nranks <= 1 || !c->comm) {
+        CK(cudaStreamSynchronize(c->st));
+    } else {
+        sfv_status r = poll_wait(c, what, -1);
+        if (r != SFV_OK) return r;
     }
     for (auto &pe : c->prog) c->ev_pool.push_back(pe.first);
     c->prog.clear();
@@ -1305,6 +1311,13 @@ sfv_status sfv_step(sfv_ctx *c, int32_t nsteps) {
             if (r != SFV_OK) return r;
         }
         if (track) {
+            // at most kMaxInflight NCCL steps queued: a launch behind a stalled
+            // exchange can block inside the runtime, so the wait stays ours
+            // (bounded)
+            if ((long long)c->prog.size() >= kMaxInflight) {
+                sfv_status r = poll_wait(c, "sfv_step", kMaxInflight - 1);
+                if (r != SFV_OK) return r;
+            }
             cudaEvent_t ev = nullptr;
             if (!c->ev_pool.empty()) {
                 ev = c->ev_pool.back();

@@ -18,3 +18,4 @@ timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --lo
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:stage_kernel -s 40 -c 4 -o gpurun_out/prof_$TAG python bench.py --steps 20 --warmup 10 --min-timed-s 0 --no-cpu-baseline --no-e2e > gpurun_out/ncu_$TAG.log 2>&1
 timeout 900 ncu --set full --clock-control none -k regex:stage_kernel -s 20 -c 4 -o gpurun_out/prof_${TAG}_c3 python bench.py --workload C3 --steps 6 --warmup 5 --min-timed-s 0 --no-cpu-baseline --no-e2e > gpurun_out/ncu_${TAG}_c3.log 2>&1
 bash scripts/gpu_sanitize.sh $TAG
+timeout 900 ncu --set full --clock-control none -k regex:"stage_kernel|gradvisc" -s 80 -c 8 -o gpurun_out/prof_${TAG}_ns python bench.py --ns --steps 20 --warmup 20 --min-timed-s 0 --no-cpu-baseline --no-e2e > gpurun_out/ncu_${TAG}_ns.log 2>&1

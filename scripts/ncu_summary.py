@@ -85,6 +85,8 @@ def main():
     ap.add_argument("--tag", required=True)
     ap.add_argument("--launches")
     ap.add_argument("--bench-json", action="store_true")
+    ap.add_argument("--ns-json", action="store_true",
+                    help="Navier-Stokes capture (stage + gradient/viscous kernels): per-stage sums -> profiles/ncu_ns.json")
     ap.add_argument("--note", default="")
     a = ap.parse_args()
     res = summarise(a.rep, a.cells)
@@ -117,6 +119,16 @@ def main():
                    fp64_inst_per_cell_stage=sum(r["fp64_inst_per_cell_stage"] for r in res) / n,
                    fp64_pipe_pct=sum(r["fp64_pipe_pct"] for r in res) / n)
         with open(os.path.join(ROOT, "profiles", "ncu_stage_kernel.json"), "w") as fo:
+            json.dump(agg, fo, indent=1)
+    if a.ns_json:
+        # all kernels of the captured stages, summed per stage launch
+        nst = max(1, sum(1 for r in res if "stage_kernel" in r["kernel"]))
+        agg = dict(source=f"profiles/{a.tag}.json", cells=a.cells, stage_launches=nst,
+                   kernels=sorted({r["kernel"] for r in res}),
+                   dram_bytes_per_cell_stage=sum(r["dram_bytes_per_cell_stage"] for r in res) / nst,
+                   fp64_inst_per_cell_stage=sum(r["fp64_inst_per_cell_stage"] for r in res) / nst,
+                   fp64_pipe_pct=sum(r["fp64_pipe_pct"] for r in res) / len(res))
+        with open(os.path.join(ROOT, "profiles", "ncu_ns.json"), "w") as fo:
             json.dump(agg, fo, indent=1)
     print("\n".join(lines))
 
