@@ -9,7 +9,10 @@
 #include <unistd.h>
 
 #include <algorithm>
+#include <atomic>
 #include <chrono>
+#include <memory>
+#include <thread>
 #include <cmath>
 #include <deque>
 #include <cstdarg>
@@ -905,6 +908,22 @@ std::string edge_names(const sfv_ctx *c) {
 // comm_timeout seconds, aborts the communicator (unblocking the stream) and
 // returns SFV_ERR_NCCL naming this rank's edges and the pending step
 // instead of hanging.
+// Abort the communicator after a failure: ncclCommAbort runs on a detached
+// thread -- it unblocks the stream's NCCL kernels, but with a dead
+// peer it may itself wait on the transport, and the caller must get its
+// error within the timeout.  Bounded wait of 2 s for it here.
+void abort_comm(sfv_ctx *c) {
+    // (the step graphs stay: destroying an executable graph that still has
+    // launches in flight behind the stalled exchange would block here)
+    auto done = std::make_shared<std::atomic<bool>>(false);
+    ncclComm_t comm = c->comm;
+    std::thread([comm, done]() {
+        nccl().CommAbort(comm);
+        done->store(true);
+    }).detach();
+    for (int k = 0; k < 2000 && !done->load(); ++k) usleep(1000);
+}
+
 // Poll until the stream has drained (inflight < 0) or at most `inflight`
 // tracked steps are still pending, watching NCCL's async error and progress.
 sfv_status poll_wait(sfv_ctx *c, const char *what, long long inflight) {
@@ -933,8 +952,8 @@ sfv_status poll_wait(sfv_ctx *c, const char *what, long long inflight) {
             const long long pend = c->prog.empty() ? -1 : c->prog.front().second;
             const bool dbg = getenv("SFV_DEBUG_WAIT") != nullptr;
             if (dbg) fprintf(stderr, "[sfv] %s: async=%d idle=%.1fs pending step %lld: aborting\n", what, (int)ar, idle, pend);
-            N.CommAbort(c->comm);
-            if (dbg) fprintf(stderr, "[sfv] %s: communicator aborted\n", what);
+            abort_comm(c);
+            if (dbg) fprintf(stderr, "[sfv] %s: communicator abort issued\n", what);
             c->comm = nullptr;
             c->comm_dead = true;
             c->have_state = false;
@@ -984,6 +1003,21 @@ sfv_status agree_errors(sfv_ctx *c) {
     NK(N.AllReduce(c->halo_err, c->halo_err, 1, ncclUint32, ncclMax, c->comm, c->st));
     SYNC("error agreement");
     return SFV_OK;
+}
+
+// Block <-> full-grid host array ([j][i][4]): one contiguous copy when the
+// block spans the full width (single block, slabs along j), else a 2D copy.
+cudaError_t copy_block_h2d(const Block &b, const double *U, int NI, cudaStream_t st) {
+    const double *src = U + ((size_t)b.j0 * NI + b.i0) * 4;
+    if (b.ni == NI) return cudaMemcpyAsync(b.stage, src, (size_t)b.ni * b.nj * 32, cudaMemcpyHostToDevice, st);
+    return cudaMemcpy2DAsync(b.stage, (size_t)b.ni * 32, src, (size_t)NI * 32, (size_t)b.ni * 32, b.nj,
+                             cudaMemcpyHostToDevice, st);
+}
+cudaError_t copy_block_d2h(const Block &b, double *U, int NI, cudaStream_t st) {
+    double *dst = U + ((size_t)b.j0 * NI + b.i0) * 4;
+    if (b.ni == NI) return cudaMemcpyAsync(dst, b.stage, (size_t)b.ni * b.nj * 32, cudaMemcpyDeviceToHost, st);
+    return cudaMemcpy2DAsync(dst, (size_t)NI * 32, b.stage, (size_t)b.ni * 32, (size_t)b.ni * 32, b.nj,
+                             cudaMemcpyDeviceToHost, st);
 }
 
 sfv_status check_device_error(sfv_ctx *c, bool collective = false) {
@@ -1221,8 +1255,7 @@ sfv_status sfv_set_state(sfv_ctx *c, const double *U) {
     }
     CK(cudaMemsetAsync(c->err, 0xff, 8, st));
     for (Block &b : c->blocks) {
-        CK(cudaMemcpy2DAsync(b.stage, (size_t)b.ni * 32, U + ((size_t)b.j0 * NI + b.i0) * 4, (size_t)NI * 32,
-                             (size_t)b.ni * 32, b.nj, cudaMemcpyHostToDevice, st));
+        CK(copy_block_h2d(b, U, NI, st));
         CK(launch_scatter(b.stage, b.buf[0], b.ni, b.nj, b.PJ, st));
         for (int e = 0; e < 4; ++e) bcfill[e] = b.edge[e] == E_CONNECTED ? -1 : b.edge[e];
         for (int k = 0; k < nbuf; ++k) {
@@ -1302,8 +1335,10 @@ sfv_status sfv_step(sfv_ctx *c, int32_t nsteps) {
     }
     if (c->comm_dead) return fail(c, SFV_ERR_NCCL, "the NCCL communicator was aborted by an earlier failure");
     const bool track = c->nranks > 1 && c->comm;  // progress events for the deadlock timeout
+    const bool dbg = getenv("SFV_DEBUG_WAIT") != nullptr;
     for (int s = 0; s < nsteps; ++s) {
         const bool batch = (c->steps_enq + s + 1) % c->pring == 0;
+        if (dbg) fprintf(stderr, "[sfv] step %lld: launch (in flight %zu)\n", c->steps_enq + s, c->prog.size());
         if (c->gexec && !c->prof) {
             CK(cudaGraphLaunch(batch ? c->gexec_norms : c->gexec, c->st));
         } else {
@@ -1327,6 +1362,7 @@ sfv_status sfv_step(sfv_ctx *c, int32_t nsteps) {
             }
             CK(cudaEventRecord(ev, c->st));
             c->prog.emplace_back(ev, c->steps_enq + s);
+            if (dbg) fprintf(stderr, "[sfv] step %lld: recorded\n", c->steps_enq + s);
         }
     }
     CK(cudaEventRecord(c->ev1, c->st));
@@ -1445,8 +1481,7 @@ sfv_status sfv_get_state(sfv_ctx *c, double *U) {
     if (c->nranks == 1) {
         for (Block &b : c->blocks) {
             CK(launch_gather(b.buf[0], b.stage, b.ni, b.nj, b.PJ, c->st));
-            CK(cudaMemcpy2DAsync(U + ((size_t)b.j0 * NI + b.i0) * 4, (size_t)NI * 32, b.stage, (size_t)b.ni * 32,
-                                 (size_t)b.ni * 32, b.nj, cudaMemcpyDeviceToHost, c->st));
+            CK(copy_block_d2h(b, U, NI, c->st));
         }
         CK(cudaStreamSynchronize(c->st));
         return SFV_OK;
@@ -1739,8 +1774,10 @@ void sfv_destroy(sfv_ctx *c) {
     for (cudaEvent_t e : c->ev_pool) cudaEventDestroy(e);
     for (auto &sp : c->spans) { cudaEventDestroy(sp.a); cudaEventDestroy(sp.b); }
     for (cudaEvent_t e : c->tev_pool) cudaEventDestroy(e);
-    if (c->gexec) cudaGraphExecDestroy(c->gexec);
-    if (c->gexec_norms) cudaGraphExecDestroy(c->gexec_norms);
+    // after an aborted communicator the stream may never drain: the step graphs
+    // are left to the process teardown (destroying them would wait on it)
+    if (c->gexec && !c->comm_dead) cudaGraphExecDestroy(c->gexec);
+    if (c->gexec_norms && !c->comm_dead) cudaGraphExecDestroy(c->gexec_norms);
     if (c->ev0) cudaEventDestroy(c->ev0);
     if (c->ev1) cudaEventDestroy(c->ev1);
     if (c->ev_edge) cudaEventDestroy(c->ev_edge);

@@ -86,10 +86,13 @@ def lib():
         L.sfv_peer_connect.argtypes = [_VP, _VP]
         L.sfv_debug_block_buffer.argtypes = [_VP, C.c_int32, C.c_int32, _D]
         L.sfv_residual.argtypes = [_VP, _D, _D]
-        L.sfv_set_profiling.argtypes = [_VP, C.c_int32]
-        L.sfv_get_stage_timings.argtypes = [_VP, _D]
-        L.sfv_set_comm_timeout.argtypes = [_VP, C.c_double]
-        L.sfv_get_block_state.argtypes = [_VP, C.c_int32, _D]
+        # (round-2 entry points; an older library build -- A/B experiments
+        # via SFV_LIB -- may lack them, every other call still works)
+        for name, at in (("sfv_set_profiling", [_VP, C.c_int32]), ("sfv_get_stage_timings", [_VP, _D]),
+                         ("sfv_set_comm_timeout", [_VP, C.c_double]),
+                         ("sfv_get_block_state", [_VP, C.c_int32, _D])):
+            if hasattr(L, name):
+                getattr(L, name).argtypes = at
         L.sfv_last_error.argtypes = [_VP]
         L.sfv_last_error.restype = C.c_char_p
         L.sfv_destroy.argtypes = [_VP]

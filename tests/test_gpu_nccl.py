@@ -183,6 +183,7 @@ def _fault_worker(rank, world, port, mode, out_q):
         import faulthandler
         os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)
         logf = open(os.path.join(ROOT, "gpurun_out", "dead_peer_rank0.log"), "w")
+        os.dup2(logf.fileno(), 2)  # the library's SFV_DEBUG_WAIT trace goes to the same file
         faulthandler.dump_traceback_later(90, exit=False, file=logf)
         def note(m):
             logf.write(f"{time.time():.3f} {m}\n"); logf.flush()
