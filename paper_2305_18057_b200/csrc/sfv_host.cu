@@ -1254,8 +1254,18 @@ sfv_status sfv_set_state(sfv_ctx *c, const double *U) {
         CK(cudaMemsetAsync(c->halo_err, 0, sizeof(unsigned), st));
     }
     CK(cudaMemsetAsync(c->err, 0xff, 8, st));
+    // SFV_DEBUG_TIMING: host-side phase times of this call (diagnostic)
+    const bool tdbg = getenv("SFV_DEBUG_TIMING") != nullptr;
+    auto t_0 = std::chrono::steady_clock::now();
+    auto tmark = [&](const char *what) {
+        if (!tdbg) return;
+        cudaStreamSynchronize(st);
+        fprintf(stderr, "[sfv] set_state %s: %.3f ms\n", what,
+                std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_0).count());
+    };
     for (Block &b : c->blocks) {
         CK(copy_block_h2d(b, U, NI, st));
+        tmark("h2d");
         CK(launch_scatter(b.stage, b.buf[0], b.ni, b.nj, b.PJ, st));
         for (int e = 0; e < 4; ++e) bcfill[e] = b.edge[e] == E_CONNECTED ? -1 : b.edge[e];
         for (int k = 0; k < nbuf; ++k) {
@@ -1264,6 +1274,7 @@ sfv_status sfv_set_state(sfv_ctx *c, const double *U) {
         }
         CK(launch_check_state(b.buf[0], b.ni, b.nj, b.PJ, b.i0, b.j0, NI, c->err, st));
     }
+    tmark("ghosts + check");
     sfv_status r = exchange(c, 0, st);
     if (r != SFV_OK) return r;
     CK(cudaMemsetAsync(c->sig, 0, 24, st));  // sig[2], step counter
@@ -1290,6 +1301,7 @@ sfv_status sfv_set_state(sfv_ctx *c, const double *U) {
         for (int r = 0; r < c->nranks; ++r)
             CK(cudaMemcpyAsync(c->sig_tab + r, c->sig, sizeof(double), cudaMemcpyDeviceToDevice, st));
     SYNC("sfv_set_state");
+    tmark("dt_0 (done)");
     c->steps_enq = 0;
     c->have_state = true;
     c->timing_open = false;

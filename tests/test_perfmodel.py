@@ -63,3 +63,26 @@ def test_multi_gpu_is_max_over_ranks():
     skew = M.blocks_of(11520, 5760, 8, 1, wx=[4, 1, 1, 1, 1, 1, 1, 1])
     assert m.multi_gpu_step(skew) > m.multi_gpu_step(even)
     assert m.multi_gpu_step(even) == pytest.approx(m.stages * m.block_stage(even[0]))
+
+
+def test_closure_script_predicts_and_calibrates_alpha(tmp_path):
+    """scripts/perfmodel_closure.py (SURVEY §8(f) f3 closure): every bench line
+    in a file gets the launch-geometry model's prediction for its slab
+    decomposition; alpha (Eq. 12) comes from the line's measured halo time
+    (config.halo_measured: slab alone vs in the N-rank run)."""
+    import json
+    import os
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    sys.path.insert(0, os.path.join(root, "scripts"))
+    import perfmodel_closure as PC
+    line = {"metric": "m", "value": 1.0, "n_gpus": 4, "ms_per_step": 3.0,
+            "config": {"workload": "C3 strong scaling, 11520x5760 = 66,355,200 cells", "global_cells": 66355200,
+                       "rk_stages": 4, "halo_measured": {"slab_alone_ms_per_step_max": 2.5}}}
+    f = tmp_path / "scale.json"
+    f.write_text(json.dumps({"runs": [{"stdout_tail": "== bench\n" + json.dumps(line) + "\n"}]}))
+    sys.argv = ["perfmodel_closure.py", str(f)]
+    rows = PC.main()
+    assert len(rows) == 1 and rows[0]["n"] == 4 and rows[0]["grid"] == "11520x5760"
+    assert abs(rows[0]["alpha"] - (3.0 / 2.5 - 1.0)) < 1e-12
+    assert rows[0]["predicted_ms"] > 0 and rows[0]["predicted_alpha_ms"] > rows[0]["predicted_ms"]
