@@ -1125,9 +1125,7 @@ cudaError_t stage_occupancy_visc(int mode, bool norms, bool dtmax, bool fast, in
     const bool peer = false, visc = true;
     SFV_DISPATCH(occ_t, n)
 }
-cudaError_t prepare_gradvisc3_kernel();
 cudaError_t prepare_stage_kernels() {
-    if (cudaError_t e = prepare_gradvisc3_kernel(); e != cudaSuccess) return e;
     const int variants[9][3] = {{M_OWN, 1, 0}, {M_OWN, 0, 0}, {M_UN, 0, 0}, {M_UN, 0, 1},  {M_RK4F, 0, 1},
                                 {M_RK4F, 0, 0}, {M_HEUNF, 0, 1}, {M_HEUNF, 0, 0}, {M_RES, 0, 0}};
     for (auto &v : variants)
@@ -1227,34 +1225,16 @@ __device__ __forceinline__ double *gradp(double *grad, int PG, int i, int j, int
 
 // Green-Gauss gradient (reading N-R2) of cell (i, j) from the (u, v, T) of
 // the cell and its 4 face neighbours; faces: the mean of the two cells times A
-// metric accessors (row, field, column) -> value: the block's metrics in global
-// memory, or a tile of them staged in shared memory (same values, so the
-// same arithmetic gives bitwise the same results)
-struct GMet {
-    const double *met;
-    int PJ;
-    __device__ __forceinline__ double operator()(int row, int f, int j) const { return metf(met, PJ, row, f, j); }
-};
-template <int MPJ>
-struct SMet {
-    const double *s;  // [rows][NMET][MPJ], local row = row - r0, column = j - c0
-    int r0, c0;
-    __device__ __forceinline__ double operator()(int row, int f, int j) const {
-        return s[((row - r0) * NMET + f) * MPJ + (j - c0)];
-    }
-};
-
-template <class M>
-__device__ __forceinline__ void gg_cell_m(const M &met, int i, int j, const double c[3], const double w[3],
-                                          const double e[3], const double s[3], const double n[3], double g[6]) {
+__device__ __forceinline__ void gg_cell(const double *met, int PJ, int i, int j, const double c[3], const double w[3],
+                                        const double e[3], const double s[3], const double n[3], double g[6]) {
     // per face: n A / (2 V), so grad = sum_f (phi_L + phi_R) n A / (2 V) with outward signs
-    const double h = met(i + 1, 6, j);  // (the metrics hold A/2)
-    const double hW = DM(met(i, 2, j), h), hE = DM(met(i + 1, 2, j), h);
-    const double hS = DM(met(i + 1, 5, j), h), hN = DM(met(i + 1, 5, j + 1), h);
-    const double kWx = DM(met(i, 0, j), hW), kWy = DM(met(i, 1, j), hW);
-    const double kEx = DM(met(i + 1, 0, j), hE), kEy = DM(met(i + 1, 1, j), hE);
-    const double kSx = DM(met(i + 1, 3, j), hS), kSy = DM(met(i + 1, 4, j), hS);
-    const double kNx = DM(met(i + 1, 3, j + 1), hN), kNy = DM(met(i + 1, 4, j + 1), hN);
+    const double h = metf(met, PJ, i + 1, 6, j);  // (the metrics hold A/2)
+    const double hW = DM(metf(met, PJ, i, 2, j), h), hE = DM(metf(met, PJ, i + 1, 2, j), h);
+    const double hS = DM(metf(met, PJ, i + 1, 5, j), h), hN = DM(metf(met, PJ, i + 1, 5, j + 1), h);
+    const double kWx = DM(metf(met, PJ, i, 0, j), hW), kWy = DM(metf(met, PJ, i, 1, j), hW);
+    const double kEx = DM(metf(met, PJ, i + 1, 0, j), hE), kEy = DM(metf(met, PJ, i + 1, 1, j), hE);
+    const double kSx = DM(metf(met, PJ, i + 1, 3, j), hS), kSy = DM(metf(met, PJ, i + 1, 4, j), hS);
+    const double kNx = DM(metf(met, PJ, i + 1, 3, j + 1), hN), kNy = DM(metf(met, PJ, i + 1, 4, j + 1), hN);
 #pragma unroll
     for (int q = 0; q < 3; ++q) {
         const double sE = DA(c[q], e[q]), sW = DA(w[q], c[q]), sN = DA(c[q], n[q]), sS = DA(s[q], c[q]);
@@ -1262,10 +1242,6 @@ __device__ __forceinline__ void gg_cell_m(const M &met, int i, int j, const doub
         g[2 * q] = fma(-sS, kSx, fma(sN, kNx, fma(-sW, kWx, DM(sE, kEx))));
         g[2 * q + 1] = fma(-sS, kSy, fma(sN, kNy, fma(-sW, kWy, DM(sE, kEy))));
     }
-}
-__device__ __forceinline__ void gg_cell(const double *met, int PJ, int i, int j, const double c[3], const double w[3],
-                                        const double e[3], const double s[3], const double n[3], double g[6]) {
-    gg_cell_m(GMet{met, PJ}, i, j, c, w, e, s, n, g);
 }
 
 __global__ void grad_kernel(const ViscArgs a) {
@@ -1414,112 +1390,7 @@ __global__ void __launch_bounds__(VT_J * VT_I) gradvisc_kernel(const ViscArgs a)
     store_rv(a, i, j, FW, FE, FS, FN);
 }
 
-#ifndef SFV_GV_STAGED
-#define SFV_GV_STAGED 1  // fused NS kernel with the tile's metrics and state staged first (batched loads)
-#endif
-// Staged variant of gradvisc_kernel: the tile's metrics (15 rows x 7 fields
-// x 35 columns) and state (tile + 2 rings) are loaded in one batch of
-// independent coalesced loads before any use, so their latency is exposed
-// once per CTA instead of per cell (round-1 ncu: long-scoreboard 4.0 stalls
-// per issue); everything after reads shared memory.  Same per-cell / per-face
-// arithmetic and arguments: bitwise equal to gradvisc_kernel and the
-// two-kernel path.
-constexpr int GM_R = VT_I + 3, GM_C = VT_J + 3;  // metric rows i0-1 .. i0+VT_I+1, columns j0-1 .. j0+VT_J+1
-constexpr size_t GV3_SMEM = sizeof(double) * ((size_t)VP_I * VP_J * 3 + (size_t)VG_I * VG_J * 7 +
-                                              (size_t)GM_R * NMET * GM_C);
-constexpr int GV3_NM = (GM_R * NMET * GM_C + VT_J * VT_I - 1) / (VT_J * VT_I);  // metric loads per thread
-constexpr int GV3_NS = (VP_I * VP_J + VT_J * VT_I - 1) / (VT_J * VT_I);        // state cells per thread
-
-__global__ void __launch_bounds__(VT_J * VT_I) gradvisc3_kernel(const ViscArgs a) {
-    constexpr int NTH = VT_J * VT_I;
-    extern __shared__ __align__(16) double gv3[];
-    auto pr = reinterpret_cast<double (*)[VP_J][3]>(gv3);
-    auto gs = reinterpret_cast<double (*)[VG_J][7]>(gv3 + VP_I * VP_J * 3);
-    double *ms = gv3 + VP_I * VP_J * 3 + VG_I * VG_J * 7;
-    const int i0 = blockIdx.y * VT_I, j0 = blockIdx.x * VT_J;
-    const int tid = threadIdx.y * VT_J + threadIdx.x;
-    // ---- one batch of loads: metrics tile and state tile (independent)
-    double mv[GV3_NM];
-#pragma unroll
-    for (int q = 0; q < GV3_NM; ++q) {
-        const int e = tid + q * NTH;
-        mv[q] = 0.0;
-        if (e < GM_R * NMET * GM_C) {
-            const int c = e % GM_C, rf = e / GM_C, f = rf % NMET, r = rf / NMET;
-            const int row = i0 - 1 + r, col = j0 - 1 + c;
-            if (row >= 0 && row <= a.ni && col >= -1 && col <= a.nj + 1) mv[q] = metf(a.met, a.PJ, row, f, col);
-        }
-    }
-    double sv[GV3_NS][4];
-    bool sok[GV3_NS];
-#pragma unroll
-    for (int q = 0; q < GV3_NS; ++q) {
-        const int k = tid + q * NTH;
-        const int ti = k / VP_J, tj = k % VP_J, i = i0 - 2 + ti, j = j0 - 2 + tj;
-        const bool iin = i >= 0 && i < a.ni, jin = j >= 0 && j < a.nj;
-        sok[q] = k < VP_I * VP_J && i >= -2 && i < a.ni + 2 && j >= -2 && j < a.nj + 2 && (iin || jin);
-        if (sok[q]) {
-            const double *p = a.in + (size_t)((i + 2) * 4) * a.PJ + (j + JOFF);
-#pragma unroll
-            for (int c = 0; c < 4; ++c) sv[q][c] = p[(size_t)c * a.PJ];
-        }
-    }
-#pragma unroll
-    for (int q = 0; q < GV3_NM; ++q)
-        if (tid + q * NTH < GM_R * NMET * GM_C) ms[tid + q * NTH] = mv[q];
-#pragma unroll
-    for (int q = 0; q < GV3_NS; ++q) {
-        const int k = tid + q * NTH;
-        if (sok[q]) uvT_core(sv[q][0], sv[q][1], sv[q][2], sv[q][3], a.P, pr[k / VP_J][k % VP_J]);
-    }
-    __syncthreads();
-    const SMet<GM_C> M{ms, i0 - 1, j0 - 1};
-    // gradients of interior cells i0-1 .. i0+VT_I, j0-1 .. j0+VT_J
-    for (int k = tid; k < VG_I * VG_J; k += NTH) {
-        const int ti = k / VG_J, tj = k % VG_J, i = i0 - 1 + ti, j = j0 - 1 + tj;
-        if (i >= 0 && i < a.ni && j >= 0 && j < a.nj)
-            gg_cell_m(M, i, j, pr[ti + 1][tj + 1], pr[ti][tj + 1], pr[ti + 2][tj + 1], pr[ti + 1][tj],
-                      pr[ti + 1][tj + 2], gs[ti][tj]);
-    }
-    __syncthreads();
-    // physical ghost ring inside the gradient region: the adjacent interior cell's
-    for (int k = tid; k < VG_I * VG_J; k += NTH) {
-        const int ti = k / VG_J, tj = k % VG_J, i = i0 - 1 + ti, j = j0 - 1 + tj;
-        const bool iin = i >= 0 && i < a.ni, jin = j >= 0 && j < a.nj;
-        if (iin == jin) continue;
-        if (!iin && (i == -1 || i == a.ni) && jin) {
-            const int si = i < 0 ? ti + 1 : ti - 1;
-            for (int q = 0; q < 6; ++q) gs[ti][tj][q] = gs[si][tj][q];
-        } else if (!jin && (j == -1 || j == a.nj) && iin) {
-            const int sj = j < 0 ? tj + 1 : tj - 1;
-            for (int q = 0; q < 6; ++q) gs[ti][tj][q] = gs[ti][sj][q];
-        }
-    }
-    __syncthreads();
-    const int i = i0 + threadIdx.y, j = j0 + threadIdx.x;
-    if (i >= a.ni || j >= a.nj) return;
-    const int ti = threadIdx.y + 1, tj = threadIdx.x + 1;
-    const double *c = pr[ti + 1][tj + 1];
-    double FW[4], FE[4], FS[4], FN[4];
-    face_visc_core(gs[ti - 1][tj], gs[ti][tj], pr[ti][tj + 1], c, M(i, 0, j), M(i, 1, j), M(i, 2, j), a.P, FW);
-    face_visc_core(gs[ti][tj], gs[ti + 1][tj], c, pr[ti + 2][tj + 1], M(i + 1, 0, j), M(i + 1, 1, j), M(i + 1, 2, j),
-                   a.P, FE);
-    face_visc_core(gs[ti][tj - 1], gs[ti][tj], pr[ti + 1][tj], c, M(i + 1, 3, j), M(i + 1, 4, j), M(i + 1, 5, j),
-                   a.P, FS);
-    face_visc_core(gs[ti][tj], gs[ti][tj + 1], c, pr[ti + 1][tj + 2], M(i + 1, 3, j + 1), M(i + 1, 4, j + 1),
-                   M(i + 1, 5, j + 1), a.P, FN);
-    store_rv(a, i, j, FW, FE, FS, FN);
-}
-
-cudaError_t prepare_gradvisc3_kernel() {  // (at sfv_bind, outside any stream capture)
-    return cudaFuncSetAttribute(gradvisc3_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)GV3_SMEM);
-}
-
 cudaError_t launch_gradvisc(const ViscArgs &v, cudaStream_t st) {
-    if (SFV_GV_STAGED) {
-        gradvisc3_kernel<<<dim3((v.nj + VT_J - 1) / VT_J, (v.ni + VT_I - 1) / VT_I), dim3(VT_J, VT_I), GV3_SMEM, st>>>(v);
-        return cudaGetLastError();
-    }
     gradvisc_kernel<<<dim3((v.nj + VT_J - 1) / VT_J, (v.ni + VT_I - 1) / VT_I), dim3(VT_J, VT_I), 0, st>>>(v);
     return cudaGetLastError();
 }
