@@ -388,10 +388,15 @@ def main():
     else:
         warm()
 
+    # host-side barrier (gloo): a rank waiting in it leaves no NCCL kernel spinning on
+    # its GPU (with simulated ranks sharing one GPU such a kernel would time-slice
+    # against the rank that is measuring)
+    cpu_group = dist.new_group(backend="gloo") if world > 1 else None
+
     def barrier():
         torch.cuda.synchronize(dev)
         if world > 1:
-            dist.barrier()
+            dist.barrier(group=cpu_group)
 
     # ---- device-timed region (inputs resident in HBM) ----
     # R repeats of exactly K steps (each bracketed by barrier + sync, CUDA

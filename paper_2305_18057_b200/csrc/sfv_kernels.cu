@@ -124,6 +124,9 @@ __device__ __forceinline__ double frcp(double d) {
     double e = fma(-d, y, 1.0);
     return fma(y, fma(e, e, e), y);
 }
+#ifndef SFV_DIET
+#define SFV_DIET 0  // FP64 diet v2: limiter max-form, rho tests folded into a~^2 > 0, |x| by a sign-bit mask
+#endif
 #ifndef SFV_LIM_RCP2
 #define SFV_LIM_RCP2 1
 #endif
@@ -169,6 +172,14 @@ __device__ __forceinline__ unsigned long long err_key(long long n, int nstages, 
 template <bool FAST>
 __device__ __forceinline__ void muscl_cell(double w, double b, double f, const Params &P, double &qU,
                                            double &qD) {
+    if constexpr (FAST && SFV_DIET) {
+        // eps = 1 (c1 = 1/2): s1 = max(0, (bf + d/2) / (b^2+f^2+d)); qU = w + s1 b, qD = w - s1 f
+        const double r = frcp_lim(fma(b, b, fma(f, f, P.delta)));
+        const double s1 = fmax(fma(b, f, P.c1dh + P.c1dh) * r, 0.0);  // c1dh = delta/4 when eps = 1
+        qU = fma(s1, b, w);
+        qD = fma(-s1, f, w);
+        return;
+    }
     if constexpr (FAST) {
         // bounded van Albada, kappa = -1 (c2 = 0): s1 = c1 max(0, (2bf+d)/(b^2+f^2+d))
         //   qU = w + s1 b,  qD = w - s1 f
@@ -203,6 +214,10 @@ __device__ __forceinline__ void muscl_cell(double w, double b, double f, const P
 }
 
 // ------------------------------------------------- Roe + Harten face flux
+// |x| by clearing the sign bit (integer pipe; fabs as a value costs a DADD)
+__device__ __forceinline__ double dabs(double x) {
+    return __longlong_as_double(__double_as_longlong(x) & 0x7fffffffffffffffLL);
+}
 // Flux through a face of area A with unit normal (nx, ny), times A
 // (eigenvector form re-associated into the compact
 // dissipation form; Roe averages with sqrt(rho) weights from one rsqrt per
@@ -227,7 +242,9 @@ __device__ __forceinline__ bool roe_flux(const double qL[4], const double qR[4],
     const double rhot = sL * sR;
     const double q2h = 0.5 * fma(ut, ut, vt * vt);
     const double a2 = gm1 * (Ht - q2h);
-    const bool ok = (qL[0] > 0.0) & (qR[0] > 0.0) & (pL > 0.0) & (pR > 0.0) & (a2 > 0.0);
+    // (rho <= 0 makes the rsqrt NaN or inf, hence a2 NaN: the a2 test covers it)
+    const bool ok = SFV_DIET ? ((pL > 0.0) & (pR > 0.0) & (a2 > 0.0))
+                             : ((qL[0] > 0.0) & (qR[0] > 0.0) & (pL > 0.0) & (pR > 0.0) & (a2 > 0.0));
     const double ra = frsqrt(a2);
     const double at = a2 * ra;
     const double ia2 = ra * ra;
@@ -240,9 +257,9 @@ __device__ __forceinline__ bool roe_flux(const double qL[4], const double qR[4],
     const double a4 = (dp + tt) * hia2;
     const double a2w = fma(-dp, ia2, drho);
 
-    double l1 = fabs(Vnt - at);
+    double l1 = SFV_DIET ? dabs(Vnt - at) : fabs(Vnt - at);
     const double l2 = fabs(Vnt);
-    double l4 = fabs(Vnt + at);
+    double l4 = SFV_DIET ? dabs(Vnt + at) : fabs(Vnt + at);
     double dH = P.heps * at;
     const bool floor_h = dH < 1e-12;
     const double inv2dH = floor_h ? 0.5e12 : P.hinv * ra;  // 1/(2 eps a) = (0.5/eps) (1/a)
@@ -1111,7 +1128,7 @@ static cudaError_t occ_t(int *n) {
     }
 
 // fast = bounded van Albada with kappa = -1 (the default scheme, reading A-R3/A-R7)
-bool fast_path(const Params &P) { return P.limiter == 1 && P.c2 == 0.0; }
+bool fast_path(const Params &P) { return P.limiter == 1 && P.c2 == 0.0 && (!SFV_DIET || P.c1 == 0.5); }
 cudaError_t launch_stage(const StageArgs &a, int mode, bool norms, bool dtmax, bool peer, bool visc,
                          cudaStream_t st) {
     const bool fast = fast_path(a.P);

@@ -20,7 +20,8 @@ from paper_2305_18057_b200 import inputs as I, sfv  # noqa: E402
 from parity_util import norm_error, state_error  # noqa: E402
 
 CASES = [("C1_wedge", 64, 32, 15.0, None), ("inlet256_seed0", 256, 128, 30.0, 0),
-         ("inlet256_seed1", 256, 128, 30.0, 1), ("inlet256_seed2", 256, 128, 30.0, 2)]
+         ("inlet256_seed1", 256, 128, 30.0, 1), ("inlet256_seed2", 256, 128, 30.0, 2),
+         ("C2_full_freestream", 1440, 720, 30.0, None)]  # the bench workload itself (oracle: -fopenmp build)
 
 
 def ulp_nudge(U):
@@ -31,15 +32,17 @@ def ulp_nudge(U):
 
 def main():
     only = sys.argv[1:]
+    os.environ.setdefault("OMP_NUM_THREADS", str(len(os.sched_getaffinity(0))))
     for name, ni, nj, th, seed in CASES:
         if only and name not in only:
             continue
         X, Y = I.ramp_nodes(ni, nj, th)
         cfg = I.default_config(ni, nj)
         U0 = I.uniform_state(ni, nj) if seed is None else I.perturbed_state(ni, nj, seed)
+        big = ni * nj > 100000  # the bitwise-equal OpenMP oracle build on every host core
         g = sfv.Solver(cfg, X, Y); g.set_state(U0)
-        o = oracle.Oracle(cfg, X, Y); o.set_state(U0)
-        s = oracle.Oracle(cfg, X, Y); s.set_state(ulp_nudge(U0))
+        o = oracle.Oracle(cfg, X, Y, omp=big); o.set_state(U0)
+        s = oracle.Oracle(cfg, X, Y, omp=big); s.set_state(ulp_nudge(U0))
         done, rec = 0, {"case": name, "lib": os.path.basename(os.environ.get("SFV_LIB", "libsfv.so"))}
         for n in (1, 100, 1000):
             g.step(n - done); g.sync(); o.step(n - done); s.step(n - done); done = n
