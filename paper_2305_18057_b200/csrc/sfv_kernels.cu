@@ -95,6 +95,14 @@ __device__ __forceinline__ unsigned long long globaltimer_ns() {
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
     return t;
 }
+#ifndef SFV_TIMELINE
+#define SFV_TIMELINE 0  // diagnostic build: per-task globaltimer stamps of the stage kernel (scripts/timeline.py)
+#endif
+#if SFV_TIMELINE
+// [stage slot 0..7][task][10]: entry, after griddepcontrol.wait, first flux data ready, loop end,
+// smid | warpid << 16, rows, stamps at rows i_start+4, +8, +12, +16 (first segment)
+__device__ unsigned long long g_timeline[8][8192][10];
+#endif
 constexpr unsigned long long HALO_TIMEOUT_NS = 20ull * 1000 * 1000 * 1000;
 // Wait (all lanes) until the neighbour has published stage sequence >= need
 // for this edge, then make its data visible to the async (TMA) proxy.  A
@@ -507,6 +515,10 @@ __global__ void __launch_bounds__(NT, StageTraits<MODE>::MINW / WPC) stage_kerne
             mbar_wait_s(mbar_s + 8u * ((unsigned)(r - m0) % TR::MS), ((unsigned)(r - m0) / TR::MS) & 1u);
         };
 
+#if SFV_TIMELINE
+        const unsigned long long tl_entry = globaltimer_ns();
+        unsigned long long tl_ready = 0, tl_first = 0, tl_row[4] = {0, 0, 0, 0};
+#endif
         if (lane == 0) {
             for (int s = 0; s < TR::NBAR; ++s) mbar_init(&wbar[s], 1);
             asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -520,6 +532,9 @@ __global__ void __launch_bounds__(NT, StageTraits<MODE>::MINW / WPC) stage_kerne
         // its waiting CTAs cannot hold slots this grid still needs
         pdl_launch_dependents();
         read_step();
+#if SFV_TIMELINE
+        tl_ready = globaltimer_ns();
+#endif
         if constexpr (PEER) {
             // the stage input's ghost layers on a peer edge are the neighbour's
             // previous-stage edge layers: wait for its signal (sequence n*s + k - 1)
@@ -557,6 +572,9 @@ __global__ void __launch_bounds__(NT, StageTraits<MODE>::MINW / WPC) stage_kerne
         for (int r = r0 + TR::WS; r <= r0 + TR::WS + 1 && r <= r_last; ++r) issue_w(r);
         wait_w(r0 + 3);
         wait_m(m0);
+#if SFV_TIMELINE
+        tl_first = globaltimer_ns();
+#endif
         {
             const double *s3 = wslot(r0 + 3);
             const double *m = mslot(m0);
@@ -610,6 +628,9 @@ __global__ void __launch_bounds__(NT, StageTraits<MODE>::MINW / WPC) stage_kerne
 #endif
 #pragma unroll kRowUnroll
         for (int v = i_start; v < i_end; ++v) {
+#if SFV_TIMELINE
+            if (((v - i_start) & 3) == 0 && v > i_start && v - i_start <= 16) tl_row[(v - i_start) / 4 - 1] = globaltimer_ns();
+#endif
             // NS: this row's viscous sum, loaded before the fluxes so the load
             // latency hides behind them
             double rvv[CPL][4];
@@ -914,6 +935,17 @@ __global__ void __launch_bounds__(NT, StageTraits<MODE>::MINW / WPC) stage_kerne
                 }
             }
         }
+#if SFV_TIMELINE
+        if (lane == 0 && task < 8192) {
+            unsigned smid, wid;
+            asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+            asm volatile("mov.u32 %0, %%warpid;" : "=r"(wid));
+            unsigned long long *tl = g_timeline[(a.stage - 1) & 7][task];
+            tl[0] = tl_entry; tl[1] = tl_ready; tl[2] = tl_first; tl[3] = globaltimer_ns();
+            tl[4] = smid | (wid << 16); tl[5] = (unsigned long long)(i_end - i_start);
+            for (int q = 0; q < 4; ++q) tl[6 + q] = tl_row[q];
+        }
+#endif
         if constexpr (TR::PARK && NORMS) {
 #pragma unroll
             for (int k = 0; k < CPL; ++k)
@@ -1639,3 +1671,11 @@ cudaError_t launch_debug_math(int which, const double *in, double *out, long lon
 }
 
 }  // namespace sfv
+
+#if SFV_TIMELINE
+// diagnostic export (timeline builds only; not part of include/sfv.h)
+extern "C" int sfv_debug_timeline(void *host, unsigned long long bytes) {
+    if (bytes > sizeof(sfv::g_timeline)) bytes = sizeof(sfv::g_timeline);
+    return (int)cudaMemcpyFromSymbol(host, sfv::g_timeline, bytes);
+}
+#endif
