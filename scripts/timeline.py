@@ -37,8 +37,10 @@ for s in range(4):
     T = T[:n].astype(np.int64)
     t0 = T[:, 0].min()
     e, r, f, x = (T[:, k] - t0 for k in range(4))
-    rows = T[:, 5]
-    line = (f"stage {s+1}: tasks {n} rows {rows.min()}-{rows.max()} | entry span {e.max()/1e3:.2f} us | "
+    rows = T[:, 5] & 0xffffffff
+    nsegs = T[:, 5] >> 32
+    line = (f"stage {s+1}: tasks {n} rows {rows.min()}-{rows.max()} segs/task max {nsegs.max()} "
+            f"(steals {int((nsegs - 1).clip(0).sum())}) | entry span {e.max()/1e3:.2f} us | "
             f"ready min/med/max {r.min()/1e3:.2f}/{np.median(r)/1e3:.2f}/{r.max()/1e3:.2f} | "
             f"fill (ready->first) med {np.median(f-r)/1e3:.2f} max {(f-r).max()/1e3:.2f} | "
             f"end min/med/max {x.min()/1e3:.2f}/{np.median(x)/1e3:.2f}/{x.max()/1e3:.2f} us")
