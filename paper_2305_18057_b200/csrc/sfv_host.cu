@@ -107,6 +107,9 @@ struct Block {
     // exchanged while the interior runs), then the interior rows
     int nlaunch = 1, row_lo[3] = {0, 0, 0}, row_hi[3] = {0, 0, 0}, lseg[3] = {1, 1, 1}, lbase[3] = {0, 0, 0};
     int lsegF[3] = {1, 1, 1};  // segments per launch part for the RK4 final stage (its own occupancy)
+    // trailing short segments of a single-wave launch, per
+    // occupancy class (0: main, 1: RK4 final stage): nstrips x tseg2 tasks over rows [tsplit, ni)
+    int tseg2[2] = {0, 0}, tsplit[2] = {0, 0};
     int ncta_total = 1;
     bool split = false;
     double *buf[4] = {nullptr, nullptr, nullptr, nullptr};
@@ -368,6 +371,26 @@ void plan_launches(sfv_ctx *c, Block &b) {
     }
     b.ncta_total = base;
     b.nseg = b.lseg[n - 1];
+    // trailing short segments (single launch, single wave): the first wave's
+    // segments cover rows [0, tsplit); the last SFV_TAIL_FRAC of the rows go
+    // into segments of ~SFV_TAIL_ROWS rows that the CTA scheduler places in
+    // the slots of the first warps to finish
+    const char *ef = getenv("SFV_TAIL_FRAC"), *er = getenv("SFV_TAIL_ROWS");
+    const double frac = ef ? atof(ef) : 0.10;  // measured optimum on C2 (profiles/r2b_ab_tail_segments.txt)
+    const int trows = std::max(2, er ? atoi(er) : 4);
+    for (int q = 0; q < 2; ++q) {
+        b.tseg2[q] = 0;
+        b.tsplit[q] = b.ni;
+        const int nseg = q ? b.lsegF[0] : b.lseg[0];
+        const long long slots = (long long)c->nsm * std::max(1, q ? c->occ_f : c->occ) * WPC;
+        const int tail = (int)std::lround(frac * b.ni);
+        if (n != 1 || frac <= 0.0 || (long long)b.nstrips * nseg > slots || tail < 2 * trows ||
+            b.ni - tail < 4 * nseg)
+            continue;
+        b.tseg2[q] = std::min(tail / trows, NSEG_MAX - nseg);
+        b.tsplit[q] = b.tseg2[q] > 0 ? b.ni - tail : b.ni;
+    }
+    b.ncta_total = std::max(b.ncta_total, b.nstrips * (b.lseg[0] + b.tseg2[0]));
 }
 
 sfv_status build_blocks(sfv_ctx *c) {
@@ -605,6 +628,8 @@ StageArgs make_args(sfv_ctx *c, Block &b, int k) {
     a.nseg = b.nseg;
     a.row_lo = 0;
     a.row_hi = b.ni;
+    a.row_split = b.ni;
+    a.nseg2 = 0;
     a.part_base = 0;
     a.part_stride = b.ncta_total;
     for (int e = 0; e < 4; ++e) a.bc[e] = b.edge[e];
@@ -819,6 +844,12 @@ sfv_status enqueue_step(sfv_ctx *c, cudaStream_t st, bool norms_batch) {
             a.row_lo = b.row_lo[q];
             a.row_hi = b.row_hi[q];
             a.nseg = sp.mode == M_RK4F ? b.lsegF[q] : b.lseg[q];
+            {
+                const int cls = sp.mode == M_RK4F ? 1 : 0;
+                const bool tail = b.nlaunch == 1 && c->halo != SFV_HALO_PEER;
+                a.nseg2 = tail ? b.tseg2[cls] : 0;
+                a.row_split = a.nseg2 > 0 ? b.tsplit[cls] : a.row_hi;
+            }
             a.part_base = b.lbase[q];
             for (int e = 0; e < 4; ++e) a.edge_writers[e] = a.peer_out[e] ? edge_writers(b, a.nseg, e) : 0;
             CK(launch_stage(a, sp.mode, k == 1, k == s && cflmode, c->halo == SFV_HALO_PEER, c->cfg.viscous != 0, st));
@@ -1279,6 +1310,10 @@ sfv_status sfv_set_state(sfv_ctx *c, const double *U) {
     if (r != SFV_OK) return r;
     CK(cudaMemsetAsync(c->sig, 0, 24, st));  // sig[2], step counter
     CK(cudaMemsetAsync(c->done, 0, sizeof(unsigned), st));
+    // norm partials: columns a launch configuration does not write (trailing
+    // segments off in peer mode) must read as zero
+    for (Block &b : c->blocks)
+        CK(cudaMemsetAsync(b.partials, 0, sizeof(double) * 8 * (size_t)b.ncta_total * c->pring, st));
     CK(cudaMemsetAsync(c->dt_hist, 0, sizeof(double) * c->cfg.max_history, st));
     CK(cudaMemsetAsync(c->norm_hist, 0, sizeof(double) * c->cfg.max_history * c->nblocks_total * 8, st));
     SYNC("sfv_set_state");

@@ -62,6 +62,7 @@ struct StageArgs {
     int gi0, gj0, NI, NJ;
     int nstrips, nseg;
     int row_lo, row_hi;     // rows of this launch (edge strips / interior split)
+    int row_split, nseg2;   // trailing short segments: nseg over [row_lo, row_split), nseg2 over [row_split, row_hi)
     int part_base, part_stride;  // column range of this launch in the norm partials
     int bc[4];              // Edge per W, E, S, N
     double coef;            // this stage's dt multiplier

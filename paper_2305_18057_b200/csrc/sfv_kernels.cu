@@ -429,10 +429,18 @@ __global__ void __launch_bounds__(NT, StageTraits<MODE>::MINW / WPC) stage_kerne
     double nrm[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     double smax = 0.0;
 
+    // warp tasks: nstrips x nseg segments of rows [row_lo, row_split), then
+    // (single-wave launches) nstrips x nseg2 short trailing segments of
+    // [row_split, row_hi) that the CTA scheduler hands to the slots the
+    // first-finishing warps free (the per-sub-partition issue
+    // priority makes equal segments end over a wide spread)
     const int task = blockIdx.x * WPC + warp;
-    if (task < a.nstrips * a.nseg) {
-        const int strip = task % a.nstrips;
-        const int seg = task / a.nstrips;
+    const int ntask1 = a.nstrips * a.nseg;
+    if (task < ntask1 + a.nstrips * a.nseg2) {
+        const bool trailing = task >= ntask1;
+        const int tt = trailing ? task - ntask1 : task;
+        const int strip = tt % a.nstrips;
+        const int seg = tt / a.nstrips;
         const int j0 = strip * WOUT;
         const int j1 = min(j0 + WOUT, a.nj);
         const int jc = j0 - 1 + CPL * lane;          // this lane's first column (CPL columns per lane)
@@ -452,9 +460,10 @@ __global__ void __launch_bounds__(NT, StageTraits<MODE>::MINW / WPC) stage_kerne
         // whose staged columns reach j = -1 / nj
         const bool ghost_sn = (writes_ghost(2) && j0 == 0) || (writes_ghost(3) && j1 >= a.nj - 1);
         const bool ghost_w = writes_ghost(0), ghost_e = writes_ghost(1);
-        const int nrows = a.row_hi - a.row_lo;
-        const int i_start = a.row_lo + (int)(((long long)nrows * seg) / a.nseg);
-        const int i_end = a.row_lo + (int)(((long long)nrows * (seg + 1)) / a.nseg);
+        const int lo = trailing ? a.row_split : a.row_lo, ns = trailing ? a.nseg2 : a.nseg;
+        const int nrows = (trailing ? a.row_hi : a.row_split) - lo;
+        const int i_start = lo + (int)(((long long)nrows * seg) / ns);
+        const int i_end = lo + (int)(((long long)nrows * (seg + 1)) / ns);
         const int r0 = i_start - 2, r_last = i_end + 1;  // stencil rows
         unsigned touch = 0;  // bit e: peer edge e (W, E, S, N) touched by this task
         if constexpr (PEER) {
@@ -1112,7 +1121,7 @@ template <int MODE, bool NORMS, bool DTMAX, bool FAST, bool PEER, bool VISC>
 static cudaError_t launch_t(const StageArgs &a, cudaStream_t st) {
     auto k = stage_kernel<MODE, NORMS, DTMAX, FAST, PEER, VISC>;
     cudaLaunchConfig_t cfg{};
-    cfg.gridDim = dim3((a.nstrips * a.nseg + WPC - 1) / WPC);
+    cfg.gridDim = dim3((a.nstrips * (a.nseg + a.nseg2) + WPC - 1) / WPC);
     cfg.blockDim = dim3(NT);
     cfg.dynamicSmemBytes = stage_smem<MODE>();  // attribute set by prepare_stage_kernels()
     cfg.stream = st;
