@@ -376,16 +376,19 @@ void plan_launches(sfv_ctx *c, Block &b) {
     // into segments of ~SFV_TAIL_ROWS rows that the CTA scheduler places in
     // the slots of the first warps to finish
     const char *ef = getenv("SFV_TAIL_FRAC"), *er = getenv("SFV_TAIL_ROWS");
-    const double frac = ef ? atof(ef) : 0.10;  // measured optimum on C2 (profiles/r2b_ab_tail_segments.txt)
-    const int trows = std::max(2, er ? atoi(er) : 4);
+    const char *emf = getenv("SFV_TAIL_MFRAC"), *emr = getenv("SFV_TAIL_MROWS");
     for (int q = 0; q < 2; ++q) {
         b.tseg2[q] = 0;
         b.tsplit[q] = b.ni;
         const int nseg = q ? b.lsegF[0] : b.lseg[0];
         const long long slots = (long long)c->nsm * std::max(1, q ? c->occ_f : c->occ) * WPC;
+        const bool single = (long long)b.nstrips * nseg <= slots;
+        // single wave: the measured optimum on C2 (profiles/r2b_ab_tail_segments.txt);
+        // multi-wave launches (the scheduler refills slots already): the last wave only
+        const double frac = single ? (ef ? atof(ef) : 0.10) : (emf ? atof(emf) : 0.04);
+        const int trows = std::max(2, single ? (er ? atoi(er) : 4) : (emr ? atoi(emr) : 16));
         const int tail = (int)std::lround(frac * b.ni);
-        if (n != 1 || frac <= 0.0 || (long long)b.nstrips * nseg > slots || tail < 2 * trows ||
-            b.ni - tail < 4 * nseg)
+        if (n != 1 || frac <= 0.0 || tail < 2 * trows || b.ni - tail < 4 * nseg)
             continue;
         b.tseg2[q] = std::min(tail / trows, NSEG_MAX - nseg);
         b.tsplit[q] = b.tseg2[q] > 0 ? b.ni - tail : b.ni;
