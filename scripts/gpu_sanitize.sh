@@ -19,6 +19,15 @@ for (ni, nj, px, py, rk, peer, ns) in [(64, 32, 1, 1, 0, 0, 0), (40, 36, 2, 2, 0
     R = g.residual(I.perturbed_state(ni, nj, 2))   # sfv_residual (M_RES kernel variant)
     assert np.all(np.isfinite(R))
     print("ok", ni, nj, px, py, rk, "peer" if peer else "copy", "ns" if ns else "euler", g.residual_norms()[-1][:2])
+# trailing short segments (forced 30 % tail on a 60-strip grid)
+import os
+os.environ["SFV_TAIL_FRAC"] = "0.3"; os.environ["SFV_TAIL_ROWS"] = "3"
+ni, nj = 200, 1800
+X, Y = I.ramp_nodes(ni, nj, 30.0)
+g = sfv.Solver(I.default_config(ni, nj), X, Y)
+g.set_state(I.perturbed_state(ni, nj, 1)); g.step(2); g.sync()
+assert np.all(np.isfinite(g.get_state()))
+print("ok trailing segments", ni, nj)
 PY
 for tool in memcheck racecheck synccheck; do
   timeout 900 compute-sanitizer --tool $tool --error-exitcode 9 python /tmp/san.py > gpurun_out/san_${TAG}_$tool.log 2>&1; echo rc=$? >> gpurun_out/san_${TAG}_$tool.log

@@ -310,6 +310,34 @@ def test_c2_full_size_one_step(sfv_mod, oracle_mod):
     check(g, o, 1e-12)
 
 
+@pytest.mark.parametrize("ni,nj,steps,env", [(1440, 720, 40, {}), (11520, 5760, 1, {}),
+                                              (400, 1800, 20, {"SFV_TAIL_FRAC": "0.3", "SFV_TAIL_ROWS": "3"})])
+def test_trailing_segments_are_a_schedule_only(sfv_mod, monkeypatch, ni, nj, steps, env):
+    """Trailing short segments (the last rows of each strip in
+    short tasks the CTA scheduler places in slots freed early) only reschedule
+    rows: state and dt histories equal the launch without them bitwise (the
+    per-cell arithmetic is the same), the norms (partials grouped per task)
+    to rounding; single-wave (C2, a forced 30 % tail) and multi-wave (C3)."""
+    X, Y = I.ramp_nodes(ni, nj, 30.0)
+    cfg = I.default_config(ni, nj)
+    U0 = I.perturbed_state(ni, nj, 1, amplitude=0.02)
+    out = []
+    for frac in (None, "0"):
+        for k in ("SFV_TAIL_FRAC", "SFV_TAIL_MFRAC", "SFV_TAIL_ROWS"):
+            monkeypatch.delenv(k, raising=False)
+        for k, v in env.items():
+            monkeypatch.setenv(k, v)
+        if frac is not None:
+            monkeypatch.setenv("SFV_TAIL_FRAC", frac)
+            monkeypatch.setenv("SFV_TAIL_MFRAC", frac)
+        g = sfv_mod.Solver(cfg, X, Y)
+        g.set_state(U0); g.step(steps); g.sync()
+        out.append((g.get_state(), g.dt(), g.residual_norms()))
+    np.testing.assert_array_equal(out[0][0], out[1][0])
+    np.testing.assert_array_equal(out[0][1], out[1][1])
+    assert norm_error(out[0][2], out[1][2]) <= 1e-13
+
+
 def test_c3_full_size_windows(sfv_mod, oracle_mod):
     """BASELINE config C3 (11520x5760 = 66.4 M cells) on one GPU in the
     launch configuration bench.py times: one RK4 step of a perturbed state.
