@@ -481,6 +481,13 @@ def main():
             m = solver.partition_map(rank)
             Uout = torch.empty((int(m[3] - m[2]), int(m[1] - m[0]), 4), dtype=torch.float64, pin_memory=True)
         K = args.steps
+        # one untimed pass over the same pinned buffers (first DMA touch of the
+        # pages; like the warm-up steps of the device-timed region)
+        solver.set_state_ptr(Uh.data_ptr())
+        if world == 1:
+            solver.get_state_ptr(Uout.data_ptr())
+        else:
+            solver.get_block_state_ptr(rank, Uout.data_ptr())
         barrier()
         t0 = time.perf_counter()
         solver.set_state_ptr(Uh.data_ptr())

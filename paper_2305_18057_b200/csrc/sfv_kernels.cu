@@ -340,7 +340,9 @@ __device__ __forceinline__ void store4(double *buf, int PJ, int i, int j, const 
 #define SFV_PARK 0  // park the row-carried values in shared memory (fewer registers, more resident warps)
 #endif
 #ifndef SFV_XSHFL
-#define SFV_XSHFL 0  // lane exchange of j-face states / fluxes by shuffles instead of shared memory
+// lane exchange of j-face states / fluxes by shuffles instead of shared memory
+// (round 2b A/B: C2 +1.0 %, C3 +0.6 %, profiles/r2b_ab_xshfl_l2hint.txt; bitwise the same)
+#define SFV_XSHFL 1
 #endif
 #ifndef SFV_PARK_WARPS
 #define SFV_PARK_WARPS 14  // resident warps per SM targeted by the parked variants
