@@ -138,6 +138,33 @@ def load_profile_traffic(ns=False):
         return None, None
 
 
+def operand_roofline(args, clocks, avg_launch_s, nj, ni, world, nblk):
+    """The stage kernel against the sub-partition's register-operand bandwidth
+    (profiles/r2b_tail_analysis.md section 2): the executed instruction mix of
+    the same workload (ncu source page, scripts/opcost.py ->
+    profiles/opcost_stage_kernel[_c3].json) charged with the microbenchmarked
+    costs gives the cycles a warp-row needs at that bound; achieved = the
+    average stage-kernel time x the sampled SM clock / warp-rows per
+    sub-partition.  C2 and C3 on one GPU only (where a capture exists)."""
+    name = {"C2": "opcost_stage_kernel.json", "C3": "opcost_stage_kernel_c3.json"}.get(args.workload)
+    if not name or world != 1 or nblk != 1 or args.ns or not clocks.get("sm_mhz"):
+        return None
+    try:
+        with open(os.path.join(ROOT, "profiles", name)) as f:
+            d = json.load(f)
+    except (OSError, ValueError):
+        return None
+    import torch
+    nsmsp = torch.cuda.get_device_properties(0).multi_processor_count * 4
+    warp_rows = ((nj + 29) // 30) * ni / nsmsp  # per sub-partition and stage
+    achieved = avg_launch_s * clocks["sm_mhz"] * 1e6 / warp_rows
+    model = d["model_cycles_per_warp_row_mean"]
+    return {"bound": "operand", "unit": "sub-partition cycles per warp-row", "achieved": achieved, "peak": model,
+            "frac": model / achieved, "profile": "profiles/" + name,
+            "note": "peak = cycles the executed mix needs at the register-operand bound (lower is faster), "
+                    "frac = peak / achieved"}
+
+
 def measured_peak():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -552,6 +579,9 @@ def main():
                            **extras},
                 "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches * reps,
                 "clocks": clk.summary()}
+        opr = operand_roofline(args, line["clocks"], avg_launch_s, nj, ni, world, nblk)
+        if opr and isinstance(roof, dict) and roof.get("bound") == "alu":
+            roof["operand"] = opr
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()

@@ -111,7 +111,7 @@ def main():
             print('  %6.2f cyc  x%5.2f  %s' % (cy, n, t))
 
 
-if __name__ == "__main__" and "--lines" not in sys.argv:
+if __name__ == "__main__" and "--lines" not in sys.argv and "--json" not in sys.argv:
     main()
 
 
@@ -139,6 +139,32 @@ def by_line(dis, fn, rows, ie, units):
         a[0] += n * cy; a[1] += n; a[2][base] += n
     return agg
 
+
+def to_json(path, lib, units, out, label):
+    """Modelled cycles per unit for the 4 stage launches of a capture (bench.py's operand roofline)."""
+    import json
+    res = []
+    for name, hdr, rows in kernels(path):
+        ie = hdr.index('Instructions Executed')
+        tot = 0.0
+        for r in rows:
+            n = float(r[ie] or 0) / units
+            if n:
+                tot += n * cost(r[1].strip())[2]
+        res.append({"kernel": name, "model_cycles_per_warp_row": round(tot, 1)})
+    # (ncu's source page lists every launch twice: keep the first copy of each)
+    res = res[0::2]
+    d = {"source": label, "unit": "warp-row (one warp, one row of its 30-column strip)", "launches": res,
+         "model_cycles_per_warp_row_mean": round(sum(x["model_cycles_per_warp_row"] for x in res) / len(res), 1),
+         "costs": "FP64: max(2, fresh 64-bit register operands); LDS/STS/SHFL: 2; other vector: 0.5 per register "
+                  "operand; uniform datapath: 0 (profiles/r2b_tail_analysis.md section 2)"}
+    json.dump(d, open(out, 'w'), indent=1)
+    print(json.dumps(d, indent=1))
+
+
+if __name__ == '__main__' and '--json' in sys.argv:
+    to_json(sys.argv[1], sys.argv[2], float(sys.argv[4]), sys.argv[sys.argv.index('--json') + 1],
+            sys.argv[sys.argv.index('--label') + 1] if '--label' in sys.argv else sys.argv[1])
 
 if __name__ == '__main__' and '--lines' in sys.argv:
     path, lib, kidx, units = sys.argv[1], sys.argv[2], int(sys.argv[3]), float(sys.argv[4])
