@@ -338,6 +338,23 @@ def test_trailing_segments_are_a_schedule_only(sfv_mod, monkeypatch, ni, nj, ste
     assert norm_error(out[0][2], out[1][2]) <= 1e-13
 
 
+def test_c2_full_size_1000_steps_bench_start(sfv_mod, oracle_mod):
+    """The north-star gate at full BASELINE C2 size in the launch configuration
+    bench.py times (uniform Table 1 start, trailing segments on): state 1e-9,
+    residual-norm history 1e-10 and dt 1e-13 after 1000 RK4 steps against the
+    oracle (its -fopenmp build, bitwise the single-threaded one;
+    profiles/r2c_parity_c2_full_size_1000_steps.txt: 4.7e-13 / 8.5e-13 / 3.6e-15)."""
+    X, Y = I.config_nodes("C2")
+    c = I.CONFIGS["C2"]
+    cfg = I.default_config(c["ni"], c["nj"])
+    U0 = I.uniform_state(c["ni"], c["nj"])
+    g = sfv_mod.Solver(cfg, X, Y); g.set_state(U0); g.step(1000); g.sync()
+    o = oracle_mod.Oracle(cfg, X, Y, omp=True); o.set_state(U0); o.step(1000)
+    assert state_error(g.get_state(), o.get_state()).max() <= 1e-9
+    assert norm_error(g.residual_norms(), o.residual_norms()) <= 1e-10
+    assert dt_error(g.dt(), o.dt()) <= 1e-13
+
+
 def test_c3_full_size_windows(sfv_mod, oracle_mod):
     """BASELINE config C3 (11520x5760 = 66.4 M cells) on one GPU in the
     launch configuration bench.py times: one RK4 step of a perturbed state.
