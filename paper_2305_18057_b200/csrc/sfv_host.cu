@@ -702,7 +702,11 @@ sfv_status enqueue_viscous(sfv_ctx *c, int in, cudaStream_t st) {
     bool all_fused = true;
     for (Block &b : c->blocks) {
         const bool iso = b.nbr[0] < 0 && b.nbr[1] < 0 && b.nbr[2] < 0 && b.nbr[3] < 0;
-        if (iso && fuse_ok) CK(launch_gradvisc(args(b), st));  // gradients never leave shared memory
+        if (iso && fuse_ok) {  // gradients never leave the SM (registers / shared memory)
+            const char *em = getenv("SFV_NS_MARCH");
+            if (em && em[0] == '0') CK(launch_gradvisc(args(b), st));
+            else CK(launch_gradvisc_march(args(b), st));
+        }
         else { CK(launch_grad(args(b), st)); all_fused = false; }  // (writes the physical ghost gradients too)
     }
     if (all_fused) return SFV_OK;

@@ -148,6 +148,7 @@ struct ViscArgs {
 cudaError_t launch_grad(const ViscArgs &v, cudaStream_t st);
 cudaError_t launch_visc(const ViscArgs &v, cudaStream_t st);
 cudaError_t launch_gradvisc(const ViscArgs &v, cudaStream_t st);  // blocks without connected edges
+cudaError_t launch_gradvisc_march(const ViscArgs &v, cudaStream_t st);  // (same, row-marching warps)
 cudaError_t launch_norms(const NormsArgs &f, cudaStream_t st);
 cudaError_t stage_occupancy(int mode, bool norms, bool dtmax, bool fast, bool peer, int *ctas_per_sm);
 cudaError_t stage_occupancy_visc(int mode, bool norms, bool dtmax, bool fast, int *ctas_per_sm);

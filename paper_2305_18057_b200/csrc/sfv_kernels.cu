@@ -30,6 +30,8 @@
 #include "sfv_internal.h"
 
 #include <cstdio>
+#include <cstdlib>
+#include <algorithm>
 
 namespace sfv {
 
@@ -1285,16 +1287,20 @@ __device__ __forceinline__ double *gradp(double *grad, int PG, int i, int j, int
 
 // Green-Gauss gradient (reading N-R2) of cell (i, j) from the (u, v, T) of
 // the cell and its 4 face neighbours; faces: the mean of the two cells times A
-__device__ __forceinline__ void gg_cell(const double *met, int PJ, int i, int j, const double c[3], const double w[3],
-                                        const double e[3], const double s[3], const double n[3], double g[6]) {
+// the cell's metric values: W i-face (nx, ny, A/2) = m0[0..2] (metrics row i),
+// E i-face = m1[0..2], S j-face = m1[3..5], 1/V = m1[6] (row i+1, column j),
+// N j-face = mn[0..2] (row i+1 fields 3..5, column j+1)
+__device__ __forceinline__ void gg_core(const double m0[3], const double m1[7], const double mn[3], const double c[3],
+                                        const double w[3], const double e[3], const double s[3], const double n[3],
+                                        double g[6]) {
     // per face: n A / (2 V), so grad = sum_f (phi_L + phi_R) n A / (2 V) with outward signs
-    const double h = metf(met, PJ, i + 1, 6, j);  // (the metrics hold A/2)
-    const double hW = DM(metf(met, PJ, i, 2, j), h), hE = DM(metf(met, PJ, i + 1, 2, j), h);
-    const double hS = DM(metf(met, PJ, i + 1, 5, j), h), hN = DM(metf(met, PJ, i + 1, 5, j + 1), h);
-    const double kWx = DM(metf(met, PJ, i, 0, j), hW), kWy = DM(metf(met, PJ, i, 1, j), hW);
-    const double kEx = DM(metf(met, PJ, i + 1, 0, j), hE), kEy = DM(metf(met, PJ, i + 1, 1, j), hE);
-    const double kSx = DM(metf(met, PJ, i + 1, 3, j), hS), kSy = DM(metf(met, PJ, i + 1, 4, j), hS);
-    const double kNx = DM(metf(met, PJ, i + 1, 3, j + 1), hN), kNy = DM(metf(met, PJ, i + 1, 4, j + 1), hN);
+    const double h = m1[6];  // (the metrics hold A/2)
+    const double hW = DM(m0[2], h), hE = DM(m1[2], h);
+    const double hS = DM(m1[5], h), hN = DM(mn[2], h);
+    const double kWx = DM(m0[0], hW), kWy = DM(m0[1], hW);
+    const double kEx = DM(m1[0], hE), kEy = DM(m1[1], hE);
+    const double kSx = DM(m1[3], hS), kSy = DM(m1[4], hS);
+    const double kNx = DM(mn[0], hN), kNy = DM(mn[1], hN);
 #pragma unroll
     for (int q = 0; q < 3; ++q) {
         const double sE = DA(c[q], e[q]), sW = DA(w[q], c[q]), sN = DA(c[q], n[q]), sS = DA(s[q], c[q]);
@@ -1302,6 +1308,15 @@ __device__ __forceinline__ void gg_cell(const double *met, int PJ, int i, int j,
         g[2 * q] = fma(-sS, kSx, fma(sN, kNx, fma(-sW, kWx, DM(sE, kEx))));
         g[2 * q + 1] = fma(-sS, kSy, fma(sN, kNy, fma(-sW, kWy, DM(sE, kEy))));
     }
+}
+__device__ __forceinline__ void gg_cell(const double *met, int PJ, int i, int j, const double c[3], const double w[3],
+                                        const double e[3], const double s[3], const double n[3], double g[6]) {
+    const double m0[3] = {metf(met, PJ, i, 0, j), metf(met, PJ, i, 1, j), metf(met, PJ, i, 2, j)};
+    double m1[7];
+#pragma unroll
+    for (int f = 0; f < 7; ++f) m1[f] = metf(met, PJ, i + 1, f, j);
+    const double mn[3] = {metf(met, PJ, i + 1, 3, j + 1), metf(met, PJ, i + 1, 4, j + 1), metf(met, PJ, i + 1, 5, j + 1)};
+    gg_core(m0, m1, mn, c, w, e, s, n, g);
 }
 
 __global__ void grad_kernel(const ViscArgs a) {
@@ -1448,6 +1463,174 @@ __global__ void __launch_bounds__(VT_J * VT_I) gradvisc_kernel(const ViscArgs a)
     face_visc_core(gs[ti][tj], gs[ti][tj + 1], c, pr[ti + 1][tj + 2], metf(a.met, a.PJ, i + 1, 3, j + 1),
                    metf(a.met, a.PJ, i + 1, 4, j + 1), metf(a.met, a.PJ, i + 1, 5, j + 1), a.P, FN);
     store_rv(a, i, j, FW, FE, FS, FN);
+}
+
+// Row-marching fused gradient + viscous residual (blocks without connected
+// edges; round 2c): a warp owns 28 output columns (lane l <-> column
+// j0 - 2 + l; lanes 2..29 write) and marches along i, carrying the (u, v, T)
+// of rows v, v+1 and the gradients of rows v, v+1 in registers; j neighbours
+// come by shuffles, the W face flux is the previous row's E face and the S
+// face flux is the N face of the lane below.  Every gradient and every face
+// flux is evaluated once, with the same helpers and argument values as the
+// tile and two-kernel paths (bitwise the same viscous residual).
+constexpr int VM_OUT = 28;
+#ifndef SFV_NS_MBLK
+#define SFV_NS_MBLK 2
+#endif
+__global__ void __launch_bounds__(128, SFV_NS_MBLK) gradvisc_march_kernel(const ViscArgs a, int nstrips, int nseg) {
+    const int lane = threadIdx.x & 31, task = blockIdx.x * 4 + (threadIdx.x >> 5);
+    if (task >= nstrips * nseg) return;
+    const int strip = task % nstrips, seg = task / nstrips;
+    const int jc = strip * VM_OUT - 2 + lane;  // this lane's column (may lie in the ghost frame or beyond)
+    const int i_s = (int)(((long long)a.ni * seg) / nseg), i_e = (int)(((long long)a.ni * (seg + 1)) / nseg);
+    const int jl = min(max(jc, -2), a.nj + 1);   // loadable column (state)
+    const int jg = min(max(jc, 0), a.nj - 1);    // interior column (metrics of a cell)
+    const int jn = min(max(jc + 1, 0), a.nj);    // the N j-face's column
+    const int PJ = a.PJ;
+    // raw state of row r at this lane's column; metric values a row's gradient
+    // and faces need (see gg_core): i-face row fields 0..2 at jg, fields 3..6
+    // at jg, fields 3..5 at jn
+    auto load_state = [&](int r, double q[4]) {
+        const double *p = a.in + (size_t)((r + 2) * 4) * PJ + (jl + JOFF);
+#pragma unroll
+        for (int c = 0; c < 4; ++c) q[c] = __ldg(p + (size_t)c * PJ);
+    };
+    auto load_met = [&](int m, double mr[10]) {  // metrics row m
+#pragma unroll
+        for (int f = 0; f < 7; ++f) mr[f] = __ldg(a.met + (size_t)(m * NMET + f) * PJ + jg + JOFF);
+#pragma unroll
+        for (int f = 0; f < 3; ++f) mr[7 + f] = __ldg(a.met + (size_t)(m * NMET + 3 + f) * PJ + jn + JOFF);
+    };
+    auto to_uvt = [&](const double q[4], double o[3]) { uvT_core(q[0], q[1], q[2], q[3], a.P, o); };
+    // gradient of cell row r from its (u, v, T) c (W w, E e; S/N by shuffles) and
+    // metrics rows r (mA) and r+1 (mB); physical ghost columns (-1, nj) take the
+    // adjacent interior column's (reading N-R1)
+    auto grad_row = [&](const double mA[10], const double mB[10], const double c[3], const double w[3],
+                        const double e[3], double g[6]) {
+        double sS[3], sN[3];
+#pragma unroll
+        for (int q = 0; q < 3; ++q) {
+            sS[q] = __shfl_up_sync(0xffffffffu, c[q], 1);
+            sN[q] = __shfl_down_sync(0xffffffffu, c[q], 1);
+        }
+        const double m0[3] = {mA[0], mA[1], mA[2]};
+        const double mn[3] = {mB[7], mB[8], mB[9]};
+        gg_core(m0, mB, mn, c, w, e, sS, sN, g);
+#pragma unroll
+        for (int q = 0; q < 6; ++q) {
+            const double fromE = __shfl_down_sync(0xffffffffu, g[q], 1), fromW = __shfl_up_sync(0xffffffffu, g[q], 1);
+            g[q] = jc == -1 ? fromE : (jc == a.nj ? fromW : g[q]);
+        }
+    };
+    // ---- prologue: rows i_s-1 .. i_s+1, gradients of rows i_s-1 and i_s, W face of row i_s
+    double uA[3], uB[3], uC[3], g1[6], FW[4];
+    double mr1[10], mr2[10];  // metrics rows v+1, v+2
+    double sN2[4], mN3[10];   // prefetched: state row v+2 (as raw), metrics row v+3
+    {
+        double q[4], mr0[10], g0[6];
+        load_state(i_s - 1, q); to_uvt(q, uA);
+        load_state(i_s, q); to_uvt(q, uB);
+        load_state(i_s + 1, q); to_uvt(q, uC);
+        load_met(i_s, mr0);
+        load_met(i_s + 1, mr1);
+        grad_row(mr0, mr1, uB, uA, uC, g1);  // row i_s
+        if (i_s == 0) {
+#pragma unroll
+            for (int k = 0; k < 6; ++k) g0[k] = g1[k];
+        } else {
+            double um[3], mrm[10];
+            load_state(i_s - 2, q); to_uvt(q, um);
+            load_met(i_s - 1, mrm);
+            grad_row(mrm, mr0, uA, um, uB, g0);  // row i_s - 1
+        }
+        // i-face i_s between cells i_s-1 and i_s: metrics row i_s fields 0-2
+        face_visc_core(g0, g1, uA, uB, mr0[0], mr0[1], mr0[2], a.P, FW);
+        // rotate to the loop state: uA = row v, uB = row v+1 (uC), mr1 = row v+1
+#pragma unroll
+        for (int k = 0; k < 3; ++k) { uA[k] = uB[k]; uB[k] = uC[k]; }
+        if (i_s + 1 < a.ni) {
+            load_met(i_s + 2, mr2);
+            load_state(i_s + 2, sN2);
+            if (i_s + 2 < a.ni) load_met(i_s + 3, mN3);
+        }
+    }
+    // loop state at the top of iteration v: uA = (u, v, T) of row v, uB = row
+    // v+1, g1 = gradient of row v, FW = W face flux of row v, mr1 = metrics
+    // row v+1, mr2 = row v+2 and sN2 = raw state of row v+2 (if v+1 < ni),
+    // mN3 = metrics row v+3 (if v+2 < ni)
+    for (int v = i_s; v < i_e; ++v) {
+        double gn[6];
+        if (v + 1 < a.ni) {
+            double uN[3];
+            to_uvt(sN2, uN);  // row v+2
+            // prefetch one row ahead: state row v+3, metrics row v+4
+            double sN3[4], mN4[10];
+            if (v + 2 < a.ni) load_state(v + 3, sN3);
+            if (v + 3 < a.ni) load_met(v + 4, mN4);
+            grad_row(mr1, mr2, uB, uA, uN, gn);  // row v+1
+            // E face of row v (i-face v+1: metrics row v+1 fields 0-2), N face (row v+1 fields 3-5 at jn)
+            double FE[4], FN[4], FS[4];
+            face_visc_core(g1, gn, uA, uB, mr1[0], mr1[1], mr1[2], a.P, FE);
+            {
+                double gE[6], uE[3];
+#pragma unroll
+                for (int q = 0; q < 6; ++q) gE[q] = __shfl_down_sync(0xffffffffu, g1[q], 1);
+#pragma unroll
+                for (int q = 0; q < 3; ++q) uE[q] = __shfl_down_sync(0xffffffffu, uA[q], 1);
+                face_visc_core(g1, gE, uA, uE, mr1[7], mr1[8], mr1[9], a.P, FN);
+            }
+#pragma unroll
+            for (int c = 0; c < 4; ++c) FS[c] = __shfl_up_sync(0xffffffffu, FN[c], 1);
+            if (lane >= 2 && lane < 2 + VM_OUT && jc < a.nj) store_rv(a, v, jc, FW, FE, FS, FN);
+#pragma unroll
+            for (int c = 0; c < 4; ++c) FW[c] = FE[c];
+#pragma unroll
+            for (int q = 0; q < 6; ++q) g1[q] = gn[q];
+#pragma unroll
+            for (int k = 0; k < 3; ++k) { uA[k] = uB[k]; uB[k] = uN[k]; }
+#pragma unroll
+            for (int f = 0; f < 10; ++f) { mr1[f] = mr2[f]; mr2[f] = mN3[f]; mN3[f] = mN4[f]; }
+#pragma unroll
+            for (int c = 0; c < 4; ++c) sN2[c] = sN3[c];
+        } else {
+            // last row (v = ni-1): the E neighbour is the ghost row ni, whose
+            // gradient is row ni-1's (physical E edge)
+            double FE[4], FN[4], FS[4];
+            face_visc_core(g1, g1, uA, uB, mr1[0], mr1[1], mr1[2], a.P, FE);
+            {
+                double gE[6], uE[3];
+#pragma unroll
+                for (int q = 0; q < 6; ++q) gE[q] = __shfl_down_sync(0xffffffffu, g1[q], 1);
+#pragma unroll
+                for (int q = 0; q < 3; ++q) uE[q] = __shfl_down_sync(0xffffffffu, uA[q], 1);
+                face_visc_core(g1, gE, uA, uE, mr1[7], mr1[8], mr1[9], a.P, FN);
+            }
+#pragma unroll
+            for (int c = 0; c < 4; ++c) FS[c] = __shfl_up_sync(0xffffffffu, FN[c], 1);
+            if (lane >= 2 && lane < 2 + VM_OUT && jc < a.nj) store_rv(a, v, jc, FW, FE, FS, FN);
+        }
+    }
+}
+
+cudaError_t launch_gradvisc_march(const ViscArgs &v, cudaStream_t st) {
+    // one wave of warp tasks: segments per strip = resident warps / strips
+    // (SFV_NS_MROWS overrides with a segment height)
+    static int resident = 0;
+    if (!resident) {
+        int dev = 0, nsm = 0, blk = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blk, gradvisc_march_kernel, 128, 0);
+        resident = std::max(1, nsm * std::max(1, blk) * 4);
+    }
+    const int nstrips = (v.nj + VM_OUT - 1) / VM_OUT;
+    const char *er = getenv("SFV_NS_MROWS");
+    int nseg = std::max(1, resident / nstrips);
+    if (er && *er) nseg = std::max(1, (v.ni + std::max(4, atoi(er)) - 1) / std::max(4, atoi(er)));
+    nseg = std::min(nseg, std::max(1, v.ni / 4));
+    const int tasks = nstrips * nseg;
+    gradvisc_march_kernel<<<(tasks + 3) / 4, 128, 0, st>>>(v, nstrips, nseg);
+    return cudaGetLastError();
 }
 
 cudaError_t launch_gradvisc(const ViscArgs &v, cudaStream_t st) {

@@ -125,20 +125,21 @@ def test_ns_operator_matches_oracle(sfv_mod, oracle_mod):
     assert np.max(np.abs(rv - Rv)) <= 1e-11 * np.max(np.abs(Rv))
 
 
-def test_ns_fused_equals_two_kernel_path(sfv_mod):
-    """The fused tile kernel (blocks without connected edges) and the
-    gradient + viscous kernel pair give bitwise the same evolution."""
-    import os
-    ni, nj = 70, 45
+@pytest.mark.parametrize("ni,nj,rows", [(70, 45, "32"), (70, 45, "5"), (131, 61, "32"), (40, 90, "7")])
+def test_ns_fused_equals_two_kernel_path(sfv_mod, monkeypatch, ni, nj, rows):
+    """The fused kernels for blocks without connected edges -- the row-marching
+    one (default; segments of SFV_NS_MROWS rows, strips of 28 columns: ragged
+    strips and segments) and the tile one -- and the gradient + viscous kernel
+    pair give bitwise the same evolution."""
     X, Y = I.ramp_nodes(ni, nj, 5.0)
     cfg = I.default_config(ni, nj, viscous=1, mu=0.1, bc=NOSLIP_S)
     U0 = I.perturbed_state(ni, nj, 17)
     out = []
-    for fused in ("1", "0"):
-        os.environ["SFV_NS_FUSED"] = fused
-        try:
-            g = sfv_mod.Solver(cfg, X, Y); g.set_state(U0); g.step(15); g.sync()
-        finally:
-            del os.environ["SFV_NS_FUSED"]
+    monkeypatch.setenv("SFV_NS_MROWS", rows)
+    for fused, march in (("1", "1"), ("1", "0"), ("0", "1")):
+        monkeypatch.setenv("SFV_NS_FUSED", fused)
+        monkeypatch.setenv("SFV_NS_MARCH", march)
+        g = sfv_mod.Solver(cfg, X, Y); g.set_state(U0); g.step(15); g.sync()
         out.append(g.get_state())
-    np.testing.assert_array_equal(out[0], out[1])
+    np.testing.assert_array_equal(out[0], out[2])
+    np.testing.assert_array_equal(out[1], out[2])
