@@ -1525,7 +1525,7 @@ __global__ void __launch_bounds__(128, SFV_NS_MBLK) gradvisc_march_kernel(const 
     // ---- prologue: rows i_s-1 .. i_s+1, gradients of rows i_s-1 and i_s, W face of row i_s
     double uA[3], uB[3], uC[3], g1[6], FW[4];
     double mr1[10], mr2[10];  // metrics rows v+1, v+2
-    double sN2[4], mN3[10];   // prefetched: state row v+2 (as raw), metrics row v+3
+    double sN2[4];            // prefetched: state row v+2 (as raw)
     {
         double q[4], mr0[10], g0[6];
         load_state(i_s - 1, q); to_uvt(q, uA);
@@ -1551,22 +1551,23 @@ __global__ void __launch_bounds__(128, SFV_NS_MBLK) gradvisc_march_kernel(const 
         if (i_s + 1 < a.ni) {
             load_met(i_s + 2, mr2);
             load_state(i_s + 2, sN2);
-            if (i_s + 2 < a.ni) load_met(i_s + 3, mN3);
         }
     }
     // loop state at the top of iteration v: uA = (u, v, T) of row v, uB = row
     // v+1, g1 = gradient of row v, FW = W face flux of row v, mr1 = metrics
     // row v+1, mr2 = row v+2 and sN2 = raw state of row v+2 (if v+1 < ni),
-    // mN3 = metrics row v+3 (if v+2 < ni)
+    // (each iteration prefetches the state and metrics rows the next one needs)
     for (int v = i_s; v < i_e; ++v) {
         double gn[6];
         if (v + 1 < a.ni) {
             double uN[3];
             to_uvt(sN2, uN);  // row v+2
             // prefetch one row ahead: state row v+3, metrics row v+4
-            double sN3[4], mN4[10];
-            if (v + 2 < a.ni) load_state(v + 3, sN3);
-            if (v + 3 < a.ni) load_met(v + 4, mN4);
+            double sN3[4], mN[10];
+            if (v + 2 < a.ni) {
+                load_state(v + 3, sN3);
+                load_met(v + 3, mN);
+            }
             grad_row(mr1, mr2, uB, uA, uN, gn);  // row v+1
             // E face of row v (i-face v+1: metrics row v+1 fields 0-2), N face (row v+1 fields 3-5 at jn)
             double FE[4], FN[4], FS[4];
@@ -1589,7 +1590,7 @@ __global__ void __launch_bounds__(128, SFV_NS_MBLK) gradvisc_march_kernel(const 
 #pragma unroll
             for (int k = 0; k < 3; ++k) { uA[k] = uB[k]; uB[k] = uN[k]; }
 #pragma unroll
-            for (int f = 0; f < 10; ++f) { mr1[f] = mr2[f]; mr2[f] = mN3[f]; mN3[f] = mN4[f]; }
+            for (int f = 0; f < 10; ++f) { mr1[f] = mr2[f]; mr2[f] = mN[f]; }
 #pragma unroll
             for (int c = 0; c < 4; ++c) sN2[c] = sN3[c];
         } else {
