@@ -263,7 +263,11 @@ sfv_status sfv_debug_math(sfv_ctx *ctx, int32_t which, const double *in_dev, dou
  * and the peer flags restart there).  PEER with nranks > 1 needs
  * sfv_peer_connect first.  ARG: unknown mode.  SEQUENCE: order violated.
  * A peer that never signals is reported by the next synchronising call as
- * SFV_ERR_HALO (after a 20 s device-side timeout; no hang). */
+ * SFV_ERR_HALO (after a 20 s device-side timeout; no hang).  Navier-Stokes
+ * mode (viscous = 1) in PEER: the gradient kernel also stores its edge
+ * gradients into the neighbour's gradient frame and signals (PAPER.md:120
+ * "exchange ghost cells", here the 1-layer gradient ghosts the viscous
+ * flux of Eq. 2, needs). */
 sfv_status sfv_set_halo_mode(sfv_ctx *ctx, int32_t mode);
 
 /* nranks > 1, after sfv_bind: 128 opaque bytes describing this rank's block

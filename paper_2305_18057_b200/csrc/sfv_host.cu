@@ -83,6 +83,7 @@ Nccl &nccl() {
 struct PeerView {
     double *buf[4] = {nullptr, nullptr, nullptr, nullptr};
     unsigned long long *flags = nullptr;
+    double *grad = nullptr;  // Navier-Stokes: the neighbour's gradient frame (pitch nj + 2)
     int PJ = 0, ni = 0, nj = 0;
 };
 
@@ -489,7 +490,7 @@ size_t layout(sfv_ctx *c, bool assign) {
             b.xr[0] = reinterpret_cast<double *>(c->ws + ox[2]);
             b.xr[1] = reinterpret_cast<double *>(c->ws + ox[3]);
             b.flags = reinterpret_cast<unsigned long long *>(c->ws + of);
-            b.ecnt = reinterpret_cast<unsigned *>(c->ws + of + PEER_SYNC_BYTES / 2);
+            b.ecnt = reinterpret_cast<unsigned *>(c->ws + of + PEER_ECNT_OFF);
             b.PG = PG;
             b.grad = c->cfg.viscous ? reinterpret_cast<double *>(c->ws + og) : nullptr;
             b.rv = c->cfg.viscous ? reinterpret_cast<double *>(c->ws + orv) : nullptr;
@@ -682,9 +683,33 @@ StageArgs make_args(sfv_ctx *c, Block &b, int k) {
 // gradients, loopback exchange of the connected ones (1 layer: rows for
 // i-cuts, columns for j-cuts), then every block's viscous residual
 // (readings N-R1..N-R3)
-sfv_status enqueue_viscous(sfv_ctx *c, int in, cudaStream_t st) {
+// stage > 0 in peer mode: device-initiated gradient halos (grad_kernel stores
+// its edge gradients into the neighbours' frames and signals; visc_kernel's
+// edge CTAs wait), no copies; stage 0 (sfv_residual): copy exchange.
+sfv_status enqueue_viscous(sfv_ctx *c, int in, cudaStream_t st, int stage = 0) {
+    const bool peer = stage > 0 && c->halo == SFV_HALO_PEER;
     auto args = [&](Block &b) {
         ViscArgs v{};
+        if (peer) {
+            static const int opp[4] = {1, 0, 3, 2};
+            v.peer = 1;
+            for (int e = 0; e < 4; ++e) {
+                const PeerView &pv = b.pv[e];
+                if (b.nbr[e] < 0 || !pv.grad) continue;
+                v.peer_grad[e] = pv.grad;
+                v.peer_PG[e] = pv.nj + 2;
+                v.peer_n[e] = e == 0 ? pv.ni : (e == 2 ? pv.nj : 0);
+                v.peer_gflag[e] = pv.flags + PEER_GFLAG_OFF / 8 + opp[e] * FLAG_STRIDE;
+                v.gwriters[e] = e < 2 ? (b.nj + 127) / 128 : b.ni;  // grad_kernel's grid: (ceil(nj/128), ni)
+            }
+            v.in_flag = b.flags;
+            v.in_gflag = b.flags + PEER_GFLAG_OFF / 8;
+            v.gcnt = reinterpret_cast<unsigned *>(reinterpret_cast<uint8_t *>(b.flags) + PEER_GCNT_OFF);
+            v.halo_err = c->halo_err;
+            v.step_ctr = c->step_ctr;
+            v.stage = stage;
+            v.nstages = nstages_of(c->cfg.rk);
+        }
         v.in = b.buf[in];
         v.met = b.met;
         v.grad = b.grad;
@@ -710,6 +735,13 @@ sfv_status enqueue_viscous(sfv_ctx *c, int in, cudaStream_t st) {
         else { CK(launch_grad(args(b), st)); all_fused = false; }  // (writes the physical ghost gradients too)
     }
     if (all_fused) return SFV_OK;
+    if (peer) {  // every block's grads (and their peer stores) precede every visc in stream order
+        for (Block &b : c->blocks) {
+            const bool iso = b.nbr[0] < 0 && b.nbr[1] < 0 && b.nbr[2] < 0 && b.nbr[3] < 0;
+            if (!(iso && fuse_ok)) CK(launch_visc(args(b), st));
+        }
+        return SFV_OK;
+    }
     if (c->nranks > 1) {
         // NCCL: this rank's block; rows (i-cuts) straight from / into the frame,
         // columns (j-cuts) through the pack buffers
@@ -840,7 +872,7 @@ sfv_status enqueue_step(sfv_ctx *c, cudaStream_t st, bool norms_batch) {
         const StageSpec sp = stage_spec(c->cfg.rk, k);
         if (c->cfg.viscous) {
             const int sv = span_begin(c, P_VISC, st);
-            sfv_status r = enqueue_viscous(c, sp.in, st);
+            sfv_status r = enqueue_viscous(c, sp.in, st, k);
             if (r != SFV_OK) return r;
             span_end(c, sv, st);
         }
@@ -1658,6 +1690,7 @@ sfv_status sfv_peer_connect(sfv_ctx *c, const void *handles) {
         PeerView &v = b.pv[e];
         for (int k = 0; k < 4; ++k) v.buf[k] = h.buf_off[k] >= 0 ? reinterpret_cast<double *>(w + h.buf_off[k]) : nullptr;
         v.flags = reinterpret_cast<unsigned long long *>(w + h.flags_off);
+        v.grad = c->cfg.viscous ? reinterpret_cast<double *>(w + h.flags_off + al(PEER_SYNC_BYTES)) : nullptr;
         v.PJ = h.PJ;
         v.ni = h.ni;
         v.nj = h.nj;
@@ -1682,8 +1715,6 @@ sfv_status sfv_set_halo_mode(sfv_ctx *c, int32_t mode) {
     if (!c) return SFV_ERR_ARG;
     if (!c->bound) return fail(c, SFV_ERR_SEQUENCE, "sfv_set_halo_mode before sfv_bind");
     if (mode != SFV_HALO_COPY && mode != SFV_HALO_PEER) return fail(c, SFV_ERR_ARG, "unknown halo mode %d", mode);
-    if (mode == SFV_HALO_PEER && c->cfg.viscous)
-        return fail(c, SFV_ERR_UNSUPPORTED, "Navier-Stokes mode uses SFV_HALO_COPY");
     if (mode == SFV_HALO_PEER && c->nranks > 1 && !c->peer_ready)
         return fail(c, SFV_ERR_SEQUENCE, "SFV_HALO_PEER across ranks needs sfv_peer_connect first");
     CK(cudaStreamSynchronize(c->st));
@@ -1696,6 +1727,7 @@ sfv_status sfv_set_halo_mode(sfv_ctx *c, int32_t mode) {
                 const Block &n = *local_block(c, b.nbr[e]);
                 for (int k = 0; k < 4; ++k) b.pv[e].buf[k] = n.buf[k];
                 b.pv[e].flags = n.flags;
+                b.pv[e].grad = n.grad;
                 b.pv[e].PJ = n.PJ;
                 b.pv[e].ni = n.ni;
                 b.pv[e].nj = n.nj;

@@ -103,7 +103,12 @@ struct StageArgs {
 };
 constexpr int FLAG_STRIDE = 16;   // u64 per inbound flag (own 128-B line)
 constexpr int CNT_STRIDE = 32;    // u32 per arrival counter
-constexpr size_t PEER_SYNC_BYTES = 1024;
+// per block: state flags [0, 512), state-writer counters [512, 1024), and in
+// Navier-Stokes peer mode gradient flags [1024, 1536), gradient-writer
+// counters [1536, 2048); the block's gradient frame follows at the next
+// 256-byte boundary on every rank (sfv_peer_connect derives it)
+constexpr size_t PEER_SYNC_BYTES = 2048;
+constexpr size_t PEER_ECNT_OFF = 512, PEER_GFLAG_OFF = 1024, PEER_GCNT_OFF = 1536;
 constexpr int SIG_RANKS_MAX = 32;
 // workspace misc region (same offsets on every rank)
 constexpr size_t MISC_BYTES = 2048;
@@ -144,6 +149,22 @@ struct ViscArgs {
     int ni, nj, PJ, PG;
     int bc[4];               // Edge per W, E, S, N (E_CONNECTED: exchanged ghosts)
     Params P;
+    // device-initiated halos (SFV_HALO_PEER): grad_kernel waits
+    // for the stage input's ghost layers (inbound state flags, sequence
+    // n*s + k - 1), stores its edge gradients into the neighbour's gradient
+    // frame and publishes n*s + k to the neighbour's inbound gradient flag;
+    // visc_kernel's edge CTAs wait for that flag.  peer = 0: copy mode.
+    int peer;
+    double *peer_grad[4];                  // neighbour's gradient frame per edge W, E, S, N (NULL: none)
+    int peer_PG[4], peer_n[4];             // its pitch, its ni (W) / nj (S)
+    unsigned long long *peer_gflag[4];     // neighbour's inbound gradient flag for the shared edge
+    const unsigned long long *in_flag;     // this block's inbound state flags [4 * FLAG_STRIDE]
+    unsigned long long *in_gflag;          // this block's inbound gradient flags [4 * FLAG_STRIDE]
+    unsigned *gcnt;                        // gradient-writer arrival counters [4 * CNT_STRIDE]
+    int gwriters[4];                       // CTAs of the grad launch touching each edge
+    unsigned *halo_err;
+    const long long *step_ctr;
+    int stage, nstages;
 };
 cudaError_t launch_grad(const ViscArgs &v, cudaStream_t st);
 cudaError_t launch_visc(const ViscArgs &v, cudaStream_t st);
@@ -151,7 +172,7 @@ cudaError_t launch_gradvisc(const ViscArgs &v, cudaStream_t st);  // blocks with
 cudaError_t launch_gradvisc_march(const ViscArgs &v, cudaStream_t st);  // (same, row-marching warps)
 cudaError_t launch_norms(const NormsArgs &f, cudaStream_t st);
 cudaError_t stage_occupancy(int mode, bool norms, bool dtmax, bool fast, bool peer, int *ctas_per_sm);
-cudaError_t stage_occupancy_visc(int mode, bool norms, bool dtmax, bool fast, int *ctas_per_sm);
+cudaError_t stage_occupancy_visc(int mode, bool norms, bool dtmax, bool fast, bool peer, int *ctas_per_sm);
 bool fast_path(const Params &P);
 cudaError_t prepare_stage_kernels();
 size_t stage_smem_bytes(int mode);

@@ -1159,15 +1159,15 @@ static cudaError_t occ_t(int *n) {
         case M_RES * 4 + 0: return FN<M_RES, false, false, F, Q, V>(__VA_ARGS__);        \
         default: return cudaErrorInvalidValue;                                           \
     }
-// (peer halos and Navier-Stokes are not combined: NS runs in copy mode)
 #define SFV_DISPATCH(FN, ...)                                                             \
-    if (peer && visc) return cudaErrorNotSupported;                                       \
     if (fast) {                                                                           \
-        if (peer) { SFV_DISPATCH_F(FN, true, true, false, __VA_ARGS__) }                  \
+        if (peer && visc) { SFV_DISPATCH_F(FN, true, true, true, __VA_ARGS__) }           \
+        else if (peer) { SFV_DISPATCH_F(FN, true, true, false, __VA_ARGS__) }             \
         else if (visc) { SFV_DISPATCH_F(FN, true, false, true, __VA_ARGS__) }             \
         else { SFV_DISPATCH_F(FN, true, false, false, __VA_ARGS__) }                      \
     } else {                                                                              \
-        if (peer) { SFV_DISPATCH_F(FN, false, true, false, __VA_ARGS__) }                 \
+        if (peer && visc) { SFV_DISPATCH_F(FN, false, true, true, __VA_ARGS__) }          \
+        else if (peer) { SFV_DISPATCH_F(FN, false, true, false, __VA_ARGS__) }            \
         else if (visc) { SFV_DISPATCH_F(FN, false, false, true, __VA_ARGS__) }            \
         else { SFV_DISPATCH_F(FN, false, false, false, __VA_ARGS__) }                     \
     }
@@ -1183,18 +1183,18 @@ cudaError_t stage_occupancy(int mode, bool norms, bool dtmax, bool fast, bool pe
     const bool visc = false;
     SFV_DISPATCH(occ_t, n)
 }
-cudaError_t stage_occupancy_visc(int mode, bool norms, bool dtmax, bool fast, int *n) {
-    const bool peer = false, visc = true;
+cudaError_t stage_occupancy_visc(int mode, bool norms, bool dtmax, bool fast, bool peer, int *n) {
+    const bool visc = true;
     SFV_DISPATCH(occ_t, n)
 }
 cudaError_t prepare_stage_kernels() {
     const int variants[9][3] = {{M_OWN, 1, 0}, {M_OWN, 0, 0}, {M_UN, 0, 0}, {M_UN, 0, 1},  {M_RK4F, 0, 1},
                                 {M_RK4F, 0, 0}, {M_HEUNF, 0, 1}, {M_HEUNF, 0, 0}, {M_RES, 0, 0}};
     for (auto &v : variants)
-        for (int f = 0; f < 6; ++f) {
+        for (int f = 0; f < 8; ++f) {
             int n = 0;
             cudaError_t e = f < 4 ? stage_occupancy(v[0], v[1] != 0, v[2] != 0, (f & 1) != 0, (f & 2) != 0, &n)
-                                  : stage_occupancy_visc(v[0], v[1] != 0, v[2] != 0, (f & 1) != 0, &n);
+                                  : stage_occupancy_visc(v[0], v[1] != 0, v[2] != 0, (f & 1) != 0, (f & 2) != 0, &n);
             if (e != cudaSuccess) return e;
         }
     return cudaSuccess;
@@ -1319,26 +1319,69 @@ __device__ __forceinline__ void gg_cell(const double *met, int PJ, int i, int j,
     gg_core(m0, m1, mn, c, w, e, s, n, g);
 }
 
+// Peer mode (a.peer): edges whose ghosts a CTA of grad_kernel / visc_kernel
+// (grid (ceil(nj/128), ni), one cell per thread) reads: W row 0, E row ni-1,
+// S the CTA holding column 0, N the one holding column nj-1
+__device__ __forceinline__ unsigned visc_touch(const ViscArgs &a) {
+    const int i = blockIdx.y;
+    return (a.peer_grad[0] && i == 0 ? 1u : 0u) | (a.peer_grad[1] && i == a.ni - 1 ? 2u : 0u) |
+           (a.peer_grad[2] && blockIdx.x == 0 ? 4u : 0u) | (a.peer_grad[3] && blockIdx.x == gridDim.x - 1 ? 8u : 0u);
+}
+
 __global__ void grad_kernel(const ViscArgs a) {
     const int j = blockIdx.x * blockDim.x + threadIdx.x, i = blockIdx.y;
-    if (j >= a.nj) return;
-    double c[3], w[3], e[3], s[3], n[3], g[6];
-    uvT(a.in, a.PJ, i, j, a.P, c);
-    uvT(a.in, a.PJ, i - 1, j, a.P, w);
-    uvT(a.in, a.PJ, i + 1, j, a.P, e);
-    uvT(a.in, a.PJ, i, j - 1, a.P, s);
-    uvT(a.in, a.PJ, i, j + 1, a.P, n);
-    gg_cell(a.met, a.PJ, i, j, c, w, e, s, n, g);
-    // physical-edge ghost cells take this cell's gradient (reading N-R1)
-    const bool gw = i == 0 && a.bc[0] != E_CONNECTED, ge = i == a.ni - 1 && a.bc[1] != E_CONNECTED;
-    const bool gs = j == 0 && a.bc[2] != E_CONNECTED, gn = j == a.nj - 1 && a.bc[3] != E_CONNECTED;
+    const unsigned touch = a.peer ? visc_touch(a) : 0u;
+    unsigned long long seq = 0;
+    if (touch) {  // CTA-uniform: the stage input's ghost layers are the neighbour's stage k-1 edge rows
+        seq = (unsigned long long)(*a.step_ctr * a.nstages + a.stage);
 #pragma unroll
-    for (int q = 0; q < 6; ++q) {
-        *gradp(a.grad, a.PG, i, j, q) = g[q];
-        if (gw) *gradp(a.grad, a.PG, -1, j, q) = g[q];
-        if (ge) *gradp(a.grad, a.PG, a.ni, j, q) = g[q];
-        if (gs) *gradp(a.grad, a.PG, i, -1, q) = g[q];
-        if (gn) *gradp(a.grad, a.PG, i, a.nj, q) = g[q];
+        for (int e = 0; e < 4; ++e)
+            if (touch & (1u << e)) wait_flag(a.in_flag + e * FLAG_STRIDE, seq - 1, a.halo_err);
+    }
+    if (j < a.nj) {
+        double c[3], w[3], e[3], s[3], n[3], g[6];
+        uvT(a.in, a.PJ, i, j, a.P, c);
+        uvT(a.in, a.PJ, i - 1, j, a.P, w);
+        uvT(a.in, a.PJ, i + 1, j, a.P, e);
+        uvT(a.in, a.PJ, i, j - 1, a.P, s);
+        uvT(a.in, a.PJ, i, j + 1, a.P, n);
+        gg_cell(a.met, a.PJ, i, j, c, w, e, s, n, g);
+        // physical-edge ghost cells take this cell's gradient (reading N-R1)
+        const bool gw = i == 0 && a.bc[0] != E_CONNECTED, ge = i == a.ni - 1 && a.bc[1] != E_CONNECTED;
+        const bool gs = j == 0 && a.bc[2] != E_CONNECTED, gn = j == a.nj - 1 && a.bc[3] != E_CONNECTED;
+        // peer edges: the neighbour's ghost gradient is this edge cell's (bit copy)
+        const bool pw = (touch & 1u) != 0, pe = (touch & 2u) != 0;
+        const bool ps = (touch & 4u) && j == 0, pn = (touch & 8u) && j == a.nj - 1;
+#pragma unroll
+        for (int q = 0; q < 6; ++q) {
+            *gradp(a.grad, a.PG, i, j, q) = g[q];
+            if (gw) *gradp(a.grad, a.PG, -1, j, q) = g[q];
+            if (ge) *gradp(a.grad, a.PG, a.ni, j, q) = g[q];
+            if (gs) *gradp(a.grad, a.PG, i, -1, q) = g[q];
+            if (gn) *gradp(a.grad, a.PG, i, a.nj, q) = g[q];
+            if (pw) *gradp(a.peer_grad[0], a.peer_PG[0], a.peer_n[0], j, q) = g[q];
+            if (pe) *gradp(a.peer_grad[1], a.peer_PG[1], -1, j, q) = g[q];
+            if (ps) *gradp(a.peer_grad[2], a.peer_PG[2], i, a.peer_n[2], q) = g[q];
+            if (pn) *gradp(a.peer_grad[3], a.peer_PG[3], i, -1, q) = g[q];
+        }
+    }
+    if (touch) {
+        // arrival of this CTA on every peer edge it touches; the launch's last
+        // writer on an edge publishes the sequence to the neighbour's gradient flag
+        __threadfence_system();
+        __syncthreads();
+        if (threadIdx.x == 0) {
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                if (!(touch & (1u << e))) continue;
+                unsigned *cnt = a.gcnt + e * CNT_STRIDE;
+                if (atom_add_acq_rel_gpu(cnt, 1u) == (unsigned)a.gwriters[e] - 1u) {
+                    *cnt = 0u;
+                    __threadfence_system();
+                    st_release_sys(a.peer_gflag[e], seq);
+                }
+            }
+        }
     }
 }
 
@@ -1386,6 +1429,18 @@ __device__ __forceinline__ void store_rv(const ViscArgs &a, int i, int j, const 
 
 __global__ void visc_kernel(const ViscArgs a) {
     const int j = blockIdx.x * blockDim.x + threadIdx.x, i = blockIdx.y;
+    if (a.peer) {
+        const unsigned touch = visc_touch(a);
+        if (touch) {  // the neighbours' edge gradients of this stage (and, already met, its ghost state)
+            const unsigned long long seq = (unsigned long long)(*a.step_ctr * a.nstages + a.stage);
+#pragma unroll
+            for (int e = 0; e < 4; ++e)
+                if (touch & (1u << e)) {
+                    wait_flag(a.in_flag + e * FLAG_STRIDE, seq - 1, a.halo_err);
+                    wait_flag(a.in_gflag + e * FLAG_STRIDE, seq, a.halo_err);
+                }
+        }
+    }
     if (j >= a.nj) return;
     double c[3], w[3], e[3], s[3], n[3];
     uvT(a.in, a.PJ, i, j, a.P, c);

@@ -7,7 +7,8 @@ sys.path.insert(0, '.')
 from paper_2305_18057_b200 import inputs as I, sfv
 for (ni, nj, px, py, rk, peer, ns) in [(64, 32, 1, 1, 0, 0, 0), (40, 36, 2, 2, 0, 0, 0), (96, 48, 1, 1, 1, 0, 0),
                                        (96, 48, 3, 1, 2, 0, 0), (40, 36, 2, 2, 0, 1, 0), (96, 48, 3, 1, 2, 1, 0),
-                                       (64, 70, 1, 3, 1, 1, 0), (70, 45, 1, 1, 0, 0, 1), (64, 40, 2, 2, 0, 0, 1)]:
+                                       (64, 70, 1, 3, 1, 1, 0), (70, 45, 1, 1, 0, 0, 1), (64, 40, 2, 2, 0, 0, 1),
+                                       (64, 40, 2, 2, 0, 1, 1), (90, 70, 1, 3, 1, 1, 1)]:
     X, Y = I.ramp_nodes(ni, nj, 5.0 if ns else 30.0)
     cfg = I.default_config(ni, nj, rk=rk, **(dict(viscous=1, mu=0.1, bc=(0, 1, 3, 2)) if ns else {}))
     g = sfv.Solver(cfg, X, Y, px=px, py=py)

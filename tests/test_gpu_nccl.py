@@ -119,17 +119,20 @@ def test_nccl_ranks_match_loopback_and_oracle(oracle_mod, world, px, py, overlap
     assert dt_error(res[0][4], o.dt()) <= 1e-13
 
 
-@pytest.mark.parametrize("world,px,py", [(2, 2, 1), (2, 1, 2), (4, 2, 2)])
-def test_nccl_navier_stokes_ranks(oracle_mod, world, px, py):
+@pytest.mark.parametrize("world,px,py,halo", [(2, 2, 1, "copy"), (2, 1, 2, "copy"), (4, 2, 2, "copy"),
+                                               (2, 2, 1, "peer"), (2, 1, 2, "peer"), (4, 2, 2, "peer")])
+def test_nccl_navier_stokes_ranks(oracle_mod, world, px, py, halo):
     """Navier-Stokes across NCCL ranks: ghost gradients travel by send/recv
-    (rows from the frame, columns packed); bitwise equal to loopback blocks
-    and within the parity gates of the oracle."""
+    (rows from the frame, columns packed) or, halo="peer", grad_kernel stores
+    them into the neighbour rank's gradient frame through its CUDA-IPC
+    mapping; bitwise equal to loopback blocks and within the parity gates of
+    the oracle."""
     from paper_2305_18057_b200 import inputs as I
     from paper_2305_18057_b200 import sfv
     from parity_util import state_error
     ni, nj, steps = 96, 48, 30
     visc = dict(viscous=1, mu=0.1, bc=(I.BC_INFLOW, I.BC_OUTFLOW, I.BC_NOSLIP_WALL, I.BC_SLIP_WALL))
-    res = _run(world, px, py, ni, nj, steps, 1, "copy", 0, None, visc)
+    res = _run(world, px, py, ni, nj, steps, 1, halo, 0, None, visc)
     U = res[0][2]
     X, Y = I.ramp_nodes(ni, nj, 5.0)
     cfg = I.default_config(ni, nj, **visc)

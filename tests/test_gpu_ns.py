@@ -91,13 +91,37 @@ def test_ns_loopback_bitwise(sfv_mod, oracle_mod, px, py):
     assert np.all(state_error(gp.get_state(), o.get_state()) <= 1e-11)
 
 
-def test_ns_peer_mode_unsupported(sfv_mod):
-    ni, nj = 32, 16
-    X, Y = I.ramp_nodes(ni, nj, 15.0)
-    g = sfv_mod.Solver(I.default_config(ni, nj, viscous=1, mu=0.1), X, Y, px=2)
-    with pytest.raises(sfv_mod.SfvError) as ex:
-        g.set_halo_mode(sfv_mod.HALO_PEER)
-    assert ex.value.code == sfv_mod.ERR_UNSUPPORTED
+@pytest.mark.parametrize("px,py,rk", [(2, 1, 0), (1, 3, 0), (2, 2, 0), (3, 2, 1), (2, 2, 2)])
+def test_ns_peer_loopback_bitwise(sfv_mod, oracle_mod, px, py, rk):
+    """Navier-Stokes with device-initiated halos (SFV_HALO_PEER): the stage
+    kernels store the state edge layers, grad_kernel the edge gradients into
+    the neighbour block's frames and signal; visc_kernel's edge CTAs wait.
+    Bit copies, so bitwise equal to one block."""
+    ni, nj, steps = 90, 70, 20
+    X, Y = I.ramp_nodes(ni, nj, 5.0)
+    cfg = I.default_config(ni, nj, viscous=1, mu=0.2, bc=NOSLIP_S, rk=rk)
+    U0 = I.perturbed_state(ni, nj, 8)
+    g1 = sfv_mod.Solver(cfg, X, Y); g1.set_state(U0); g1.step(steps); g1.sync()
+    gp = sfv_mod.Solver(cfg, X, Y, px=px, py=py)
+    gp.enable_peer_halo()
+    gp.set_state(U0); gp.step(steps); gp.sync()
+    np.testing.assert_array_equal(gp.get_state(), g1.get_state())
+    np.testing.assert_array_equal(gp.dt(), g1.dt())
+    o = oracle_mod.Oracle(cfg, X, Y); o.set_state(U0); o.step(steps)
+    assert np.all(state_error(gp.get_state(), o.get_state()) <= 1e-11)
+
+
+def test_ns_peer_then_copy_mode(sfv_mod):
+    """Switching the halo mode back and forth keeps the NS results bitwise."""
+    ni, nj = 64, 40
+    X, Y = I.ramp_nodes(ni, nj, 5.0)
+    cfg = I.default_config(ni, nj, viscous=1, mu=0.1, bc=NOSLIP_S)
+    U0 = I.perturbed_state(ni, nj, 4)
+    g = sfv_mod.Solver(cfg, X, Y, px=2, py=2)
+    g.enable_peer_halo(); g.set_state(U0); g.step(10); g.sync()
+    Up = g.get_state()
+    g.set_halo_mode(sfv_mod.HALO_COPY); g.set_state(U0); g.step(10); g.sync()
+    np.testing.assert_array_equal(g.get_state(), Up)
 
 
 def test_ns_operator_matches_oracle(sfv_mod, oracle_mod):
