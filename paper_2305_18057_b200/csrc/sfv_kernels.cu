@@ -1532,9 +1532,28 @@ constexpr int VM_OUT = 28;
 #ifndef SFV_NS_MBLK
 #define SFV_NS_MBLK 2
 #endif
+#ifndef SFV_NS_RING
+#define SFV_NS_RING 0  // rows of a per-warp cp.async prefetch ring (0: one row ahead in registers; 3 and 4 measured -1 % / -2.5 %, profiles/r2e_ab_ns_ring.txt)
+#endif
+constexpr int VM_RF = 14;  // doubles per lane and row in the ring: raw state (4) + metrics (10)
+constexpr size_t VM_SMEM = SFV_NS_RING > 0 ? (size_t)4 * SFV_NS_RING * VM_RF * 32 * sizeof(double) : 0;
+__device__ __forceinline__ void cp_async8(unsigned dst, const double *src) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(dst), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
 __global__ void __launch_bounds__(128, SFV_NS_MBLK) gradvisc_march_kernel(const ViscArgs a, int nstrips, int nseg) {
     const int lane = threadIdx.x & 31, task = blockIdx.x * 4 + (threadIdx.x >> 5);
     if (task >= nstrips * nseg) return;
+#if SFV_NS_RING > 0
+    // per-warp ring [SFV_NS_RING][VM_RF][32]: slot r % SFV_NS_RING holds state
+    // row r and metrics row r of this lane's columns (each lane copies and
+    // reads only its own elements: no warp synchronisation)
+    extern __shared__ double vm_ring[];
+    double *ring = vm_ring + (size_t)(threadIdx.x >> 5) * SFV_NS_RING * VM_RF * 32 + lane;
+#endif
     const int strip = task % nstrips, seg = task / nstrips;
     const int jc = strip * VM_OUT - 2 + lane;  // this lane's column (may lie in the ghost frame or beyond)
     const int i_s = (int)(((long long)a.ni * seg) / nseg), i_e = (int)(((long long)a.ni * (seg + 1)) / nseg);
@@ -1577,6 +1596,25 @@ __global__ void __launch_bounds__(128, SFV_NS_MBLK) gradvisc_march_kernel(const 
             g[q] = jc == -1 ? fromE : (jc == a.nj ? fromW : g[q]);
         }
     };
+#if SFV_NS_RING > 0
+    // ring entry r (state row r, metrics row r; rows <= ni exist) -> slot r % SFV_NS_RING;
+    // one commit group per entry (empty past the last row) so wait_group counts rows
+    auto issue_ring = [&](int r) {
+        if (r <= a.ni) {
+            const unsigned d = (unsigned)__cvta_generic_to_shared(ring + (size_t)(r % SFV_NS_RING) * VM_RF * 32);
+            const double *ps = a.in + (size_t)((r + 2) * 4) * PJ + (jl + JOFF);
+#pragma unroll
+            for (int c = 0; c < 4; ++c) cp_async8(d + c * 256, ps + (size_t)c * PJ);
+#pragma unroll
+            for (int f = 0; f < 7; ++f) cp_async8(d + (4 + f) * 256, a.met + (size_t)(r * NMET + f) * PJ + jg + JOFF);
+#pragma unroll
+            for (int f = 0; f < 3; ++f)
+                cp_async8(d + (11 + f) * 256, a.met + (size_t)(r * NMET + 3 + f) * PJ + jn + JOFF);
+        }
+        cp_async_commit();
+    };
+    for (int r = i_s + 2; r < i_s + 2 + SFV_NS_RING; ++r) issue_ring(r);  // in flight during the prologue
+#endif
     // ---- prologue: rows i_s-1 .. i_s+1, gradients of rows i_s-1 and i_s, W face of row i_s
     double uA[3], uB[3], uC[3], g1[6], FW[4];
     double mr1[10], mr2[10];  // metrics rows v+1, v+2
@@ -1603,10 +1641,12 @@ __global__ void __launch_bounds__(128, SFV_NS_MBLK) gradvisc_march_kernel(const 
         // rotate to the loop state: uA = row v, uB = row v+1 (uC), mr1 = row v+1
 #pragma unroll
         for (int k = 0; k < 3; ++k) { uA[k] = uB[k]; uB[k] = uC[k]; }
+#if SFV_NS_RING == 0
         if (i_s + 1 < a.ni) {
             load_met(i_s + 2, mr2);
             load_state(i_s + 2, sN2);
         }
+#endif
     }
     // loop state at the top of iteration v: uA = (u, v, T) of row v, uB = row
     // v+1, g1 = gradient of row v, FW = W face flux of row v, mr1 = metrics
@@ -1616,13 +1656,25 @@ __global__ void __launch_bounds__(128, SFV_NS_MBLK) gradvisc_march_kernel(const 
         double gn[6];
         if (v + 1 < a.ni) {
             double uN[3];
+#if SFV_NS_RING > 0
+            {  // ring entry v+2: state and metrics rows v+2
+                cp_async_wait<SFV_NS_RING - 1>();
+                const double *sl = ring + (size_t)((v + 2) % SFV_NS_RING) * VM_RF * 32;
+#pragma unroll
+                for (int c = 0; c < 4; ++c) sN2[c] = sl[c * 32];
+#pragma unroll
+                for (int f = 0; f < 10; ++f) mr2[f] = sl[(4 + f) * 32];
+            }
+#endif
             to_uvt(sN2, uN);  // row v+2
+#if SFV_NS_RING == 0
             // prefetch one row ahead: state row v+3, metrics row v+4
             double sN3[4], mN[10];
             if (v + 2 < a.ni) {
                 load_state(v + 3, sN3);
                 load_met(v + 3, mN);
             }
+#endif
             grad_row(mr1, mr2, uB, uA, uN, gn);  // row v+1
             // E face of row v (i-face v+1: metrics row v+1 fields 0-2), N face (row v+1 fields 3-5 at jn)
             double FE[4], FN[4], FS[4];
@@ -1644,10 +1696,16 @@ __global__ void __launch_bounds__(128, SFV_NS_MBLK) gradvisc_march_kernel(const 
             for (int q = 0; q < 6; ++q) g1[q] = gn[q];
 #pragma unroll
             for (int k = 0; k < 3; ++k) { uA[k] = uB[k]; uB[k] = uN[k]; }
+#if SFV_NS_RING > 0
+#pragma unroll
+            for (int f = 0; f < 10; ++f) mr1[f] = mr2[f];
+            issue_ring(v + 2 + SFV_NS_RING);  // into the slot just read
+#else
 #pragma unroll
             for (int f = 0; f < 10; ++f) { mr1[f] = mr2[f]; mr2[f] = mN[f]; }
 #pragma unroll
             for (int c = 0; c < 4; ++c) sN2[c] = sN3[c];
+#endif
         } else {
             // last row (v = ni-1): the E neighbour is the ghost row ni, whose
             // gradient is row ni-1's (physical E edge)
@@ -1666,6 +1724,9 @@ __global__ void __launch_bounds__(128, SFV_NS_MBLK) gradvisc_march_kernel(const 
             if (lane >= 2 && lane < 2 + VM_OUT && jc < a.nj) store_rv(a, v, jc, FW, FE, FS, FN);
         }
     }
+#if SFV_NS_RING > 0
+    cp_async_wait<0>();
+#endif
 }
 
 cudaError_t launch_gradvisc_march(const ViscArgs &v, cudaStream_t st) {
@@ -1676,7 +1737,9 @@ cudaError_t launch_gradvisc_march(const ViscArgs &v, cudaStream_t st) {
         int dev = 0, nsm = 0, blk = 0;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blk, gradvisc_march_kernel, 128, 0);
+        if (VM_SMEM > 48 * 1024)
+            cudaFuncSetAttribute(gradvisc_march_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)VM_SMEM);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blk, gradvisc_march_kernel, 128, VM_SMEM);
         resident = std::max(1, nsm * std::max(1, blk) * 4);
     }
     const int nstrips = (v.nj + VM_OUT - 1) / VM_OUT;
@@ -1685,7 +1748,7 @@ cudaError_t launch_gradvisc_march(const ViscArgs &v, cudaStream_t st) {
     if (er && *er) nseg = std::max(1, (v.ni + std::max(4, atoi(er)) - 1) / std::max(4, atoi(er)));
     nseg = std::min(nseg, std::max(1, v.ni / 4));
     const int tasks = nstrips * nseg;
-    gradvisc_march_kernel<<<(tasks + 3) / 4, 128, 0, st>>>(v, nstrips, nseg);
+    gradvisc_march_kernel<<<(tasks + 3) / 4, 128, VM_SMEM, st>>>(v, nstrips, nseg);
     return cudaGetLastError();
 }
 
