@@ -281,10 +281,35 @@ def run_reference(args, rank, world):
             "cpu_baseline": {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample,
                              "cpu_model": cpu_model(), "affinity_cores": len(os.sched_getaffinity(0))},
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
-    print(json.dumps(line), flush=True)
+    emit(line)
+
+
+# The JSON line goes to the process's original stdout; everything else that
+# writes to fd 1 while the run is in flight (NCCL's "NCCL version" banner when
+# NCCL_DEBUG is set, library diagnostics) is sent to stderr, so stdout holds
+# exactly one line per run.
+_JSON_FD = None
+
+
+def quiet_stdout():
+    global _JSON_FD
+    if _JSON_FD is None:
+        sys.stdout.flush()
+        _JSON_FD = os.dup(1)
+        os.dup2(2, 1)
+
+
+def emit(line):
+    data = (json.dumps(line) + "\n").encode()
+    if _JSON_FD is None:
+        sys.stdout.write(data.decode())
+        sys.stdout.flush()
+    else:
+        os.write(_JSON_FD, data)
 
 
 def main():
+    quiet_stdout()
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=None,
@@ -368,8 +393,6 @@ def main():
                         device=local_rank, stream=stream)
     nblk = px if world == 1 else 1
     halo_note = args.halo
-    if args.ns:
-        args.halo = "copy"  # NS runs with copy-mode halos (single rank)
     if args.halo == "peer" and px > 1:
         if world == 1:
             solver.enable_peer_halo()
@@ -582,7 +605,7 @@ def main():
         opr = operand_roofline(args, line["clocks"], avg_launch_s, nj, ni, world, nblk)
         if opr and isinstance(roof, dict) and roof.get("bound") == "alu":
             roof["operand"] = opr
-        print(json.dumps(line), flush=True)
+        emit(line)
     if world > 1:
         dist.destroy_process_group()
 
