@@ -1535,6 +1535,9 @@ constexpr int VM_OUT = 28;
 #ifndef SFV_NS_RING
 #define SFV_NS_RING 0  // rows of a per-warp cp.async prefetch ring (0: one row ahead in registers; 3 and 4 measured -1 % / -2.5 %, profiles/r2e_ab_ns_ring.txt)
 #endif
+#ifndef SFV_NS_JEDGE
+#define SFV_NS_JEDGE 1  // physical ghost-column gradient shuffles only in the edge strips
+#endif
 constexpr int VM_RF = 14;  // doubles per lane and row in the ring: raw state (4) + metrics (10)
 constexpr size_t VM_SMEM = SFV_NS_RING > 0 ? (size_t)4 * SFV_NS_RING * VM_RF * 32 * sizeof(double) : 0;
 __device__ __forceinline__ void cp_async8(unsigned dst, const double *src) {
@@ -1560,6 +1563,7 @@ __global__ void __launch_bounds__(128, SFV_NS_MBLK) gradvisc_march_kernel(const 
     const int jl = min(max(jc, -2), a.nj + 1);   // loadable column (state)
     const int jg = min(max(jc, 0), a.nj - 1);    // interior column (metrics of a cell)
     const int jn = min(max(jc + 1, 0), a.nj);    // the N j-face's column
+    const bool jedge = strip * VM_OUT - 2 <= -1 || strip * VM_OUT + 29 >= a.nj;  // physical ghost column in the warp
     const int PJ = a.PJ;
     // raw state of row r at this lane's column; metric values a row's gradient
     // and faces need (see gg_core): i-face row fields 0..2 at jg, fields 3..6
@@ -1590,10 +1594,13 @@ __global__ void __launch_bounds__(128, SFV_NS_MBLK) gradvisc_march_kernel(const 
         const double m0[3] = {mA[0], mA[1], mA[2]};
         const double mn[3] = {mB[7], mB[8], mB[9]};
         gg_core(m0, mB, mn, c, w, e, sS, sN, g);
+        if (!SFV_NS_JEDGE || jedge) {  // warp-uniform: only strips holding column -1 or nj
 #pragma unroll
-        for (int q = 0; q < 6; ++q) {
-            const double fromE = __shfl_down_sync(0xffffffffu, g[q], 1), fromW = __shfl_up_sync(0xffffffffu, g[q], 1);
-            g[q] = jc == -1 ? fromE : (jc == a.nj ? fromW : g[q]);
+            for (int q = 0; q < 6; ++q) {
+                const double fromE = __shfl_down_sync(0xffffffffu, g[q], 1),
+                             fromW = __shfl_up_sync(0xffffffffu, g[q], 1);
+                g[q] = jc == -1 ? fromE : (jc == a.nj ? fromW : g[q]);
+            }
         }
     };
 #if SFV_NS_RING > 0
