@@ -178,6 +178,15 @@ def measured_peak():
 # impulsive Mach-4 start against a no-slip 30-degree ramp is not stable under the inviscid CFL
 # (it fails within a few steps on the C2 grid); the no-slip wall is exercised by tests/test_gpu_ns.py.
 NS_MU = 1.0e-3
+# Navier-Stokes workload: the C2 grid with a 5-degree ramp and a no-slip adiabatic
+# ramp wall (an impulsive Mach-4 start against a no-slip 30-degree
+# ramp gives invalid MUSCL face states within ~20 steps at mu <= 1e-2,
+# profiles/r1_ns_noslip_probe.txt; the 5-degree ramp runs)
+NS_THETA = 5.0
+
+
+def ns_kwargs():
+    return dict(viscous=1, mu=NS_MU, bc=(I.BC_INFLOW, I.BC_OUTFLOW, I.BC_NOSLIP_WALL, I.BC_SLIP_WALL))
 
 
 def cpu_model():
@@ -192,8 +201,8 @@ def cpu_model():
 
 def _time_oracle(omp, budget_s, ni, rows, ns, threads=None):
     import oracle
-    X, Y = I.ramp_nodes(ni, rows, 30.0)
-    cfg = I.default_config(ni, rows, **(dict(viscous=1, mu=NS_MU) if ns else {}))
+    X, Y = I.ramp_nodes(ni, rows, NS_THETA if ns else 30.0)
+    cfg = I.default_config(ni, rows, **(ns_kwargs() if ns else {}))
     o = oracle.Oracle(cfg, X, Y, omp=omp)
     o.set_state(I.uniform_state(ni, rows))
     o.step(1)  # warm
@@ -376,12 +385,14 @@ def main():
     if world == 1 and args.blocks > 1:
         px = args.blocks
         desc += f"; {px} loopback slabs on one GPU"
+    if args.ns:
+        theta = NS_THETA
+        desc = (f"Navier-Stokes terms (mu = 1e-3, Green-Gauss gradients, no-slip adiabatic ramp wall, "
+                f"{NS_THETA:g}-deg ramp) on " + desc.replace("30-deg ramp", f"{NS_THETA:g}-deg ramp"))
     X, Y = I.ramp_nodes(ni, nj, theta)
     rk = {"rk4": I.RK4_CLASSIC, "heun": I.RK2_HEUN, "jst4": I.RK4_JAMESON}[args.rk]
     cfg = I.default_config(ni, nj, rk=rk, max_history=max(args.steps + args.warmup + 16, 64),
-                           **(dict(viscous=1, mu=NS_MU) if args.ns else {}))
-    if args.ns:
-        desc = "Navier-Stokes terms (mu = 1e-3, Green-Gauss gradients; slip walls) on " + desc
+                           **(ns_kwargs() if args.ns else {}))
     U0 = I.uniform_state(ni, nj)
     nccl_id = None
     if world > 1:
