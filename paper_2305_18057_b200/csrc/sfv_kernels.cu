@@ -137,6 +137,12 @@ __device__ __forceinline__ double frcp(double d) {
 #ifndef SFV_DIET
 #define SFV_DIET 0  // FP64 diet v2: limiter max-form, rho tests folded into a~^2 > 0, |x| by a sign-bit mask
 #endif
+#ifndef SFV_WALL_FIRST
+#define SFV_WALL_FIRST 1  // edge strips' tasks at the lowest blockIdx (high issue priority)
+#endif
+#ifndef SFV_GHOST_LEAN
+#define SFV_GHOST_LEAN 1  // S/N wall ghosts: per-lane mode and column decided once per task
+#endif
 #ifndef SFV_LIM_RCP2
 #define SFV_LIM_RCP2 1
 #endif
@@ -443,8 +449,20 @@ __global__ void __launch_bounds__(NT, StageTraits<MODE>::MINW / WPC) stage_kerne
     if (task < ntask1 + a.nstrips * a.nseg2) {
         const bool trailing = task >= ntask1;
         const int tt = trailing ? task - ntask1 : task;
-        const int strip = tt % a.nstrips;
-        const int seg = tt / a.nstrips;
+        int strip = tt % a.nstrips, seg = tt / a.nstrips;
+        if (SFV_WALL_FIRST && !trailing && a.nstrips >= 3) {
+            // the two edge strips' tasks first: the lowest blockIdx take the
+            // sub-partitions' high-priority warp slots, and these strips carry the
+            // per-row wall-ghost work (profiles/r2e_timeline_strips.txt)
+            const int nb = 2 * a.nseg;
+            if (tt < nb) {
+                strip = (tt & 1) ? a.nstrips - 1 : 0;
+                seg = tt >> 1;
+            } else {
+                strip = 1 + (tt - nb) % (a.nstrips - 2);
+                seg = (tt - nb) / (a.nstrips - 2);
+            }
+        }
         const int j0 = strip * WOUT;
         const int j1 = min(j0 + WOUT, a.nj);
         const int jc = j0 - 1 + CPL * lane;          // this lane's first column (CPL columns per lane)
@@ -464,6 +482,24 @@ __global__ void __launch_bounds__(NT, StageTraits<MODE>::MINW / WPC) stage_kerne
         // whose staged columns reach j = -1 / nj
         const bool ghost_sn = (writes_ghost(2) && j0 == 0) || (writes_ghost(3) && j1 >= a.nj - 1);
         const bool ghost_w = writes_ghost(0), ghost_e = writes_ghost(1);
+#if SFV_GHOST_LEAN
+        // S / N physical-wall ghosts this lane writes every row (reading A-R11):
+        // mode per wall (1 slip mirror, 2 outflow copy into 2 columns, 3 no-slip;
+        // bits 0-1 S, 2-3 N), decided once per task instead of per row
+        int gmode[CPL];
+#pragma unroll
+        for (int k = 0; k < CPL; ++k) {
+            const int jk = jc + k;
+            int mS = 0, mN = 0;
+            if (a.bc[2] == E_SLIP && jk <= 1) mS = 1;
+            else if (a.bc[2] == E_OUTFLOW && jk == 0) mS = 2;
+            else if (VISC && a.bc[2] == E_NOSLIP && jk <= 1) mS = 3;
+            if (a.bc[3] == E_SLIP && jk >= a.nj - 2) mN = 1;
+            else if (a.bc[3] == E_OUTFLOW && jk == a.nj - 1) mN = 2;
+            else if (VISC && a.bc[3] == E_NOSLIP && jk >= a.nj - 2) mN = 3;
+            gmode[k] = is_out[k] ? (mS | mN << 2) : 0;
+        }
+#endif
         const int lo = trailing ? a.row_split : a.row_lo, ns = trailing ? a.nseg2 : a.nseg;
         const int nrows = (trailing ? a.row_hi : a.row_split) - lo;
         const int i_start = lo + (int)(((long long)nrows * seg) / ns);
@@ -813,7 +849,25 @@ __global__ void __launch_bounds__(NT, StageTraits<MODE>::MINW / WPC) stage_kerne
                 bad |= (is_out[k] & (!okE[k] | !st_ok)) | (jflux[k] & !okS[k]);
                 // physical-boundary ghosts of the new state (reading A-R11), behind one
                 // warp-uniform test: only strips at the S / N walls and rows 0, 1, ni-2, ni-1
+#if SFV_GHOST_LEAN
+                if (MODE != M_RES && ghost_sn) {  // warp-uniform: the S / N wall strips
+                    // column 0's (S) / column nj's (N) j-face normal sits at staged index 2 - j0 (+ nj)
+                    auto wall = [&](int m, int col, int kk, int col2) {
+                        double g[4];
+                        if (m == 1) mirror(U, mv[3 * WROW + kk], mv[4 * WROW + kk], g);
+                        else if (m == 3) { g[0] = U[0]; g[1] = -U[1]; g[2] = -U[2]; g[3] = U[3]; }
+                        else { g[0] = U[0]; g[1] = U[1]; g[2] = U[2]; g[3] = U[3]; }
+                        store4(a.out, PJ, v, col, g);
+                        if (m == 2) store4(a.out, PJ, v, col2, U);
+                    };
+                    if (gmode[k] & 3) wall(gmode[k] & 3, -1 - jk, 2 - j0, -2);  // (outflow: jk = 0 -> column -1)
+                    if (gmode[k] >> 2) wall(gmode[k] >> 2, a.nj + (a.nj - 1 - jk), 2 - j0 + a.nj, a.nj + 1);
+                }
+                if (MODE != M_RES && ((ghost_w && v <= 1) || (ghost_e && v >= a.ni - 2)) && is_out[k]) {
+#else
                 if (MODE != M_RES && (ghost_sn || (ghost_w && v <= 1) || (ghost_e && v >= a.ni - 2)) && is_out[k]) {
+#endif
+#if !SFV_GHOST_LEAN
                     if (a.bc[2] == E_SLIP && jk <= 1) {
                         double g[4];
                         const int k0 = o - jk;  // column 0
@@ -838,6 +892,7 @@ __global__ void __launch_bounds__(NT, StageTraits<MODE>::MINW / WPC) stage_kerne
                         const double g[4] = {U[0], -U[1], -U[2], U[3]};
                         store4(a.out, PJ, v, a.nj + (a.nj - 1 - jk), g);
                     }
+#endif
                     if (a.bc[0] == E_SLIP && v <= 1) {  // segments start at 0 or >= 4 (choose_launch)
                         double g[4];
                         if constexpr (TR::PARK)  // i-face(0) normal: metrics row 0 (rare path)
