@@ -140,6 +140,9 @@ __device__ __forceinline__ double frcp(double d) {
 #ifndef SFV_WALL_FIRST
 #define SFV_WALL_FIRST 1  // edge strips' tasks at the lowest blockIdx (high issue priority)
 #endif
+#ifndef SFV_WALL_OFF
+#define SFV_WALL_OFF 148  // first blockIdx of the edge strips' tasks (one CTA per SM of B200 before them)
+#endif
 #ifndef SFV_GHOST_LEAN
 #define SFV_GHOST_LEAN 1  // S/N wall ghosts: per-lane mode and column decided once per task
 #endif
@@ -454,13 +457,17 @@ __global__ void __launch_bounds__(NT, StageTraits<MODE>::MINW / WPC) stage_kerne
             // the two edge strips' tasks first: the lowest blockIdx take the
             // sub-partitions' high-priority warp slots, and these strips carry the
             // per-row wall-ghost work (profiles/r2e_timeline_strips.txt)
+            // (after the first SFV_WALL_OFF tasks: the first CTA dispatched to
+            // each SM ends late in stages that follow a stage of the same step)
             const int nb = 2 * a.nseg;
-            if (tt < nb) {
-                strip = (tt & 1) ? a.nstrips - 1 : 0;
-                seg = tt >> 1;
+            const int off = ntask1 >= SFV_WALL_OFF + nb ? SFV_WALL_OFF : 0;
+            if (tt >= off && tt < off + nb) {
+                strip = ((tt - off) & 1) ? a.nstrips - 1 : 0;
+                seg = (tt - off) >> 1;
             } else {
-                strip = 1 + (tt - nb) % (a.nstrips - 2);
-                seg = (tt - nb) / (a.nstrips - 2);
+                const int ti = tt < off ? tt : tt - nb;
+                strip = 1 + ti % (a.nstrips - 2);
+                seg = ti / (a.nstrips - 2);
             }
         }
         const int j0 = strip * WOUT;
