@@ -174,9 +174,7 @@ def measured_peak():
         return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
 
 
-# --ns: constant viscosity (Re ~ 2e5 on the unit-length inlet).  The walls stay slip walls: the
-# impulsive Mach-4 start against a no-slip 30-degree ramp is not stable under the inviscid CFL
-# (it fails within a few steps on the C2 grid); the no-slip wall is exercised by tests/test_gpu_ns.py.
+# --ns: constant viscosity (Re ~ 2e5 on the unit-length inlet).
 NS_MU = 1.0e-3
 # Navier-Stokes workload: the C2 grid with a 5-degree ramp and a no-slip adiabatic
 # ramp wall (an impulsive Mach-4 start against a no-slip 30-degree
