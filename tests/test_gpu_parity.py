@@ -160,6 +160,29 @@ def test_va1_limiter_option(sfv_mod, oracle_mod):
         check(g, o, 1e-12)
 
 
+def test_va1_limiter_1000_steps_at_the_oracles_own_sensitivity(sfv_mod, oracle_mod):
+    """VA1 over 1000 steps (reading A-R30's method): the limiter's ab < 0
+    switch makes the scheme discontinuous, so the gate is the oracle's own
+    sensitivity -- the oracle restarted with every density moved by one ulp
+    -- times 5, or 1e-9 where that is larger; 100 steps keep the 1e-10 gate
+    if the oracle's 100-step sensitivity is below it."""
+    ni, nj = 80, 40
+    X, Y = I.ramp_nodes(ni, nj, 30.0)
+    cfg = I.default_config(ni, nj, limiter=I.LIM_VAN_ALBADA)
+    U0 = I.perturbed_state(ni, nj, 9)
+    g, o = run_pair(sfv_mod, oracle_mod, cfg, X, Y, U0, 100)
+    U1 = U0.copy(); U1[..., 0] = np.nextafter(U1[..., 0], np.inf)
+    s = oracle_mod.Oracle(cfg, X, Y); s.set_state(U1); s.step(100)
+    sens100 = state_error(s.get_state(), o.get_state()).max()
+    assert state_error(g.get_state(), o.get_state()).max() <= max(1e-10, 5.0 * sens100)
+    g.step(900); g.sync(); o.step(900); s.step(900)
+    Uo = o.get_state()
+    sens = state_error(s.get_state(), Uo).max()
+    e = state_error(g.get_state(), Uo).max()
+    assert e <= max(1e-9, 5.0 * sens), (e, sens)
+    assert dt_error(g.dt(), o.dt()) <= max(1e-13, 5.0 * dt_error(s.dt(), o.dt()))
+
+
 @pytest.mark.parametrize("bc", [(0, 1, 2, 2), (0, 1, 2, 1), (2, 2, 2, 2), (1, 1, 1, 1), (0, 0, 0, 0),
                                 (2, 1, 0, 2), (1, 2, 2, 0)])
 def test_boundary_combinations(sfv_mod, oracle_mod, bc):
